@@ -1,0 +1,413 @@
+"""NIF shadow-ray visibility benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): synthetic
+multi-object scene, 12 x icosphere(6) + NIF-enabled ground plane =
+983,042 triangles in 13 objects, 1920x1080, 1 spp direct-illumination
+shadow rays, inference only. One step = one NIF visibility pass over the
+frame's shadow rays: phase-1 gather (top-level culling + fp64 T_outer /
+T_inner) -> fused grid encoding + visibility MLP (tcgen05) -> p < 0.5 ->
+per-ray OR. Rays are generated on the GPU by the sample pass (not timed).
+
+value : shadow rays resolved per second, whole job (sum over ranks),
+        rays resident in HBM, L2 flushed (256 MiB write) between steps.
+e2e   : the same through the public API with pinned host buffers
+        (H2D of origins/dirs/tmaxs + D2H of the per-ray bits every step).
+Multi-GPU: one process per GPU (torchrun), each rank owns its own frame
+(sample index = rank): weak scaling, no collective on the inference path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "NIF shadow-ray queries/s per GPU; secondary-ray cast ms/frame vs BVH"
+UNIT = "shadow rays/s"
+WORKLOAD = ("C2: 12x icosphere(6) + NIF plane, 983,042 tris, 13 objects, 1920x1080, "
+            "1 spp point-light shadow rays, inference only")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--train-epochs", type=int, default=0,
+                   help="epochs of GPU training on 1 spp before timing (0 = random init)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile", action="store_true", help="few steps, no clocks / cpu leg")
+    return p.parse_args()
+
+
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    elif args.impl == "ours":
+        torch.cuda.set_device(0)
+    return rank, ws, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def build_workload(args, rank):
+    from paper_2306_07191_b200 import synthetic
+    if args.config == "c1":
+        return synthetic.c1(min(args.width, 256), min(args.height, 256))
+    if args.config == "c3":
+        return synthetic.c3(args.width, args.height)
+    return synthetic.c2(args.width, args.height)
+
+
+def cpu_baseline_leg(scene, model, rays_np, max_rays=20000, budget_s=20.0):
+    """Oracle port of the reference CPU path on a bounded sample, all host
+    threads (gather + encode + row-sequential forward, cmd_bench method:
+    1 warm-up + median)."""
+    from oracle import oracle
+    n = min(len(rays_np[0]), max_rays)
+    o, d, t = (a[:n] for a in rays_np)
+    osc = oracle.OracleScene(scene.pack, scene.epsilon_t)
+    route = scene.nif_route_mask(None)
+    grids = model.host_grids()
+    fams = {}
+    for fam in ("outer", "inner"):
+        hl = model.host_layers(fam)[0]
+        fams[fam] = dict(
+            w=np.concatenate([a.reshape(-1) for a, _ in hl]),
+            b=np.concatenate([bb for _, bb in hl]),
+            dims=[hl[0][0].shape[1]] + [a.shape[0] for a, _ in hl],
+            pos=np.stack([g[f"{fam}_pos"] for g in grids]),
+            dir=np.stack([g[f"{fam}_dir"] for g in grids]),
+            dist=np.stack([g["inner_dist"] for g in grids]) if fam == "inner" else None)
+
+    def one():
+        kind, obj, ray, coord, bvh_occ, _ = oracle.gather(osc, o, d, t, route)
+        occ = bvh_occ.copy()
+        for fam, k, width in (("outer", 0, 4), ("inner", 1, 5)):
+            sel = kind == k
+            if sel.any():
+                f = fams[fam]
+                x = oracle.encode(f["pos"], f["dir"], f["dist"], obj[sel], coord[sel, :width])
+                p = oracle.dense_forward(f["w"], f["b"], f["dims"], x)
+                occ[ray[sel][p[:, 0] < 0.5]] = True
+        return occ
+
+    one()
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while len(times) < 5 and (time.perf_counter() < t_end or len(times) < 1):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    med = float(np.median(times))
+    return {"value": n / med, "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
+            "sample": f"{n} C2 shadow rays (first {n} of the frame), gather+encode+MLP, "
+                      f"median of {len(times)}"}
+
+
+def run_reference(args, rank, ws):
+    """--impl reference: the reference's CPU path (oracle port; the Python
+    reference cannot travel to the GPU box) on the host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2306_07191_b200 import synthetic
+    from paper_2306_07191_b200.nif import NifConfig, init_arrays
+    scene = build_workload(args, rank)
+    # shadow rays from the oracle's own sample pass (same rays as ours)
+    osc = oracle.OracleScene(scene.pack, scene.epsilon_t)
+    cum, kind, data = scene.light_tables()
+    sp = oracle.sample_pass(osc, scene.camera, cum, kind, data, scene.seed, 0)
+    cos = np.einsum("ij,ij->i", sp["normal"], sp["ldir"])
+    cast = sp["hit"] & (cos > 0) & (sp["pdf"] > 0)
+    rays = (sp["point"][cast], sp["ldir"][cast], sp["tmax"][cast])
+
+    class HostModel:
+        def __init__(self):
+            outer, inner, grids, _, _ = init_arrays(NifConfig(seed=0), scene.n_objects)
+            self._l = {"outer": outer[0], "inner": inner[0]}
+            self._g = grids
+
+        def host_layers(self, fam):
+            return [self._l[fam]]
+
+        def host_grids(self):
+            return self._g
+
+    model = HostModel()
+    n = min(len(rays[0]), 20000)
+    base = cpu_baseline_leg(scene, model, rays, max_rays=n, budget_s=10.0)
+    # steps: each step is the same bounded sample, timed individually
+    from bench import cpu_baseline_leg as _leg  # noqa: F401
+    per = n / base["value"]
+    value = base["value"]
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "rays_per_frame": int(len(rays[0])),
+                       "sample_rays_per_step": n},
+            "cpu_baseline": base,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    rank, ws, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, ws)
+        return
+    import torch
+    from paper_2306_07191_b200 import NifBackend, _lib, build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import (VisibilityEngine, sample_pass_dev,
+                                                shadow_rays_dev)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    scene = build_workload(args, rank)
+    data = sample_pass_dev(scene, scene.camera, rank, scene.seed)
+    _, o, d, t = shadow_rays_dev(data, require_emit=False)
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0), scene)
+    if args.train_epochs > 0:
+        from paper_2306_07191_b200 import train as tr
+        samples = tr.collect_samples_dev(scene, spp=1, seed=scene.seed)
+        tr.train(model, samples, epochs=args.train_epochs)
+    eng = VisibilityEngine(scene, model, n)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    graph = eng.capture(n)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # --- device-resident timed loop -----------------------------------------
+    for _ in range(args.warmup):
+        graph.replay()
+    barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    with clocks:
+        barrier()
+        for e0, e1 in evs:
+            flush.fill_(1.0)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+        barrier()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    ms_local = float(np.sum(step_ms))
+    counts = eng.counts()
+
+    # --- per-kernel breakdown (eager, events on the launching stream) -------
+    L = _lib.lib()
+    b = eng.buf
+    vo, vi = eng._family_views()
+    kt = {}
+    reps = max(3, min(args.steps, 10))
+
+    def timed(name, fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        acc = 0.0
+        for _ in range(reps):
+            flush.fill_(1.0)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            acc += e0.elapsed_time(e1)
+        kt[name] = acc / reps
+
+    from paper_2306_07191_b200.pipeline import gather_dev
+    sp = _lib.stream_ptr()
+    timed("gather", lambda: gather_dev(eng.ds, eng.route, eng.origins, eng.dirs, eng.tmaxs, n, b))
+    timed("query_outer", lambda: L.nif_query_dev(
+        vo, b.outer_obj.data_ptr(), b.outer_ray.data_ptr(), b.outer_coord.data_ptr(), None,
+        b.counts.data_ptr(), b.cap, eng.occ.data_ptr(), None, 0, sp))
+    timed("query_inner", lambda: L.nif_query_dev(
+        vi, b.inner_obj.data_ptr(), b.inner_ray.data_ptr(), b.inner_coord.data_ptr(),
+        b.inner_r.data_ptr(), b.counts.data_ptr() + 8, b.cap, eng.occ.data_ptr(), None, 0, sp))
+    bvh_out = torch.empty(n, dtype=torch.uint8, device=dev)
+    timed("bvh_anyhit", lambda: L.nif_bvh_occluded_dev(
+        eng.ds.view, o.data_ptr(), d.data_ptr(), t.data_ptr(), n, bvh_out.data_ptr(), sp))
+
+    # --- e2e through the public API with pinned host buffers ----------------
+    ho = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    hd = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    ht = torch.empty(n, dtype=torch.float64).pin_memory()
+    ho.copy_(o)
+    hd.copy_(d)
+    ht.copy_(t)
+    hocc = torch.empty(n, dtype=torch.uint8).pin_memory()
+
+    def e2e_step():
+        eng.origins[:n].copy_(ho, non_blocking=True)
+        eng.dirs[:n].copy_(hd, non_blocking=True)
+        eng.tmaxs[:n].copy_(ht, non_blocking=True)
+        graph.replay()
+        hocc.copy_(eng.occ[:n], non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+    for e0, e1 in e_evs:
+        flush.fill_(1.0)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+    barrier()
+    e2e_ms_local = float(np.sum([e0.elapsed_time(e1) for e0, e1 in e_evs]))
+
+    # --- reduce over ranks (max time) ---------------------------------------
+    ms, e2e_ms = ms_local, e2e_ms_local
+    n_total = n
+    if ws > 1:
+        tt = torch.tensor([ms_local, e2e_ms_local], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, e2e_ms = float(tt[0]), float(tt[1])
+        nn = torch.tensor([n], device=dev, dtype=torch.int64)
+        torch.distributed.all_reduce(nn)
+        n_total = int(nn)
+    if rank != 0:
+        return
+    value = n_total * args.steps / (ms / 1e3)
+    e2e_value = n_total * args.steps / (e2e_ms / 1e3)
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+    n_outer, n_inner = int(counts[0]), int(counts[1])
+    cfgm = model.config
+    fl_o = 2 * (cfgm.outer.input_dim * cfgm.outer.hidden_width
+                + (cfgm.outer.hidden_layers - 1) * cfgm.outer.hidden_width ** 2
+                + cfgm.outer.hidden_width)
+    fl_i = 2 * (cfgm.inner.input_dim * cfgm.inner.hidden_width
+                + (cfgm.inner.hidden_layers - 1) * cfgm.inner.hidden_width ** 2
+                + cfgm.inner.hidden_width)
+    gather_bytes = 56 * n + 1 * n + 28 * (n_outer + n_inner)
+    dominant = max(("gather", "query_outer", "query_inner"), key=lambda k: kt[k])
+    if dominant == "gather":
+        roof = {"bound": "hbm", "kernel": "nif_gather (count+scan+write)",
+                "achieved": gather_bytes / (kt["gather"] / 1e3) / 1e9,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    else:
+        nrec = n_outer if dominant == "query_outer" else n_inner
+        fl = fl_o if dominant == "query_outer" else fl_i
+        roof = {"bound": "tensor", "kernel": f"query_tc_kernel ({dominant})",
+                "achieved": nrec * fl / (kt[dominant] / 1e3) / 1e12,
+                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["peak_source"] = "MEASURED_PEAKS.json (burst)"
+
+    cpu = None
+    if not args.no_cpu_baseline and not args.profile:
+        try:
+            rays_np = (o[:20000].cpu().numpy(), d[:20000].cpu().numpy(),
+                       t[:20000].cpu().numpy())
+            cpu = cpu_baseline_leg(scene, model, rays_np)
+        except Exception as e:  # the checker must never hide the main number
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp16-mma/fp32-acc (fp64 gather)",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "rays_per_frame_per_gpu": n, "outer_records": n_outer,
+                   "inner_records": n_inner, "model": "NifConfig() defaults (R 256/128)",
+                   "trained_epochs": args.train_epochs, "l2": "flushed (256 MiB write) per step",
+                   "parallelism": f"{ws} independent frames (sample index = rank)"},
+        "frame_ms": ms / args.steps,
+        "bvh_ms_per_frame": kt["bvh_anyhit"],
+        "kernel_ms": kt,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n)},
+        "gpu_launches": args.steps * 6,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

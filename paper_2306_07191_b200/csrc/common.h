@@ -1,0 +1,20 @@
+// Small host helpers shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "status.h"
+
+namespace nif {
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Launch errors are reported synchronously (configuration errors); device
+// faults surface at the caller's next synchronisation as usual.
+inline int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(NIF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return NIF_OK;
+}
+
+}  // namespace nif

@@ -1,0 +1,580 @@
+// Phase 2 of the split visibility pass: per-record grid encoding, the
+// visibility MLP, the p < 0.5 threshold and the per-ray OR
+// (nif.py:467-483 infer_records, renderer.py:675-683 PredictorBackend).
+//
+// Two implementations behind nif_query_dev:
+//  * query_tc_kernel  -- persistent, 128 records per tile (M = 128 rows of
+//    tcgen05.mma kind::f16), features/activations staged fp16 in shared
+//    memory in the UMMA canonical K-major layout, fp32 accumulators in TMEM,
+//    biases folded into the GEMMs through a constant-one input column, the
+//    N=1 head run as an N=16 MMA. Weights live in shared memory for the
+//    kernel's lifetime; latent tables are fp16 (nif_fast_pack_dev).
+//  * query_simt_kernel -- fp32 CUDA-core kernel over the fp32 master
+//    tables; the numerical anchor for the tensor-core path and the path for
+//    configurations the tensor-core kernel does not cover (per-object MLPs,
+//    the geometry head, very wide inputs).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+#include "nif_b200.h"
+#include "status.h"
+#include "tc.cuh"
+
+namespace nif {
+namespace {
+
+constexpr float kSlope = 0.01f;  // mlp.py:17 HIDDEN_SLOPE
+constexpr int kTileRows = 128;
+constexpr int kK1 = 16;          // padded layer-1 K (features + bias column)
+
+// ---------------------------------------------------------------------------
+// fast blob layout
+// ---------------------------------------------------------------------------
+
+struct FastLayout {
+  int W, L, in_dim, Kp, NP, NPd, R, Rd, N, Nd, n_obj;
+  size_t off_w1, off_hidden, off_head, w_bytes;
+  size_t off_pos, off_dir, off_dist, total;
+  int tmem_cols;
+  bool tc_ok;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 255) / 256 * 256; }
+
+__host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
+  FastLayout l{};
+  l.in_dim = f.dims[0];
+  l.W = f.dims[1];
+  l.L = f.n_layers - 1;
+  l.Kp = ((l.W + 1) + 15) / 16 * 16;
+  l.N = f.N;
+  l.Nd = f.Nd;
+  l.NP = f.N <= 4 ? 4 : 8;
+  l.NPd = 4;
+  l.R = f.R;
+  l.Rd = f.Rd;
+  l.n_obj = f.n_obj;
+  l.off_w1 = 0;
+  l.off_hidden = l.off_w1 + (size_t)l.W * kK1 * 2;
+  l.off_head = l.off_hidden + (size_t)(l.L > 0 ? l.L - 1 : 0) * l.W * l.Kp * 2;
+  l.w_bytes = l.off_head + (size_t)16 * l.Kp * 2;
+  l.off_pos = al16(l.w_bytes);
+  const size_t tab = (size_t)f.n_obj * f.R * f.R * l.NP * 2;
+  l.off_dir = al16(l.off_pos + tab);
+  l.off_dist = al16(l.off_dir + tab);
+  const size_t dtab = f.family == NIF_FAMILY_INNER ? (size_t)f.n_obj * f.Rd * l.NPd * 2 : 0;
+  l.total = al16(l.off_dist + dtab);
+  int cols = l.W + 16;
+  l.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  bool hidden_same = true;
+  for (int i = 1; i < f.n_layers; ++i) hidden_same = hidden_same && f.dims[i] == l.W;
+  const bool inst = (f.family == NIF_FAMILY_OUTER && (f.N == 2 || f.N == 3 || f.N == 4)) ||
+                    (f.family == NIF_FAMILY_INNER &&
+                     ((f.N == 5 && (f.Nd == 3 || f.Nd == 4)) || (f.N == 4 && f.Nd == 3)));
+  l.tc_ok = inst && f.n_heads == 1 && f.sigmoid_head == 1 && f.dims[f.n_layers] == 1 &&
+            l.L >= 1 && hidden_same && l.W % 16 == 0 && l.W >= 16 && l.W <= 240 &&
+            l.in_dim + 1 <= kK1;
+  return l;
+}
+
+// byte offset of element (r, k) in a K-major canonical tile with K = kp
+__host__ __device__ inline size_t canon_off(int r, int k, int kp) {
+  return (size_t)(r >> 3) * (kp * 16) + (size_t)(k >> 3) * 128 + (size_t)(r & 7) * 16 +
+         (size_t)(k & 7) * 2;
+}
+
+// weights -> fp16 canonical tiles with the bias folded into column `in`
+__global__ void pack_weights_kernel(nif_family_view f, FastLayout l, uint8_t* blob) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n1 = l.W * kK1;
+  const int nh = (l.L - 1) * l.W * l.Kp;
+  const int nhead = 16 * l.Kp;
+  if (idx >= n1 + nh + nhead) return;
+  float val = 0.f;
+  size_t off;
+  if (idx < n1) {
+    const int r = idx / kK1, k = idx % kK1;
+    const int nin = f.dims[0];
+    if (k < nin) val = f.w[(size_t)r * nin + k];
+    else if (k == nin) val = f.b[r];
+    off = l.off_w1 + canon_off(r, k, kK1);
+  } else if (idx < n1 + nh) {
+    const int j = idx - n1;
+    const int layer = j / (l.W * l.Kp);  // hidden tile index -> dense layer layer+1
+    const int rem = j % (l.W * l.Kp);
+    const int r = rem / l.Kp, k = rem % l.Kp;
+    size_t wo = (size_t)f.dims[0] * l.W + (size_t)layer * l.W * l.W;
+    size_t bo = (size_t)l.W * (layer + 1);
+    if (k < l.W) val = f.w[wo + (size_t)r * l.W + k];
+    else if (k == l.W) val = f.b[bo + r];
+    off = l.off_hidden + (size_t)layer * l.W * l.Kp * 2 + canon_off(r, k, l.Kp);
+  } else {
+    const int j = idx - n1 - nh;
+    const int r = j / l.Kp, k = j % l.Kp;
+    size_t wo = (size_t)f.dims[0] * l.W + (size_t)(l.L - 1) * l.W * l.W;
+    size_t bo = (size_t)l.W * l.L;
+    if (r == 0 && k < l.W) val = f.w[wo + k];
+    else if (r == 0 && k == l.W) val = f.b[bo];
+    off = l.off_head + canon_off(r, k, l.Kp);
+  }
+  *reinterpret_cast<__half*>(blob + off) = __float2half_rn(val);
+}
+
+// fp32 master latents -> fp16 tables padded to NP latents per cell
+__global__ void pack_tables_kernel(nif_family_view f, FastLayout l, uint8_t* blob) {
+  const int64_t cells2 = (int64_t)l.n_obj * l.R * l.R;
+  const int64_t cells1 = f.family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * l.Rd : 0;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < 2 * cells2) {
+    const bool is_dir = idx >= cells2;
+    const int64_t c = is_dir ? idx - cells2 : idx;
+    const float* src = (is_dir ? f.dir : f.pos) + c * l.N;
+    __half* dst = reinterpret_cast<__half*>(blob + (is_dir ? l.off_dir : l.off_pos)) + c * l.NP;
+    for (int k = 0; k < l.NP; ++k) dst[k] = __float2half_rn(k < l.N ? src[k] : 0.f);
+  } else if (idx < 2 * cells2 + cells1) {
+    const int64_t c = idx - 2 * cells2;
+    const float* src = f.dist + c * l.Nd;
+    __half* dst = reinterpret_cast<__half*>(blob + l.off_dist) + c * l.NPd;
+    for (int k = 0; k < l.NPd; ++k) dst[k] = __float2half_rn(k < l.Nd ? src[k] : 0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// interpolation helpers (fp32 coordinates, cell-centred, u wraps, v clamps)
+// ---------------------------------------------------------------------------
+
+struct Bil {
+  int iu0, iu1, iv0, iv1;
+  float w00, w01, w10, w11;
+};
+
+__device__ __forceinline__ Bil bilinear(float u, float v, int R) {
+  Bil b;
+  u = u - floorf(u);  // wrap period 1 in u == wrap period R in the index
+  const float xu = u * (float)R - 0.5f;
+  const float fu = floorf(xu);
+  const float wu = xu - fu;
+  int i0 = (int)fu, i1 = i0 + 1;
+  if (i0 < 0) i0 += R;
+  if (i1 >= R) i1 -= R;
+  const float xv = v * (float)R - 0.5f;
+  const float fv = floorf(xv);
+  const float wv = xv - fv;
+  int j0 = (int)fv, j1 = j0 + 1;
+  j0 = min(max(j0, 0), R - 1);
+  j1 = min(max(j1, 0), R - 1);
+  b.iu0 = i0;
+  b.iu1 = i1;
+  b.iv0 = j0;
+  b.iv1 = j1;
+  b.w00 = (1.f - wu) * (1.f - wv);
+  b.w01 = (1.f - wu) * wv;
+  b.w10 = wu * (1.f - wv);
+  b.w11 = wu * wv;
+  return b;
+}
+
+struct Lin {
+  int i0, i1;
+  float w;
+};
+
+__device__ __forceinline__ Lin linear1(float x, int R) {
+  const float xc = x * (float)R - 0.5f;
+  const float f0 = floorf(xc);
+  Lin l;
+  l.w = xc - f0;
+  int i0 = (int)f0, i1 = i0 + 1;
+  l.i0 = min(max(i0, 0), R - 1);
+  l.i1 = min(max(i1, 0), R - 1);
+  return l;
+}
+
+// ---------------------------------------------------------------------------
+// SIMT fp32 query kernel
+// ---------------------------------------------------------------------------
+
+constexpr int kSimtMaxIn = 64;
+constexpr int kSimtMaxW = 256;
+
+__global__ void __launch_bounds__(128)
+query_simt_kernel(nif_family_view f, const int32_t* __restrict__ obj,
+                  const int32_t* __restrict__ ray, const float* __restrict__ coord4,
+                  const float* __restrict__ rr, const int64_t* __restrict__ count, int64_t cap,
+                  uint8_t* __restrict__ occ, float* __restrict__ logits) {
+  const int64_t n = min(*count, cap);
+  float x[kSimtMaxIn];
+  float a[kSimtMaxW], b[kSimtMaxW];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int o = obj[j];
+    const float4 c = reinterpret_cast<const float4*>(coord4)[j];
+    const size_t g2 = (size_t)f.R * f.R * f.N;
+    const float* gp = f.pos + (size_t)o * g2;
+    const float* gd = f.dir + (size_t)o * g2;
+    Bil bp = bilinear(c.x, c.y, f.R), bd = bilinear(c.z, c.w, f.R);
+    for (int k = 0; k < f.N; ++k) {
+      x[k] = bp.w00 * gp[((size_t)bp.iu0 * f.R + bp.iv0) * f.N + k] +
+             bp.w01 * gp[((size_t)bp.iu0 * f.R + bp.iv1) * f.N + k] +
+             bp.w10 * gp[((size_t)bp.iu1 * f.R + bp.iv0) * f.N + k] +
+             bp.w11 * gp[((size_t)bp.iu1 * f.R + bp.iv1) * f.N + k];
+      x[f.N + k] = bd.w00 * gd[((size_t)bd.iu0 * f.R + bd.iv0) * f.N + k] +
+                   bd.w01 * gd[((size_t)bd.iu0 * f.R + bd.iv1) * f.N + k] +
+                   bd.w10 * gd[((size_t)bd.iu1 * f.R + bd.iv0) * f.N + k] +
+                   bd.w11 * gd[((size_t)bd.iu1 * f.R + bd.iv1) * f.N + k];
+    }
+    if (f.family == NIF_FAMILY_INNER) {
+      const Lin l = linear1(rr[j], f.Rd);
+      const float* gr = f.dist + (size_t)o * f.Rd * f.Nd;
+      for (int k = 0; k < f.Nd; ++k)
+        x[2 * f.N + k] = (1.f - l.w) * gr[(size_t)l.i0 * f.Nd + k] + l.w * gr[(size_t)l.i1 * f.Nd + k];
+    }
+    const int head = f.n_heads > 1 ? o : 0;
+    const float* W = f.w + (size_t)head * f.w_stride;
+    const float* B = f.b + (size_t)head * f.b_stride;
+    for (int k = 0; k < f.dims[0]; ++k) a[k] = x[k];
+    int wo = 0, bo = 0;
+    for (int layer = 0; layer < f.n_layers; ++layer) {
+      const int nin = f.dims[layer], nout = f.dims[layer + 1];
+      for (int q = 0; q < nout; ++q) {
+        float acc = __ldg(B + bo + q);
+        const float* wr = W + wo + q * nin;
+        for (int k = 0; k < nin; ++k) acc = fmaf(__ldg(wr + k), a[k], acc);
+        b[q] = (layer < f.n_layers - 1) ? (acc > 0.f ? acc : kSlope * acc) : acc;
+      }
+      wo += nin * nout;
+      bo += nout;
+      for (int q = 0; q < nout; ++q) a[q] = b[q];
+    }
+    const int od = f.dims[f.n_layers];
+    if (logits)
+      for (int q = 0; q < od; ++q) logits[j * od + q] = a[q];
+    if (occ && f.sigmoid_head == 1 && a[0] < 0.f) occ[ray[j]] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 fused query kernel
+// ---------------------------------------------------------------------------
+
+struct TcArgs {
+  const uint8_t* blob;
+  FastLayout l;
+  const int32_t* obj;
+  const int32_t* ray;
+  const float* coord4;
+  const float* rr;
+  const int64_t* count;
+  int64_t cap;
+  uint8_t* occ;
+  float* logits;
+};
+
+__device__ __forceinline__ void store_chunk(uint8_t* base, int row, int chunk, int kp,
+                                            uint4 v) {
+  *reinterpret_cast<uint4*>(base + (size_t)(row >> 3) * (kp * 16) + chunk * 128 +
+                            (row & 7) * 16) = v;
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+template <int NP>
+__device__ __forceinline__ void corner(const __half* t, float w, float* acc) {
+  if constexpr (NP == 4) {
+    const uint2 q = __ldg(reinterpret_cast<const uint2*>(t));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&q.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&q.y));
+    acc[0] = fmaf(w, a.x, acc[0]);
+    acc[1] = fmaf(w, a.y, acc[1]);
+    acc[2] = fmaf(w, b.x, acc[2]);
+    acc[3] = fmaf(w, b.y, acc[3]);
+  } else {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(t));
+    const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u[i]));
+      acc[2 * i] = fmaf(w, a.x, acc[2 * i]);
+      acc[2 * i + 1] = fmaf(w, a.y, acc[2 * i + 1]);
+    }
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ void lookup16(const __half* tab, int R, float u, float v, float* acc) {
+  const Bil b = bilinear(u, v, R);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) acc[i] = 0.f;
+  corner<NP>(tab + ((size_t)b.iu0 * R + b.iv0) * NP, b.w00, acc);
+  corner<NP>(tab + ((size_t)b.iu0 * R + b.iv1) * NP, b.w01, acc);
+  corner<NP>(tab + ((size_t)b.iu1 * R + b.iv0) * NP, b.w10, acc);
+  corner<NP>(tab + ((size_t)b.iu1 * R + b.iv1) * NP, b.w11, acc);
+}
+
+template <int N, int ND>
+__global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
+  constexpr int NP = N <= 4 ? 4 : 8;
+  constexpr bool INNER = ND > 0;
+  constexpr int IN = 2 * N + ND;
+  static_assert(IN + 1 <= 16, "layer-1 inputs plus bias must fit K = 16");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const FastLayout& l = a.l;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int W = l.W, Kp = l.Kp, L = l.L;
+  const size_t w_al = al16(l.w_bytes);
+  uint8_t* sW = smem;
+  uint8_t* sA1 = smem + w_al;
+  uint8_t* sA2 = sA1 + kTileRows * kK1 * 2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA2 + (size_t)kTileRows * Kp * 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  // weights -> smem (resident for the kernel's lifetime)
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sW);
+    for (size_t i = tid; i < l.w_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  // constant tail of the activation tile: column W = 1 (bias), rest 0
+  for (int c = W / 8; c < Kp / 8; ++c) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c == W / 8) v.x = h2u(__halves2half2(__float2half_rn(1.f), __float2half_rn(0.f)));
+    store_chunk(sA2, tid, c, Kp, v);
+  }
+  if (tid == 0) {
+    tc::mbar_init(bar, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc_dyn(tslot, l.tmem_cols);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tslot;
+  const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+
+  const uint32_t sA1a = tc::smem_u32(sA1), sA2a = tc::smem_u32(sA2), sWa = tc::smem_u32(sW);
+  const uint64_t dA1 = tc::smem_desc(sA1a, 128, kK1 * 16);
+  const uint64_t dW1 = tc::smem_desc(sWa + (uint32_t)l.off_w1, 128, kK1 * 16);
+  const uint32_t idW = tc::idesc_f16(W), id16 = tc::idesc_f16(16);
+  const __half2 slope2 = __float2half2_rn(kSlope);
+
+  const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
+  const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
+  const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
+  const size_t g2 = (size_t)l.R * l.R * NP;
+
+  const int64_t n = min(*a.count, a.cap);
+  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t row = tile * kTileRows + tid;
+    const bool valid = row < n;
+    // ---- encode: 16 fp16 inputs (features, 1, zeros) ------------------------
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = 0.f;
+    if (valid) {
+      const int o = a.obj[row];
+      const float4 c = reinterpret_cast<const float4*>(a.coord4)[row];
+      float acc[NP];
+      lookup16<NP>(tpos + (size_t)o * g2, l.R, c.x, c.y, acc);
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = acc[i];
+      lookup16<NP>(tdir + (size_t)o * g2, l.R, c.z, c.w, acc);
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[N + i] = acc[i];
+      if constexpr (INNER) {
+        const Lin li = linear1(a.rr[row], l.Rd);
+        const __half* g = tdist + (size_t)o * l.Rd * 4;
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        corner<4>(g + (size_t)li.i0 * 4, 1.f - li.w, d);
+        corner<4>(g + (size_t)li.i1 * 4, li.w, d);
+#pragma unroll
+        for (int i = 0; i < ND; ++i) x[2 * N + i] = d[i];
+      }
+    }
+    x[IN] = 1.f;
+    {
+      uint4 v0, v1;
+      v0.x = h2u(__floats2half2_rn(x[0], x[1]));
+      v0.y = h2u(__floats2half2_rn(x[2], x[3]));
+      v0.z = h2u(__floats2half2_rn(x[4], x[5]));
+      v0.w = h2u(__floats2half2_rn(x[6], x[7]));
+      v1.x = h2u(__floats2half2_rn(x[8], x[9]));
+      v1.y = h2u(__floats2half2_rn(x[10], x[11]));
+      v1.z = h2u(__floats2half2_rn(x[12], x[13]));
+      v1.w = h2u(__floats2half2_rn(x[14], x[15]));
+      store_chunk(sA1, tid, 0, kK1, v0);
+      store_chunk(sA1, tid, 1, kK1, v1);
+    }
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after_sync();
+      tc::mma_f16(tbase, dA1, dW1, idW, 0);
+      tc::mma_commit(bar);
+    }
+    tc::mbar_wait(bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+    for (int layer = 1; layer <= L; ++layer) {
+      // epilogue: TMEM accumulators -> leaky ReLU (fp16) -> next A tile
+      for (int cc = 0; cc < W / 16; ++cc) {
+        float v[16];
+        tc::tmem_ld16(lane_base + cc * 16, v);
+        uint32_t h[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __half2 q = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+          q = __hmax2(q, __hmul2(q, slope2));
+          h[i] = h2u(q);
+        }
+        store_chunk(sA2, tid, 2 * cc, Kp, make_uint4(h[0], h[1], h[2], h[3]));
+        store_chunk(sA2, tid, 2 * cc + 1, Kp, make_uint4(h[4], h[5], h[6], h[7]));
+      }
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const int steps = Kp / 16;
+        if (layer < L) {
+          const uint32_t wb = sWa + (uint32_t)(l.off_hidden + (size_t)(layer - 1) * W * Kp * 2);
+          for (int s = 0; s < steps; ++s)
+            tc::mma_f16(tbase, tc::smem_desc(sA2a + s * 256, 128, Kp * 16),
+                        tc::smem_desc(wb + s * 256, 128, Kp * 16), idW, s > 0);
+        } else {
+          const uint32_t wb = sWa + (uint32_t)l.off_head;
+          for (int s = 0; s < steps; ++s)
+            tc::mma_f16(tbase + W, tc::smem_desc(sA2a + s * 256, 128, Kp * 16),
+                        tc::smem_desc(wb + s * 256, 128, Kp * 16), id16, s > 0);
+        }
+        tc::mma_commit(bar);
+      }
+      tc::mbar_wait(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+    }
+    const float logit = tc::tmem_ld1(lane_base + W);
+    if (valid) {
+      if (a.logits) a.logits[row] = logit;
+      if (a.occ && logit < 0.f) a.occ[a.ray[row]] = 1;
+    }
+    tc::fence_before_sync();
+  }
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, l.tmem_cols);
+}
+
+__global__ void occ_init_kernel(const uint8_t* __restrict__ src, int64_t n,
+                                uint8_t* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src ? src[i] : 0;
+}
+
+int g_sm_count = 0;
+
+int sm_count() {
+  if (g_sm_count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+
+size_t tc_smem_bytes(const FastLayout& l) {
+  return al16(l.w_bytes) + (size_t)kTileRows * kK1 * 2 + (size_t)kTileRows * l.Kp * 2 + 64;
+}
+
+template <int N, int ND>
+int launch_tc(const TcArgs& a, cudaStream_t st) {
+  const size_t smem = tc_smem_bytes(a.l);
+  auto kern = query_tc_kernel<N, ND>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return check_launch("query_tc: smem attribute");
+  const int per_sm_tmem = 512 / a.l.tmem_cols;
+  const int per_sm_smem = (int)((227 * 1024) / (smem + 1024));
+  int per_sm = per_sm_tmem < per_sm_smem ? per_sm_tmem : per_sm_smem;
+  if (per_sm > 8) per_sm = 8;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (grid > max_tiles) grid = max_tiles;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 128, smem, st>>>(a);
+  return check_launch("nif_query_dev(tcgen05)");
+}
+
+}  // namespace
+}  // namespace nif
+
+using namespace nif;
+
+extern "C" size_t nif_fast_pack_bytes(const nif_family_view* f) {
+  return make_layout(*f).total;
+}
+
+extern "C" int nif_fast_pack_dev(const nif_family_view* f, void* blob, void* stream) {
+  const FastLayout l = make_layout(*f);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(blob, 0, l.total, st);
+  if (l.tc_ok) {
+    const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp;
+    pack_weights_kernel<<<(nw + 255) / 256, 256, 0, st>>>(*f, l, (uint8_t*)blob);
+  }
+  const int64_t cells = 2 * (int64_t)l.n_obj * l.R * l.R +
+                        (f->family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * l.Rd : 0);
+  pack_tables_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, st>>>(*f, l, (uint8_t*)blob);
+  return check_launch("nif_fast_pack_dev");
+}
+
+extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const int32_t* ray,
+                             const float* coord4, const float* r, const int64_t* count_dev,
+                             int64_t capacity, uint8_t* occ_ray, float* logits, int32_t impl,
+                             void* stream) {
+  if (capacity <= 0) return NIF_OK;
+  if (f->family == NIF_FAMILY_INNER && r == nullptr)
+    return fail(NIF_ERR_VALUE, "inner queries need the radial coordinate");
+  cudaStream_t st = (cudaStream_t)stream;
+  const FastLayout l = make_layout(*f);
+  const bool want_tc = impl == NIF_IMPL_TCGEN05 || (impl == NIF_IMPL_AUTO && l.tc_ok && f->fast);
+  if (want_tc) {
+    if (!l.tc_ok)
+      return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernel");
+    if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
+    TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
+             logits};
+    if (f->family == NIF_FAMILY_OUTER && f->N == 3) return launch_tc<3, 0>(a, st);
+    if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 3) return launch_tc<5, 3>(a, st);
+    if (f->family == NIF_FAMILY_OUTER && f->N == 2) return launch_tc<2, 0>(a, st);
+    if (f->family == NIF_FAMILY_OUTER && f->N == 4) return launch_tc<4, 0>(a, st);
+    if (f->family == NIF_FAMILY_INNER && f->N == 4 && f->Nd == 3) return launch_tc<4, 3>(a, st);
+    if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 4) return launch_tc<5, 4>(a, st);
+    return fail(NIF_ERR_UNSUPPORTED, "no tcgen05 instantiation for N=%d Nd=%d", f->N, f->Nd);
+  }
+  if (f->dims[0] > kSimtMaxIn) return fail(NIF_ERR_UNSUPPORTED, "input width above %d", kSimtMaxIn);
+  for (int i = 1; i <= f->n_layers; ++i)
+    if (f->dims[i] > kSimtMaxW) return fail(NIF_ERR_UNSUPPORTED, "width above %d", kSimtMaxW);
+  int64_t blocks = (capacity + 127) / 128;
+  const int64_t max_blocks = (int64_t)sm_count() * 16;
+  if (blocks > max_blocks) blocks = max_blocks;
+  query_simt_kernel<<<(unsigned)blocks, 128, 0, st>>>(*f, obj, ray, coord4, r, count_dev,
+                                                      capacity, occ_ray, logits);
+  return check_launch("nif_query_dev(simt)");
+}
+
+extern "C" int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray,
+                                void* stream) {
+  if (n <= 0) return NIF_OK;
+  occ_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(bvh_occ, n,
+                                                                                  occ_ray);
+  return check_launch("nif_occ_init_dev");
+}

@@ -1,0 +1,502 @@
+// fp64 ray work: phase-1 gather, per-record labels, the two-level BVH
+// comparator and shadow-ray generation. Compiled with -fmad=false (see
+// geom.cuh): every result here is bit-exact against the reference's numba
+// kernels, which is what the parity tests assert.
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+#include "geom.cuh"
+#include "nif_b200.h"
+#include "status.h"
+
+namespace nif {
+namespace {
+
+constexpr int kGatherThreads = 128;
+
+struct RayIn {
+  double ox, oy, oz, dx, dy, dz, tmax;
+};
+
+__device__ __forceinline__ RayIn load_ray(const double* __restrict__ o,
+                                          const double* __restrict__ d,
+                                          const double* __restrict__ tm, int64_t i) {
+  RayIn r;
+  r.ox = o[i * 3 + 0];
+  r.oy = o[i * 3 + 1];
+  r.oz = o[i * 3 + 2];
+  r.dx = d[i * 3 + 0];
+  r.dy = d[i * 3 + 1];
+  r.dz = d[i * 3 + 2];
+  r.tmax = tm[i];
+  return r;
+}
+
+// One candidate classification, shared by both gather passes.
+// bvh.py:801-898: candidate <=> (n_obj == 1, the root is a leaf) or the
+// object's box passes _window_hit(-tol, tmax); by slab monotonicity this is
+// exactly the reference's top-level DFS (ancestor intervals contain the
+// leaf's). Returns 0 none, 1 outer, 2 inner, 3 routed-away candidate.
+struct Classified {
+  int kind;
+  double t0;
+};
+
+__device__ __forceinline__ Classified classify(const RayIn& r, const double* box, int n_obj,
+                                               double tol) {
+  const Hit3 h = ray_aabb(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, box[0], box[1], box[2], box[3],
+                          box[4], box[5]);
+  if (n_obj > 1 && !(h.hit && h.t0 <= r.tmax && h.t1 >= -tol)) return {0, 0.0};
+  if (box_contains(r.ox, r.oy, r.oz, box, box + 3, tol)) return {2, 0.0};
+  if (h.hit && h.t0 > 0.0 && h.t0 < r.tmax) return {1, h.t0};
+  return {0, 0.0};
+}
+
+// Pass A: per-ray record counts (outer << 32 | inner) and the hybrid
+// any-hit for objects routed to their own trees.
+__global__ void __launch_bounds__(kGatherThreads)
+gather_count_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
+                    const double* __restrict__ o, const double* __restrict__ d,
+                    const double* __restrict__ tm, int64_t n, uint64_t* __restrict__ cnt,
+                    uint8_t* __restrict__ bvh_occ) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const RayIn r = load_ray(o, d, tm, i);
+  uint32_t n_out = 0, n_in = 0;
+  bool occ = false;
+  for (int k = 0; k < s.n_obj; ++k) {
+    const int ob = __ldg(s.t_order + k);
+    const double* box = s.obox + (size_t)ob * 6;
+    const Classified c = classify(r, box, s.n_obj, s.tol);
+    if (c.kind == 0) continue;
+    const bool to_net = __ldg(route + ob) == 1;
+    if (to_net) {
+      if (c.kind == 1) ++n_out;
+      else ++n_in;
+    } else if (!occ) {
+      occ = occluded_in_object(s.nodes, s.tris, __ldg(s.roots + ob), r.ox, r.oy, r.oz, r.dx,
+                               r.dy, r.dz, s.eps, r.tmax);
+    }
+  }
+  cnt[i] = ((uint64_t)n_out << 32) | (uint64_t)n_in;
+  bvh_occ[i] = occ ? 1 : 0;
+}
+
+__global__ void gather_totals_kernel(const uint64_t* __restrict__ cnt,
+                                     const uint64_t* __restrict__ off, int64_t n,
+                                     int64_t* __restrict__ counts) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    uint64_t t = n > 0 ? off[n - 1] + cnt[n - 1] : 0;
+    counts[0] = (int64_t)(t >> 32);
+    counts[1] = (int64_t)(t & 0xffffffffu);
+    counts[2] = counts[0] + counts[1];
+    counts[3] = 0;
+  }
+}
+
+// Pass B: records at the scanned offsets, reference order within a ray.
+__global__ void __launch_bounds__(kGatherThreads)
+gather_write_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
+                    const double* __restrict__ o, const double* __restrict__ d,
+                    const double* __restrict__ tm, int64_t n, const uint64_t* __restrict__ off,
+                    nif_gather_out out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int deg_count = 0;
+  if (i < n) {
+    const RayIn r = load_ray(o, d, tm, i);
+    const uint64_t base = off[i];
+    int64_t jo = (int64_t)(base >> 32);
+    int64_t ji = (int64_t)(base & 0xffffffffu);
+    int64_t jt = jo + ji;
+    for (int k = 0; k < s.n_obj; ++k) {
+      const int ob = __ldg(s.t_order + k);
+      if (__ldg(route + ob) != 1) continue;
+      const double* box = s.obox + (size_t)ob * 6;
+      const Classified c = classify(r, box, s.n_obj, s.tol);
+      if (c.kind == 0) continue;
+      double cc[5];
+      bool deg;
+      if (c.kind == 1) {
+        deg = transform_outer(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, box, box + 3, c.t0, cc);
+        cc[4] = 0.0;
+        if (jo < out.cap_outer) {
+          out.outer_obj[jo] = ob;
+          out.outer_ray[jo] = (int32_t)i;
+          reinterpret_cast<float4*>(out.outer_coord)[jo] =
+              make_float4((float)cc[0], (float)cc[1], (float)cc[2], (float)cc[3]);
+        }
+        ++jo;
+      } else {
+        deg = transform_inner(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, box, box + 3, cc);
+        if (ji < out.cap_inner) {
+          out.inner_obj[ji] = ob;
+          out.inner_ray[ji] = (int32_t)i;
+          reinterpret_cast<float4*>(out.inner_coord)[ji] =
+              make_float4((float)cc[0], (float)cc[1], (float)cc[2], (float)cc[3]);
+          out.inner_r[ji] = (float)cc[4];
+        }
+        ++ji;
+      }
+      if (out.rec_kind != nullptr && jt < out.cap_total) {
+        out.rec_kind[jt] = c.kind == 1 ? 0 : 1;
+        out.rec_obj[jt] = ob;
+        out.rec_ray[jt] = (int32_t)i;
+        for (int q = 0; q < 5; ++q) out.rec_coord[jt * 5 + q] = cc[q];
+      }
+      ++jt;
+      deg_count += deg ? 1 : 0;
+    }
+  }
+  // degenerate counter (bvh.py:868-869, 892-893), warp-aggregated
+  const int tot = __reduce_add_sync(0xffffffffu, deg_count);
+  if ((threadIdx.x & 31) == 0 && tot > 0) atomicAdd((unsigned long long*)(out.counts + 3),
+                                                    (unsigned long long)tot);
+}
+
+// bvh.py:904-916 _k_label_visible
+__global__ void label_kernel(nif_scene_view s, const int32_t* __restrict__ rec_obj,
+                             const int32_t* __restrict__ rec_ray, int64_t m,
+                             const double* __restrict__ o, const double* __restrict__ d,
+                             const double* __restrict__ tm, uint8_t* __restrict__ vis) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int64_t i = rec_ray[j];
+  const RayIn r = load_ray(o, d, tm, i);
+  const bool occ = occluded_in_object(s.nodes, s.tris, __ldg(s.roots + rec_obj[j]), r.ox, r.oy,
+                                      r.oz, r.dx, r.dy, r.dz, s.eps, r.tmax);
+  vis[j] = occ ? 0 : 1;
+}
+
+// bvh.py:650-700 _scene_occluded. Any-hit is an OR over objects, so the
+// top-level walk reduces to the per-object window test in leaf order.
+__global__ void bvh_occluded_kernel(nif_scene_view s, const double* __restrict__ o,
+                                    const double* __restrict__ d, const double* __restrict__ tm,
+                                    int64_t n, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const RayIn r = load_ray(o, d, tm, i);
+  bool occ = false;
+  for (int k = 0; k < s.n_obj && !occ; ++k) {
+    const int ob = __ldg(s.t_order + k);
+    const double* box = s.obox + (size_t)ob * 6;
+    if (s.n_obj > 1 &&
+        !window_hit(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, box, box + 3, s.eps, r.tmax, nullptr))
+      continue;
+    occ = occluded_in_object(s.nodes, s.tris, __ldg(s.roots + ob), r.ox, r.oy, r.oz, r.dx, r.dy,
+                             r.dz, s.eps, r.tmax);
+  }
+  out[i] = occ ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// shadow-ray generation: renderer.py:86-105 (RNG), 453-532 (_k_primary,
+// _k_light_sample), 262-330 (light cores), 579-647 (bvh._scene_closest)
+// ---------------------------------------------------------------------------
+
+constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMix2 = 0x94D049BB133111EBull;
+constexpr uint64_t kGold = 0x9E3779B97F4A7C15ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMix1;
+  z = (z ^ (z >> 27)) * kMix2;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double rand01(uint64_t seed, uint64_t pixel, uint64_t sample,
+                                         uint64_t draw) {
+  uint64_t x = seed + kGold;
+  x = mix64(x + pixel * kMix1);
+  x = mix64(x + sample * kMix2);
+  x = mix64(x + draw * kGold);
+  return (double)(x >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__device__ int scene_closest(const nif_scene_view& s, double ox, double oy, double oz,
+                             double dx, double dy, double dz, double eps, double* t_out,
+                             int* obj_out, double* bu_out, double* bv_out) {
+  int stack[kStack];
+  double tstack[kStack];
+  double t_best = CUDART_INF;
+  int best_obj = -1, best_slot = -1;
+  double bu = 0.0, bv = 0.0;
+  int sp = 0;
+  int node = 0;
+  while (node >= 0) {
+    int descend = -1;
+    const nif_node& nd = s.top_nodes[node];
+    if (nd.leaf == 1) {
+      for (int k = nd.a; k < nd.a + nd.b; ++k) {
+        const int ob = s.top_order[k];
+        double t = t_best, u, v;
+        const int slot = closest_in_object(s.nodes, s.tris, s.roots[ob], ox, oy, oz, dx, dy, dz,
+                                           eps, &t, &u, &v);
+        if (slot >= 0) {
+          t_best = t;
+          best_obj = ob;
+          best_slot = slot;
+          bu = u;
+          bv = v;
+        }
+      }
+    } else {
+      int l = nd.a, r = nd.b;
+      double tl, tr;
+      const bool hl = window_hit(ox, oy, oz, dx, dy, dz, s.top_nodes[l].lo, s.top_nodes[l].hi,
+                                 eps, t_best, &tl);
+      const bool hr = window_hit(ox, oy, oz, dx, dy, dz, s.top_nodes[r].lo, s.top_nodes[r].hi,
+                                 eps, t_best, &tr);
+      if (hl && hr) {
+        if (tl > tr) {
+          int q = l; l = r; r = q;
+          double qt = tl; tl = tr; tr = qt;
+        }
+        stack[sp] = r;
+        tstack[sp] = tr;
+        ++sp;
+        descend = l;
+      } else if (hl) {
+        descend = l;
+      } else if (hr) {
+        descend = r;
+      }
+    }
+    if (descend >= 0) {
+      node = descend;
+    } else {
+      node = -1;
+      while (sp > 0) {
+        --sp;
+        if (tstack[sp] < t_best) {
+          node = stack[sp];
+          break;
+        }
+      }
+    }
+  }
+  *t_out = t_best;
+  *obj_out = best_obj;
+  *bu_out = bu;
+  *bv_out = bv;
+  return best_slot;
+}
+
+__global__ void sample_pass_kernel(nif_scene_view s, nif_camera cam, nif_lights_view L,
+                                   uint64_t seed, uint64_t sample, int sampler, int64_t pix0,
+                                   int64_t n_pix, nif_pass_out out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_pix) return;
+  const int64_t i = pix0 + j;  // global pixel index keys the RNG
+  const int64_t px = i % cam.width, py = i / cam.width;
+  const double jx = rand01(seed, i, sample, 0);
+  const double jy = rand01(seed, i, sample, 1);
+  const double sx = (((double)px + jx) / (double)cam.width) * 2.0 - 1.0;
+  const double sy = 1.0 - (((double)py + jy) / (double)cam.height) * 2.0;
+  double dx = cam.fwd[0] + sx * cam.tan_half * cam.aspect * cam.right[0] + sy * cam.tan_half * cam.up[0];
+  double dy = cam.fwd[1] + sx * cam.tan_half * cam.aspect * cam.right[1] + sy * cam.tan_half * cam.up[1];
+  double dz = cam.fwd[2] + sx * cam.tan_half * cam.aspect * cam.right[2] + sy * cam.tan_half * cam.up[2];
+  const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+  dx /= dn;
+  dy /= dn;
+  dz /= dn;
+  out.pdir[j * 3 + 0] = dx;
+  out.pdir[j * 3 + 1] = dy;
+  out.pdir[j * 3 + 2] = dz;
+  double t, bu, bv;
+  int ob;
+  const int slot = scene_closest(s, cam.pos[0], cam.pos[1], cam.pos[2], dx, dy, dz, s.eps, &t,
+                                 &ob, &bu, &bv);
+  double P[3] = {0.0, 0.0, 0.0}, Nn[3] = {0.0, 0.0, 0.0};
+  if (slot >= 0) {
+    out.hit[j] = 1;
+    out.t[j] = t;
+    out.obj[j] = ob;
+    P[0] = cam.pos[0] + t * dx;
+    P[1] = cam.pos[1] + t * dy;
+    P[2] = cam.pos[2] + t * dz;
+    const double b0 = 1.0 - bu - bv;
+    const double* n9 = s.normals + (size_t)slot * 9;
+    double nx = b0 * n9[0] + bu * n9[3] + bv * n9[6];
+    double ny = b0 * n9[1] + bu * n9[4] + bv * n9[7];
+    double nz = b0 * n9[2] + bu * n9[5] + bv * n9[8];
+    const double nn = sqrt(nx * nx + ny * ny + nz * nz);
+    if (nn > 0.0) {
+      nx /= nn;
+      ny /= nn;
+      nz /= nn;
+    }
+    Nn[0] = nx;
+    Nn[1] = ny;
+    Nn[2] = nz;
+  } else {
+    out.hit[j] = 0;
+    out.t[j] = CUDART_INF;
+    out.obj[j] = -1;
+  }
+  for (int c = 0; c < 3; ++c) {
+    out.point[j * 3 + c] = P[c];
+    out.normal[j * 3 + c] = Nn[c];
+  }
+  double ld[3] = {0.0, 0.0, 0.0}, emit[3] = {0.0, 0.0, 0.0};
+  double tmax = 0.0, pdf = 0.0;
+  if (sampler == 1) {
+    emit[0] = emit[1] = emit[2] = 1.0;  // renderer.py:797 labels only
+    if (slot >= 0) {
+      // renderer.py:325-330, 535-547
+      const double u_a = rand01(seed, i, sample, 2);
+      const double u_b = rand01(seed, i, sample, 3);
+      const double z = 1.0 - 2.0 * u_a;
+      const double sq = sqrt(fmax(0.0, 1.0 - z * z));
+      const double phi = (2.0 * kPi) * u_b;
+      ld[0] = cos(phi) * sq;
+      ld[1] = sin(phi) * sq;
+      ld[2] = z;
+      tmax = CUDART_INF;
+      pdf = 1.0 / (4.0 * kPi);
+    }
+  } else if (slot >= 0 && L.n_lights > 0) {
+    const double u_sel = rand01(seed, i, sample, 2);
+    const double u_a = rand01(seed, i, sample, 3);
+    const double u_b = rand01(seed, i, sample, 4);
+    // searchsorted(cum, u_sel, side="right")
+    int li = 0;
+    while (li < L.n_lights && L.cum[li] <= u_sel) ++li;
+    if (li >= L.n_lights) li = L.n_lights - 1;
+    const double sel_pmf = L.cum[li] - (li > 0 ? L.cum[li - 1] : 0.0);
+    const double* ldat = L.data + (size_t)li * 16;
+    if (L.kind[li] == 0) {
+      const double vx = ldat[0] - P[0], vy = ldat[1] - P[1], vz = ldat[2] - P[2];
+      const double dd = sqrt(vx * vx + vy * vy + vz * vz);
+      if (dd <= 0.0) {
+        ld[2] = 1.0;
+        pdf = 1.0;
+      } else {
+        const double inv = 1.0 / dd;
+        const double inv2 = inv * inv;
+        ld[0] = vx * inv;
+        ld[1] = vy * inv;
+        ld[2] = vz * inv;
+        tmax = dd;
+        pdf = sel_pmf;
+        emit[0] = ldat[3] * inv2;
+        emit[1] = ldat[4] * inv2;
+        emit[2] = ldat[5] * inv2;
+      }
+    } else {
+      const double sxp = ldat[0] + u_a * ldat[3] + u_b * ldat[6];
+      const double syp = ldat[1] + u_a * ldat[4] + u_b * ldat[7];
+      const double szp = ldat[2] + u_a * ldat[5] + u_b * ldat[8];
+      const double vx = sxp - P[0], vy = syp - P[1], vz = szp - P[2];
+      const double d2 = vx * vx + vy * vy + vz * vz;
+      const double dd = sqrt(d2);
+      if (dd <= 0.0) {
+        ld[2] = 1.0;
+        pdf = 1.0;
+      } else {
+        const double inv = 1.0 / dd;
+        ld[0] = vx * inv;
+        ld[1] = vy * inv;
+        ld[2] = vz * inv;
+        tmax = dd;
+        const double cos_l = -(ld[0] * ldat[12] + ld[1] * ldat[13] + ld[2] * ldat[14]);
+        if (cos_l <= 0.0) {
+          pdf = sel_pmf;
+        } else {
+          pdf = sel_pmf * d2 / (ldat[15] * cos_l);
+          emit[0] = ldat[9];
+          emit[1] = ldat[10];
+          emit[2] = ldat[11];
+        }
+      }
+    }
+  }
+  for (int c = 0; c < 3; ++c) {
+    out.ldir[j * 3 + c] = ld[c];
+    out.emit[j * 3 + c] = emit[c];
+  }
+  out.tmax[j] = tmax;
+  out.pdf[j] = pdf;
+}
+
+inline unsigned grid_for(int64_t n, int threads) {
+  return (unsigned)((n + threads - 1) / threads);
+}
+
+size_t cub_scan_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                (int)(n > 0 ? n : 1));
+  return bytes;
+}
+
+}  // namespace
+}  // namespace nif
+
+using namespace nif;
+
+extern "C" size_t nif_gather_workspace_bytes(int64_t n) {
+  const size_t a = align_up((size_t)(n > 0 ? n : 1) * sizeof(uint64_t), 256);
+  return 2 * a + align_up(cub_scan_bytes(n), 256) + 256;
+}
+
+extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
+                              const double* origins, const double* dirs, const double* tmaxs,
+                              int64_t n, const nif_gather_out* out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (n < 0) return fail(NIF_ERR_VALUE, "ray count cannot be negative");
+  if (n >= (int64_t)1 << 31) return fail(NIF_ERR_VALUE, "at most 2^31-1 rays per gather");
+  if ((uint64_t)n * (uint64_t)(s->n_obj > 0 ? s->n_obj : 1) >= ((uint64_t)1 << 32))
+    return fail(NIF_ERR_VALUE, "gather exceeds 2^32 record slots; split the ray batch");
+  if (workspace_bytes < nif_gather_workspace_bytes(n))
+    return fail(NIF_ERR_VALUE, "gather workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  const size_t a = align_up((size_t)(n > 0 ? n : 1) * sizeof(uint64_t), 256);
+  uint64_t* cnt = (uint64_t*)ws;
+  uint64_t* off = (uint64_t*)(ws + a);
+  void* tmp = ws + 2 * a;
+  size_t tmp_bytes = workspace_bytes - 2 * a;
+  if (n == 0) {
+    cudaMemsetAsync(out->counts, 0, 4 * sizeof(int64_t), st);
+    return check_launch("gather(empty)");
+  }
+  gather_count_kernel<<<grid_for(n, kGatherThreads), kGatherThreads, 0, st>>>(
+      *s, route, origins, dirs, tmaxs, n, cnt, out->bvh_occ);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)n, st);
+  gather_totals_kernel<<<1, 32, 0, st>>>(cnt, off, n, out->counts);
+  gather_write_kernel<<<grid_for(n, kGatherThreads), kGatherThreads, 0, st>>>(
+      *s, route, origins, dirs, tmaxs, n, off, *out);
+  return check_launch("nif_gather_dev");
+}
+
+extern "C" int nif_label_visible_dev(const nif_scene_view* s, const int32_t* rec_obj,
+                                     const int32_t* rec_ray, int64_t m, const double* origins,
+                                     const double* dirs, const double* tmaxs, uint8_t* out_vis,
+                                     void* stream) {
+  if (m <= 0) return NIF_OK;
+  label_kernel<<<grid_for(m, 128), 128, 0, (cudaStream_t)stream>>>(*s, rec_obj, rec_ray, m,
+                                                                   origins, dirs, tmaxs, out_vis);
+  return check_launch("nif_label_visible_dev");
+}
+
+extern "C" int nif_bvh_occluded_dev(const nif_scene_view* s, const double* origins,
+                                    const double* dirs, const double* tmaxs, int64_t n,
+                                    uint8_t* out_occ, void* stream) {
+  if (n <= 0) return NIF_OK;
+  bvh_occluded_kernel<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(*s, origins, dirs,
+                                                                          tmaxs, n, out_occ);
+  return check_launch("nif_bvh_occluded_dev");
+}
+
+extern "C" int nif_sample_pass_dev(const nif_scene_view* s, const nif_camera* cam,
+                                   const nif_lights_view* lights, int64_t seed, int64_t sample,
+                                   int32_t sampler, int64_t pix0, int64_t n_pix,
+                                   const nif_pass_out* out, void* stream) {
+  if (sampler != 0 && sampler != 1) return fail(NIF_ERR_VALUE, "unknown sampler %d", sampler);
+  if (n_pix <= 0) return NIF_OK;
+  sample_pass_kernel<<<grid_for(n_pix, 128), 128, 0, (cudaStream_t)stream>>>(
+      *s, *cam, *lights, (uint64_t)seed, (uint64_t)sample, sampler, pix0, n_pix, *out);
+  return check_launch("nif_sample_pass_dev");
+}

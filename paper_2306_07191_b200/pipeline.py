@@ -1,0 +1,466 @@
+"""The split visibility pass on the device and the reference's backend
+strategy objects (renderer.py:593-700), plus the per-sample pass and a
+progressive render loop (renderer.py:743-861) that drive it.
+
+``VisibilityEngine`` is the hot path: rays already in HBM ->
+phase-1 gather (fp64 classify + ordered compaction into outer/inner
+queues) -> per-ray OR seeded with the hybrid BVH result -> fused
+encode+MLP+threshold per family (tcgen05) -> occlusion bytes per ray.
+Every launch is stream-ordered with no host synchronisation, so a fixed
+ray count can be captured once in a CUDA graph and replayed.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .scene import QueryRecords, Scene, ShadowRays
+
+GAMMA = 1.0 / 2.2
+PSNR_SENTINEL = math.inf
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def rays_to_device(rays: ShadowRays, device):
+    torch = _torch()
+    o = torch.from_numpy(np.ascontiguousarray(rays.origins, np.float64)).to(device)
+    d = torch.from_numpy(np.ascontiguousarray(rays.dirs, np.float64)).to(device)
+    t = torch.from_numpy(np.ascontiguousarray(rays.tmaxs, np.float64)).to(device)
+    return o, d, t
+
+
+class GatherBuffers:
+    """Device outputs of nif_gather_dev for up to `n` rays."""
+
+    def __init__(self, n, n_net_obj, device, interleaved=False):
+        torch = _torch()
+        cap = max(1, n * max(1, n_net_obj))
+        self.n = n
+        self.cap = cap
+        i32 = dict(dtype=torch.int32, device=device)
+        f32 = dict(dtype=torch.float32, device=device)
+        self.outer_obj = torch.empty(cap, **i32)
+        self.outer_ray = torch.empty(cap, **i32)
+        self.outer_coord = torch.empty(cap * 4, **f32)
+        self.inner_obj = torch.empty(cap, **i32)
+        self.inner_ray = torch.empty(cap, **i32)
+        self.inner_coord = torch.empty(cap * 4, **f32)
+        self.inner_r = torch.empty(cap, **f32)
+        self.bvh_occ = torch.empty(max(n, 1), dtype=torch.uint8, device=device)
+        self.counts = torch.zeros(4, dtype=torch.int64, device=device)
+        self.interleaved = interleaved
+        if interleaved:
+            self.rec_kind = torch.empty(cap, dtype=torch.uint8, device=device)
+            self.rec_obj = torch.empty(cap, **i32)
+            self.rec_ray = torch.empty(cap, **i32)
+            self.rec_coord = torch.empty(cap * 5, dtype=torch.float64, device=device)
+        ws = _lib.lib().nif_gather_workspace_bytes(max(n, 1))
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=device)
+        p = _lib.ptr
+        self.out = _lib.GatherOut(
+            outer_obj=p(self.outer_obj), outer_ray=p(self.outer_ray),
+            outer_coord=p(self.outer_coord), inner_obj=p(self.inner_obj),
+            inner_ray=p(self.inner_ray), inner_coord=p(self.inner_coord),
+            inner_r=p(self.inner_r), cap_outer=cap, cap_inner=cap,
+            rec_kind=p(self.rec_kind) if interleaved else None,
+            rec_obj=p(self.rec_obj) if interleaved else None,
+            rec_ray=p(self.rec_ray) if interleaved else None,
+            rec_coord=p(self.rec_coord) if interleaved else None,
+            cap_total=cap if interleaved else 0, bvh_occ=p(self.bvh_occ),
+            counts=p(self.counts))
+
+
+def gather_dev(dscene, route_dev, o, d, t, n, buf: GatherBuffers, stream=None):
+    L = _lib.lib()
+    L.nif_gather_dev(dscene.view, _lib.ptr(route_dev), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
+                     buf.out, _lib.ptr(buf.workspace), buf.workspace.numel(),
+                     _lib.stream_ptr(stream))
+
+
+def gather_queries(scene: Scene, rays: ShadowRays, route: np.ndarray, threads: int = 1):
+    """renderer.py:613-644 on the device. Returns (QueryRecords,
+    bvh_occluded) with records in the reference's order (ray-major, top-level
+    DFS order within a ray). `threads` is accepted for signature parity."""
+    torch = _torch()
+    ds = scene.device()
+    n = len(rays)
+    if n == 0:
+        return QueryRecords(np.zeros(0, np.uint8), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                            np.zeros((0, 5)), 0), np.zeros(0, bool)
+    o, d, t = rays_to_device(rays, ds.device)
+    n_net = int(np.asarray(route, np.uint8).sum())
+    buf = GatherBuffers(n, n_net, ds.device, interleaved=True)
+    gather_dev(ds, ds.route(route), o, d, t, n, buf)
+    counts = buf.counts.cpu().numpy()
+    m = int(counts[2])
+    rec = QueryRecords(kind=buf.rec_kind[:m].cpu().numpy(), obj=buf.rec_obj[:m].cpu().numpy(),
+                       ray=buf.rec_ray[:m].cpu().numpy(),
+                       coord=buf.rec_coord[:m * 5].view(m, 5).cpu().numpy(),
+                       degenerate_count=int(counts[3]))
+    return rec, buf.bvh_occ[:n].cpu().numpy().astype(bool)
+
+
+def label_visible(scene: Scene, records: QueryRecords, rays: ShadowRays) -> np.ndarray:
+    """bvh.py:904-916 via nif_label_visible_dev: uint8, 1 = visible."""
+    torch = _torch()
+    ds = scene.device()
+    m = len(records)
+    if m == 0:
+        return np.zeros(0, np.uint8)
+    o, d, t = rays_to_device(rays, ds.device)
+    ro = torch.from_numpy(np.ascontiguousarray(records.obj, np.int32)).to(ds.device)
+    rr = torch.from_numpy(np.ascontiguousarray(records.ray, np.int32)).to(ds.device)
+    vis = torch.empty(m, dtype=torch.uint8, device=ds.device)
+    _lib.lib().nif_label_visible_dev(ds.view, _lib.ptr(ro), _lib.ptr(rr), m, _lib.ptr(o),
+                                     _lib.ptr(d), _lib.ptr(t), _lib.ptr(vis), _lib.stream_ptr())
+    return vis.cpu().numpy()
+
+
+def oracle_predictor(scene: Scene, records: QueryRecords, rays: ShadowRays,
+                     threads: int = 1) -> np.ndarray:
+    """renderer.py:647-662: ground-truth answers from per-object trees."""
+    return label_visible(scene, records, rays) == 0
+
+
+class BvhBackend:
+    """renderer.py:593-610 on the device (two-level fp64 any-hit)."""
+
+    name = "bvh"
+
+    def occluded(self, scene: Scene, rays: ShadowRays, threads: int = 1) -> np.ndarray:
+        torch = _torch()
+        ds = scene.device()
+        n = len(rays)
+        if n == 0:
+            return np.zeros(0, bool)
+        o, d, t = rays_to_device(rays, ds.device)
+        out = torch.empty(n, dtype=torch.uint8, device=ds.device)
+        _lib.lib().nif_bvh_occluded_dev(ds.view, _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
+                                        _lib.ptr(out), _lib.stream_ptr())
+        return out.cpu().numpy().astype(bool)
+
+
+class PredictorBackend:
+    """renderer.py:665-683: gather, answer records, OR per ray."""
+
+    name = "predictor"
+
+    def __init__(self, predictor, hybrid_threshold: Optional[int] = None):
+        self.predictor = predictor
+        self.hybrid_threshold = hybrid_threshold
+        self.last_records: Optional[QueryRecords] = None
+
+    def occluded(self, scene: Scene, rays: ShadowRays, threads: int = 1) -> np.ndarray:
+        route = scene.nif_route_mask(self.hybrid_threshold)
+        records, occ = gather_queries(scene, rays, route, threads)
+        self.last_records = records
+        if len(records):
+            rec_occ = self.predictor(scene, records, rays, threads)
+            occ = occ.copy()
+            occ[records.ray[rec_occ]] = True
+        return occ
+
+
+class OracleBackend(PredictorBackend):
+    """renderer.py:686-693: must match BvhBackend pixel for pixel."""
+
+    name = "oracle"
+
+    def __init__(self, hybrid_threshold: Optional[int] = None):
+        super().__init__(oracle_predictor, hybrid_threshold)
+
+
+class VisibilityEngine:
+    """Device-resident split visibility pass for one (scene, model, route).
+
+    Buffers are sized for `capacity` rays; `run(n)` enqueues the whole pass
+    for the first n rays already in `origins/dirs/tmaxs` and leaves one byte
+    per ray in `occ` (1 = shadowed). No host synchronisation inside.
+    """
+
+    def __init__(self, scene: Scene, model, capacity: int, hybrid_threshold=None,
+                 impl: int = _lib.IMPL_AUTO):
+        torch = _torch()
+        self.scene = scene
+        self.ds = scene.device()
+        self.model = model
+        self.impl = impl
+        self.capacity = capacity
+        route = scene.nif_route_mask(hybrid_threshold)
+        self.route_np = route
+        self.route = self.ds.route(route)
+        dev = self.ds.device
+        self.origins = torch.empty((capacity, 3), dtype=torch.float64, device=dev)
+        self.dirs = torch.empty((capacity, 3), dtype=torch.float64, device=dev)
+        self.tmaxs = torch.empty(capacity, dtype=torch.float64, device=dev)
+        self.buf = GatherBuffers(capacity, int(route.sum()), dev)
+        self.occ = torch.empty(capacity, dtype=torch.uint8, device=dev)
+        self._views = None
+        self.graphs = {}
+
+    def _family_views(self):
+        if self._views is None or self.model.outer.dirty or self.model.inner.dirty:
+            self._views = (self.model.outer.view(with_fast=True),
+                           self.model.inner.view(with_fast=True))
+        return self._views
+
+    def load(self, rays: ShadowRays, non_blocking=False):
+        torch = _torch()
+        n = len(rays)
+        if n > self.capacity:
+            raise ValueError(f"{n} rays exceed the engine capacity {self.capacity}")
+        self.origins[:n].copy_(torch.from_numpy(np.ascontiguousarray(rays.origins, np.float64)),
+                               non_blocking=non_blocking)
+        self.dirs[:n].copy_(torch.from_numpy(np.ascontiguousarray(rays.dirs, np.float64)),
+                            non_blocking=non_blocking)
+        self.tmaxs[:n].copy_(torch.from_numpy(np.ascontiguousarray(rays.tmaxs, np.float64)),
+                             non_blocking=non_blocking)
+        return n
+
+    def run(self, n: int, stream=None):
+        L = _lib.lib()
+        sp = _lib.stream_ptr(stream)
+        b = self.buf
+        gather_dev(self.ds, self.route, self.origins, self.dirs, self.tmaxs, n, b, stream)
+        L.nif_occ_init_dev(_lib.ptr(b.bvh_occ), n, _lib.ptr(self.occ), sp)
+        if self.model is None:
+            return
+        vo, vi = self._family_views()
+        p = _lib.ptr
+        cnt = b.counts.data_ptr()
+        L.nif_query_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None, cnt,
+                        b.cap, p(self.occ), None, self.impl, sp)
+        L.nif_query_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord), p(b.inner_r),
+                        cnt + 8, b.cap, p(self.occ), None, self.impl, sp)
+
+    def capture(self, n: int):
+        """CUDA-graph the pass for a fixed ray count (replayed by `replay`)."""
+        torch = _torch()
+        self._family_views()  # pack outside the capture
+        s = torch.cuda.Stream(device=self.ds.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run(n, s)  # warm (kernel attributes, lazy module load)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(n)
+        self.graphs[n] = g
+        return g
+
+    def counts(self):
+        return self.buf.counts.cpu().numpy()
+
+
+class NifBackend(PredictorBackend):
+    """nif.py:486-499: visibility from the learned model, optionally hybrid.
+    occluded() runs the fused device pass; predict() keeps the record API."""
+
+    def __init__(self, model, hybrid_threshold: Optional[int] = None,
+                 impl: int = _lib.IMPL_AUTO, keep_records: bool = False):
+        if model is None:
+            raise ValueError("the learned backend needs a model")
+        from .nif import infer_records
+        self.model = model
+        self.impl = impl
+        self.keep_records = keep_records
+
+        def predict(scene, records, rays, threads=1):
+            return infer_records(model, records, impl)
+
+        super().__init__(predict, hybrid_threshold)
+        self.name = "nif" if hybrid_threshold is None else "hybrid"
+        self._engines = {}
+
+    def engine(self, scene: Scene, n: int) -> VisibilityEngine:
+        key = id(scene)
+        eng = self._engines.get(key)
+        if eng is None or eng.capacity < n:
+            cap = max(n, 1024)
+            eng = VisibilityEngine(scene, self.model, cap, self.hybrid_threshold, self.impl)
+            self._engines[key] = eng
+        return eng
+
+    def occluded(self, scene: Scene, rays: ShadowRays, threads: int = 1) -> np.ndarray:
+        if self.keep_records:
+            return super().occluded(scene, rays, threads)
+        n = len(rays)
+        if n == 0:
+            return np.zeros(0, bool)
+        eng = self.engine(scene, n)
+        eng.load(rays)
+        eng.run(n)
+        return eng.occ[:n].cpu().numpy().astype(bool)
+
+
+def shade_pass_nif(scene: Scene, rays: ShadowRays, predictor, hybrid_threshold=None,
+                   threads: int = 1) -> np.ndarray:
+    return PredictorBackend(predictor, hybrid_threshold).occluded(scene, rays, threads)
+
+
+# ---------------------------------------------------------------------------
+# per-sample pass and render (renderer.py:743-861)
+# ---------------------------------------------------------------------------
+
+
+def camera_struct(camera) -> _lib.Camera:
+    fwd, right, up, tan_half, aspect = camera.basis()
+    c = _lib.Camera()
+    for k in range(3):
+        c.pos[k] = float(camera.position[k])
+        c.fwd[k] = float(fwd[k])
+        c.right[k] = float(right[k])
+        c.up[k] = float(up[k])
+    c.tan_half = tan_half
+    c.aspect = aspect
+    c.width = camera.width
+    c.height = camera.height
+    return c
+
+
+class _LightsDev:
+    def __init__(self, scene: Scene, device):
+        torch = _torch()
+        if scene.lights:
+            cum, kind, data = scene.light_tables()
+        else:
+            cum, kind, data = np.ones(1), np.zeros(1, np.uint8), np.zeros((1, 16))
+        self.cum = torch.from_numpy(np.ascontiguousarray(cum, np.float64)).to(device)
+        self.kind = torch.from_numpy(np.ascontiguousarray(kind, np.uint8)).to(device)
+        self.data = torch.from_numpy(np.ascontiguousarray(data, np.float64)).to(device)
+        self.view = _lib.LightsView(n_lights=len(scene.lights), pad0=0, kind=_lib.ptr(self.kind),
+                                    data=_lib.ptr(self.data), cum=_lib.ptr(self.cum))
+
+
+def sample_pass_dev(scene: Scene, camera, sample: int, seed: int, sampler="importance",
+                    pix0: int = 0, n_pix: Optional[int] = None):
+    """renderer.py:743-805 on the device; returns a dict of torch tensors
+    for pixels [pix0, pix0 + n_pix) (image-tile sharding)."""
+    torch = _torch()
+    if sampler not in ("importance", "uniform"):
+        raise ValueError(f"unknown sampler {sampler!r}")
+    ds = scene.device()
+    dev = ds.device
+    n = camera.width * camera.height - pix0 if n_pix is None else n_pix
+    key = ("lights", str(dev))
+    lights = scene._device.get(key)
+    if lights is None:
+        lights = scene._device[key] = _LightsDev(scene, dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    out = {"hit": torch.empty(n, dtype=torch.uint8, device=dev), "t": torch.empty(n, **f64),
+           "obj": torch.empty(n, dtype=torch.int32, device=dev),
+           "point": torch.empty((n, 3), **f64), "normal": torch.empty((n, 3), **f64),
+           "pdir": torch.empty((n, 3), **f64), "ldir": torch.empty((n, 3), **f64),
+           "tmax": torch.empty(n, **f64), "pdf": torch.empty(n, **f64),
+           "emit": torch.empty((n, 3), **f64)}
+    po = _lib.PassOut(**{k: _lib.ptr(v) for k, v in out.items()})
+    _lib.lib().nif_sample_pass_dev(ds.view, camera_struct(camera), lights.view, int(seed),
+                                   int(sample), 0 if sampler == "importance" else 1, int(pix0),
+                                   int(n), po, _lib.stream_ptr())
+    return out
+
+
+def sample_pass(scene: Scene, camera, sample: int, seed: int, threads: int = 1,
+                sampler: str = "importance"):
+    """renderer.py:743-805 (host arrays, same keys as the reference)."""
+    d = sample_pass_dev(scene, camera, sample, seed, sampler)
+    out = {k: v.cpu().numpy() for k, v in d.items()}
+    out["hit"] = out["hit"].astype(bool)
+    return out
+
+
+def shadow_rays_dev(data, require_emit=True):
+    """Cast filter of renderer.py:831-832 (cli.py:170-183 drops the emit
+    test): returns (mask, origins, dirs, tmaxs) as device tensors."""
+    cos = (data["normal"] * data["ldir"]).sum(dim=1)
+    cast = (data["hit"] != 0) & (cos > 0.0) & (data["pdf"] > 0.0)
+    if require_emit:
+        cast &= data["emit"].amax(dim=1) > 0.0
+    idx = cast.nonzero().squeeze(1)
+    return cast, data["point"][idx].contiguous(), data["ldir"][idx].contiguous(), \
+        data["tmax"][idx].contiguous()
+
+
+@dataclass
+class RenderConfig:
+    spp: int = 16
+    sample_offset: int = 0
+    seed: Optional[int] = None
+    threads: Optional[int] = None
+
+
+@dataclass
+class HdrImage:
+    sum: np.ndarray
+    count: int
+    timings: dict = field(default_factory=dict)
+
+    def mean(self) -> np.ndarray:
+        if self.count == 0:
+            return np.zeros_like(self.sum)
+        return self.sum / self.count
+
+    def merge(self, other: "HdrImage") -> "HdrImage":
+        if self.sum.shape != other.sum.shape:
+            raise ValueError("image shapes differ")
+        return HdrImage(self.sum + other.sum, self.count + other.count)
+
+
+def render(scene: Scene, camera=None, config: RenderConfig = None, backend=None) -> HdrImage:
+    """renderer.py:808-861: progressive direct lighting, one shadow ray
+    per pixel sample, visibility from `backend`."""
+    torch = _torch()
+    config = config or RenderConfig()
+    camera = camera or scene.camera
+    if camera is None:
+        raise ValueError("no camera given and the scene has none")
+    backend = backend or BvhBackend()
+    seed = scene.seed if config.seed is None else config.seed
+    w, h = camera.width, camera.height
+    dev = scene.device().device
+    buf = torch.zeros((w * h, 3), dtype=torch.float64, device=dev)
+    albedo = scene.device().albedo
+    inv_pi = 1.0 / math.pi
+    for s in range(config.sample_offset, config.sample_offset + config.spp):
+        data = sample_pass_dev(scene, camera, s, seed)
+        cos = (data["normal"] * data["ldir"]).sum(dim=1)
+        cast, o, d, t = shadow_rays_dev(data)
+        if int(cast.sum()) == 0:
+            continue
+        rays = ShadowRays(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+        occ = backend.occluded(scene, rays, 1)
+        vis = torch.zeros(w * h, dtype=torch.float64, device=dev)
+        vis[cast] = torch.from_numpy(~occ).to(dev).double()
+        obj = data["obj"].long().clamp(min=0)
+        scale = torch.where(cast, vis * cos / torch.where(cast, data["pdf"], 1.0), 0.0)
+        contrib = albedo[obj] * inv_pi * data["emit"] * scale[:, None]
+        buf += torch.where(cast[:, None], contrib, 0.0)
+    return HdrImage(buf.view(h, w, 3).cpu().numpy(), config.spp)
+
+
+def tonemap_srgb8(linear) -> np.ndarray:
+    x = np.clip(np.asarray(linear, np.float64), 0.0, 1.0)
+    return np.rint(np.power(x, GAMMA) * 255.0).astype(np.uint8)
+
+
+def psnr(a, b) -> float:
+    """renderer.py:881-891 on tonemapped 8-bit images."""
+    la = a.mean() if isinstance(a, HdrImage) else np.asarray(a, np.float64)
+    lb = b.mean() if isinstance(b, HdrImage) else np.asarray(b, np.float64)
+    ta = tonemap_srgb8(la).astype(np.float64)
+    tb = tonemap_srgb8(lb).astype(np.float64)
+    if ta.shape != tb.shape:
+        raise ValueError("image shapes differ")
+    mse = float(np.mean((ta - tb) ** 2))
+    if mse == 0.0:
+        return PSNR_SENTINEL
+    return 10.0 * math.log10(255.0 ** 2 / mse)
