@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include "nif_b200.h"
+#include "kernels.h"
 #include "status.h"
 
 extern "C" const char* nif_last_error(void) { return nif::last_error().c_str(); }
@@ -21,3 +22,16 @@ extern "C" int nif_device_check(int device) {
   }
   return 1;
 }
+
+namespace nif {
+int sm_count() {
+  static thread_local int count = 0;
+  if (count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+    if (count <= 0) count = 148;
+  }
+  return count;
+}
+}  // namespace nif

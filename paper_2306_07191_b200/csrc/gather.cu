@@ -1,0 +1,427 @@
+// Phase 1 of the split visibility pass as ONE kernel (bvh.py:772-901
+// _k_gather_queries + renderer.py:613-644 gather_queries):
+//   per ray: fp64 top-level classification of every object (slab test with
+//   the ray's reciprocal direction computed once, containment against
+//   per-object pre-widened bounds), hybrid any-hit for objects routed to
+//   their own trees, then ordered compaction into the outer / inner record
+//   queues through a decoupled look-back scan over 128-ray tiles, so rays
+//   are read from HBM once and classified once.
+// Results are bit-identical to the reference's classification: 1.0 / d,
+// lo - tol and hi + tol are deterministic IEEE operations, so hoisting them
+// out of the object loop changes no value. Compiled with -fmad=false.
+//
+// Coordinates: the interleaved API output (QueryRecords, fp64) uses the
+// reference's fp64 transforms; the hot-path queues store fp32 coordinates,
+// evaluated as fp32 atan2/acos of the fp64 box-relative vector (the
+// classification and degenerate test stay fp64). The per-ray direction
+// coordinates are computed once per ray, not once per record.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "common.h"
+#include "geom.cuh"
+#include "kernels.h"
+#include "nif_b200.h"
+#include "status.h"
+
+namespace nif {
+namespace {
+
+constexpr int kThreads = 256;    // rays per tile (one per thread)
+constexpr int kMaxObjFused = 32; // 2 bits per object in a 64-bit mask
+
+struct ObjC {
+  double lo[3], hi[3];  // box
+  double lt[3], ht[3];  // lo - tol, hi + tol  (geometry.py:260-262)
+  double c[3];          // 0.5 * (lo + hi)     (geometry.py:275-277, 295-297)
+  double hn;            // |half diagonal|      (geometry.py:302-305)
+  int id, route, root, pad;
+};
+
+struct RayX {
+  double ox, oy, oz, dx, dy, dz, tmax;
+  double ix, iy, iz;  // 1 / d where d != 0
+};
+
+// geometry.py:152-196 with the reciprocal hoisted (inv = 1.0 / d is the
+// same value the reference recomputes per box).
+__device__ __forceinline__ Hit3 slab(const RayX& r, const ObjC& b) {
+  double t0 = -CUDART_INF, t1 = CUDART_INF;
+  if (r.dx != 0.0) {
+    double ta = (b.lo[0] - r.ox) * r.ix, tb = (b.hi[0] - r.ox) * r.ix;
+    if (ta > tb) { double q = ta; ta = tb; tb = q; }
+    if (ta > t0) t0 = ta;
+    if (tb < t1) t1 = tb;
+  } else if (r.ox < b.lo[0] || r.ox > b.hi[0]) {
+    return {false, 0.0, 0.0};
+  }
+  if (r.dy != 0.0) {
+    double ta = (b.lo[1] - r.oy) * r.iy, tb = (b.hi[1] - r.oy) * r.iy;
+    if (ta > tb) { double q = ta; ta = tb; tb = q; }
+    if (ta > t0) t0 = ta;
+    if (tb < t1) t1 = tb;
+  } else if (r.oy < b.lo[1] || r.oy > b.hi[1]) {
+    return {false, 0.0, 0.0};
+  }
+  if (r.dz != 0.0) {
+    double ta = (b.lo[2] - r.oz) * r.iz, tb = (b.hi[2] - r.oz) * r.iz;
+    if (ta > tb) { double q = ta; ta = tb; tb = q; }
+    if (ta > t0) t0 = ta;
+    if (tb < t1) t1 = tb;
+  } else if (r.oz < b.lo[2] || r.oz > b.hi[2]) {
+    return {false, 0.0, 0.0};
+  }
+  if (t1 < t0 || t1 < 0.0) return {false, t0, t1};
+  return {true, t0, t1};
+}
+
+// 0 none, 1 outer, 2 inner (see trace.cu classify())
+__device__ __forceinline__ int classify_obj(const RayX& r, const ObjC& b, bool test_box,
+                                            double tol, double* t0) {
+  const Hit3 h = slab(r, b);
+  if (test_box && !(h.hit && h.t0 <= r.tmax && h.t1 >= -tol)) return 0;
+  if (b.lt[0] <= r.ox && r.ox <= b.ht[0] && b.lt[1] <= r.oy && r.oy <= b.ht[1] &&
+      b.lt[2] <= r.oz && r.oz <= b.ht[2])
+    return 2;
+  if (h.hit && h.t0 > 0.0 && h.t0 < r.tmax) {
+    *t0 = h.t0;
+    return 1;
+  }
+  return 0;
+}
+
+// fp32 spherical map of an fp64 vector (not normalised: atan2 is scale
+// invariant, acos gets z / |v|).
+__device__ __forceinline__ void sph32(double x, double y, double z, double n, float* u,
+                                      float* v) {
+  float uu = (atan2f((float)y, (float)x) + CUDART_PI_F) * (0.5f / CUDART_PI_F);
+  if (uu >= 1.0f) uu -= 1.0f;
+  else if (uu < 0.0f) uu += 1.0f;
+  float zz = (float)(z / n);
+  zz = fminf(fmaxf(zz, -1.0f), 1.0f);
+  *u = uu;
+  *v = acosf(zz) * (1.0f / CUDART_PI_F);
+}
+
+constexpr uint64_t kFlagA = 1ull << 62;
+constexpr uint64_t kFlagP = 2ull << 62;
+constexpr uint64_t kCntMask = (1ull << 31) - 1;
+
+__device__ __forceinline__ uint64_t pack(uint64_t flag, uint64_t o, uint64_t i) {
+  return flag | (o << 31) | i;
+}
+
+// Conservative fp32 prefilter of the top-level candidate test. The fp32
+// slab interval is widened by dt = 1e-5 * S * max|1/d| (S bounds every
+// coordinate involved), which exceeds the fp32 rounding error of each slab
+// bound (< 3 * 2^-24 * S * |1/d_a|) fifty-fold; an object it rejects can
+// therefore never pass the reference's fp64 test _window_hit(-tol, tmax),
+// and every object it accepts is re-classified exactly in fp64. Used only
+// for multi-object scenes (the single-object root is never box-tested) and
+// rays with no |d_a| below 1e-20 (fp32 reciprocal overflow).
+struct RayF {
+  float ix, iy, iz, ox_i, oy_i, oz_i, dt, tmax_ru;
+};
+
+__device__ __forceinline__ bool prefilter(const RayF& q, const float4 lo, const float4 hi) {
+  const float ax = fmaf(lo.x, q.ix, q.ox_i), bx = fmaf(hi.x, q.ix, q.ox_i);
+  const float ay = fmaf(lo.y, q.iy, q.oy_i), by = fmaf(hi.y, q.iy, q.oy_i);
+  const float az = fmaf(lo.z, q.iz, q.oz_i), bz = fmaf(hi.z, q.iz, q.oz_i);
+  const float t0 = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fminf(az, bz)) - q.dt;
+  const float t1 = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fmaxf(az, bz)) + q.dt;
+  return t1 >= t0 && t1 >= -1e-6f && t0 <= q.tmax_ru;
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, 2)
+gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
+                    const double* __restrict__ org, const double* __restrict__ dir,
+                    const double* __restrict__ tms, int64_t n, nif_gather_out out,
+                    unsigned long long* __restrict__ status, int* __restrict__ tile_ctr,
+                    int64_t n_tiles) {
+  __shared__ ObjC objs[kMaxObjFused];
+  __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
+  __shared__ float s_absmax;
+  __shared__ int s_tile;
+  __shared__ int s_warp[kThreads / 32];
+  __shared__ unsigned long long s_excl;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int n_obj = s.n_obj;
+  if (tid == 0) s_absmax = 0.f;
+  __syncthreads();
+  if (tid < n_obj) {
+    ObjC& b = objs[tid];
+    const int ob = s.t_order[tid];  // leaf (DFS) order
+    const double* bx = s.obox + (size_t)ob * 6;
+    float am = 0.f;
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = bx[a];
+      b.hi[a] = bx[3 + a];
+      b.lt[a] = bx[a] - s.tol;
+      b.ht[a] = bx[3 + a] + s.tol;
+      b.c[a] = 0.5 * (bx[a] + bx[3 + a]);
+      am = fmaxf(am, fmaxf(fabsf((float)bx[a]), fabsf((float)bx[3 + a])));
+    }
+    flo[tid] = make_float4((float)bx[0], (float)bx[1], (float)bx[2], 0.f);
+    fhi[tid] = make_float4((float)bx[3], (float)bx[4], (float)bx[5], 0.f);
+    const double hx = 0.5 * (bx[3] - bx[0]), hy = 0.5 * (bx[4] - bx[1]),
+                 hz = 0.5 * (bx[5] - bx[2]);
+    b.hn = sqrt(hx * hx + hy * hy + hz * hz);
+    b.id = ob;
+    b.route = route[ob];
+    b.root = s.roots[ob];
+    atomicMax(reinterpret_cast<int*>(&s_absmax), __float_as_int(am));
+  }
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t i = tile * kThreads + tid;
+  const bool valid = i < n;
+
+  RayX r{};
+  RayF q{};
+  bool use_pf = false;
+  if (valid) {
+    r.ox = org[i * 3 + 0];
+    r.oy = org[i * 3 + 1];
+    r.oz = org[i * 3 + 2];
+    r.dx = dir[i * 3 + 0];
+    r.dy = dir[i * 3 + 1];
+    r.dz = dir[i * 3 + 2];
+    r.tmax = tms[i];
+    r.ix = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
+    r.iy = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
+    r.iz = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
+    use_pf = n_obj > 1 && fabs(r.dx) > 1e-20 && fabs(r.dy) > 1e-20 && fabs(r.dz) > 1e-20;
+    if (use_pf) {
+      q.ix = (float)r.ix;
+      q.iy = (float)r.iy;
+      q.iz = (float)r.iz;
+      q.ox_i = -(float)r.ox * q.ix;
+      q.oy_i = -(float)r.oy * q.iy;
+      q.oz_i = -(float)r.oz * q.iz;
+      const float S = s_absmax + fmaxf(fmaxf(fabsf((float)r.ox), fabsf((float)r.oy)),
+                                       fabsf((float)r.oz)) + 1e-30f;
+      const float imax = fmaxf(fmaxf(fabsf(q.ix), fabsf(q.iy)), fabsf(q.iz));
+      q.dt = 1e-5f * S * imax;
+      q.tmax_ru = __double2float_ru(r.tmax);
+      use_pf = isfinite(q.dt);
+    }
+  }
+  // ---- classify (once) --------------------------------------------------
+  uint64_t mask = 0;   // 2 bits per object slot: 1 outer, 2 inner
+  uint32_t hyb = 0;    // routed-away candidates
+  int n_out = 0, n_in = 0;
+  const bool test_box = n_obj > 1;
+  if (valid) {
+    for (int k = 0; k < n_obj; ++k) {
+      if (use_pf && !prefilter(q, flo[k], fhi[k])) continue;
+      double t0;
+      const int kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
+      if (kind == 0) continue;
+      if (objs[k].route == 1) {
+        mask |= (uint64_t)kind << (2 * k);
+        if (kind == 1) ++n_out;
+        else ++n_in;
+      } else {
+        hyb |= 1u << k;
+      }
+    }
+  }
+  // ---- block scan of (outer, inner) counts, packed 16|16 ------------------
+  const int packed = (n_out << 16) | n_in;
+  int incl = packed;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  int warp_base = 0, block_total = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) warp_base += s_warp[w];
+    block_total += s_warp[w];
+  }
+  const int excl_in_block = warp_base + incl - packed;
+  // ---- publish the tile aggregate, then the hybrid any-hit ----------------
+  const uint64_t agg_o = (uint32_t)block_total >> 16, agg_i = (uint32_t)block_total & 0xffff;
+  if (tid == 0)
+    atomicExch(status + tile, pack(tile == 0 ? kFlagP : kFlagA, agg_o, agg_i));
+  if (valid) {
+    bool occ = false;
+    uint32_t h = hyb;
+    while (h != 0 && !occ) {
+      const int k = __ffs(h) - 1;
+      h &= h - 1;
+      occ = occluded_in_object(s.nodes, s.tris, objs[k].root, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz,
+                               s.eps, r.tmax);
+    }
+    out.bvh_occ[i] = occ ? 1 : 0;
+  }
+  // ---- decoupled look-back, one warp, 32 predecessors per probe -----------
+  if (warp == 0) {
+    uint32_t ex_o = 0, ex_i = 0;
+    if (tile > 0) {
+      int64_t base = tile - 1;
+      while (true) {
+        const int64_t j = base - lane;
+        uint64_t v = kFlagP;  // before tile 0: an inclusive prefix of zero
+        if (j >= 0) {
+          do {
+            v = *reinterpret_cast<volatile unsigned long long*>(status + j);
+          } while ((v >> 62) == 0);
+        }
+        const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int stop = pm ? __ffs(pm) - 1 : 31;
+        const uint32_t co = lane <= stop ? (uint32_t)((v >> 31) & kCntMask) : 0u;
+        const uint32_t ci = lane <= stop ? (uint32_t)(v & kCntMask) : 0u;
+        ex_o += __reduce_add_sync(0xffffffffu, co);
+        ex_i += __reduce_add_sync(0xffffffffu, ci);
+        if (pm) break;
+        base -= 32;
+      }
+      if (lane == 0) atomicExch(status + tile, pack(kFlagP, ex_o + agg_o, ex_i + agg_i));
+    }
+    if (lane == 0) {
+      if (tile == n_tiles - 1) {
+        out.counts[0] = (int64_t)(ex_o + agg_o);
+        out.counts[1] = (int64_t)(ex_i + agg_i);
+        out.counts[2] = (int64_t)(ex_o + agg_o) + (int64_t)(ex_i + agg_i);
+      }
+      s_excl = ((uint64_t)ex_o << 32) | ex_i;
+    }
+  }
+  __syncthreads();
+  if (!valid) return;
+  // ---- write records -------------------------------------------------------
+  int64_t jo = (int64_t)(s_excl >> 32) + (excl_in_block >> 16);
+  int64_t ji = (int64_t)(s_excl & 0xffffffffu) + (excl_in_block & 0xffff);
+  int64_t jt = jo + ji;
+  float du = 0.f, dv = 0.f;
+  if (!EXACT && mask != 0) sph32(r.dx, r.dy, r.dz, 1.0, &du, &dv);
+  int deg_count = 0;
+  uint64_t m = mask;
+  while (m != 0) {
+    const int bit = __ffsll((long long)m) - 1;
+    const int k = bit >> 1;
+    const int kind = (int)((m >> (2 * k)) & 3);
+    m &= ~(3ull << (2 * k));
+    const ObjC& b = objs[k];
+    double cc[5];
+    float c4[4], rr = 0.f;
+    bool deg;
+    if (kind == 1) {
+      const Hit3 hh = slab(r, b);
+      if (EXACT) {
+        deg = transform_outer(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, b.lo, b.hi, hh.t0, cc);
+        cc[4] = 0.0;
+      } else {
+        const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy,
+                     ez = r.oz + hh.t0 * r.dz;
+        const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
+        const double rn = sqrt(rx * rx + ry * ry + rz * rz);
+        deg = rn < kDegenerateRadius;
+        if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; }
+        else sph32(rx, ry, rz, rn, &c4[0], &c4[1]);
+        c4[2] = du;
+        c4[3] = dv;
+      }
+    } else {
+      if (EXACT) {
+        deg = transform_inner(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, b.lo, b.hi, cc);
+      } else {
+        const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
+        const double rn = sqrt(rx * rx + ry * ry + rz * rz);
+        deg = rn < kDegenerateRadius;
+        if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; rr = 0.f; }
+        else {
+          sph32(rx, ry, rz, rn, &c4[0], &c4[1]);
+          rr = (float)fmin(rn / b.hn, 1.0);
+        }
+        c4[2] = du;
+        c4[3] = dv;
+      }
+    }
+    if (EXACT) {
+      c4[0] = (float)cc[0];
+      c4[1] = (float)cc[1];
+      c4[2] = (float)cc[2];
+      c4[3] = (float)cc[3];
+      rr = (float)cc[4];
+    }
+    if (kind == 1) {
+      if (jo < out.cap_outer) {
+        out.outer_obj[jo] = b.id;
+        out.outer_ray[jo] = (int32_t)i;
+        reinterpret_cast<float4*>(out.outer_coord)[jo] = make_float4(c4[0], c4[1], c4[2], c4[3]);
+      }
+      ++jo;
+    } else {
+      if (ji < out.cap_inner) {
+        out.inner_obj[ji] = b.id;
+        out.inner_ray[ji] = (int32_t)i;
+        reinterpret_cast<float4*>(out.inner_coord)[ji] = make_float4(c4[0], c4[1], c4[2], c4[3]);
+        out.inner_r[ji] = rr;
+      }
+      ++ji;
+    }
+    if (EXACT && out.rec_kind != nullptr && jt < out.cap_total) {
+      out.rec_kind[jt] = kind == 1 ? 0 : 1;
+      out.rec_obj[jt] = b.id;
+      out.rec_ray[jt] = (int32_t)i;
+      for (int q = 0; q < 5; ++q) out.rec_coord[jt * 5 + q] = cc[q];
+    }
+    ++jt;
+    deg_count += deg ? 1 : 0;
+  }
+  if (deg_count) atomicAdd((unsigned long long*)(out.counts + 3), (unsigned long long)deg_count);
+}
+
+size_t fused_ws(int64_t n) {
+  const int64_t tiles = (n + kThreads - 1) / kThreads;
+  return align_up((size_t)(tiles > 0 ? tiles : 1) * 8, 256) + 256;
+}
+
+}  // namespace
+}  // namespace nif
+
+using namespace nif;
+
+extern "C" size_t nif_gather_workspace_bytes(int64_t n) {
+  const size_t a = gather_two_pass_workspace(n), b = fused_ws(n);
+  return a > b ? a : b;
+}
+
+extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
+                              const double* origins, const double* dirs, const double* tmaxs,
+                              int64_t n, const nif_gather_out* out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (n < 0) return fail(NIF_ERR_VALUE, "ray count cannot be negative");
+  if (n >= (int64_t)1 << 31) return fail(NIF_ERR_VALUE, "at most 2^31-1 rays per gather");
+  if ((uint64_t)n * (uint64_t)(s->n_obj > 0 ? s->n_obj : 1) >= ((uint64_t)1 << 31))
+    return fail(NIF_ERR_VALUE, "gather exceeds 2^31 record slots; split the ray batch");
+  if (workspace_bytes < nif_gather_workspace_bytes(n))
+    return fail(NIF_ERR_VALUE, "gather workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(out->counts, 0, 4 * sizeof(int64_t), st);
+  if (n == 0) return check_launch("gather(empty)");
+  if (s->n_obj > kMaxObjFused)
+    return gather_two_pass(s, route, origins, dirs, tmaxs, n, out, workspace, workspace_bytes,
+                           st);
+  const int64_t tiles = (n + kThreads - 1) / kThreads;
+  uint8_t* ws = (uint8_t*)workspace;
+  unsigned long long* status = (unsigned long long*)ws;
+  int* ctr = (int*)(ws + align_up((size_t)tiles * 8, 256));
+  cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
+  if (out->rec_kind != nullptr)
+    gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
+        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
+  else
+    gather_fused_kernel<false><<<(unsigned)tiles, kThreads, 0, st>>>(
+        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
+  return check_launch("nif_gather_dev");
+}

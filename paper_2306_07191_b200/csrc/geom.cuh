@@ -165,7 +165,7 @@ __device__ __forceinline__ bool transform_inner(double px, double py, double pz,
 
 // bvh.py:524-576 (_occluded_in_object): any-hit in one object's subtree
 // with t in (eps, t_max); children visited left first, right pushed.
-__device__ __noinline__ bool occluded_in_object(const nif_node* __restrict__ nodes,
+static __device__ __noinline__ bool occluded_in_object(const nif_node* __restrict__ nodes,
                                                 const double* __restrict__ tris, int root,
                                                 double ox, double oy, double oz, double dx,
                                                 double dy, double dz, double eps,
@@ -206,7 +206,7 @@ __device__ __noinline__ bool occluded_in_object(const nif_node* __restrict__ nod
 
 // bvh.py:454-521 (_closest_in_object): nearest triangle with t in
 // (eps, t_best); near child first, far child pushed with its entry t.
-__device__ __noinline__ int closest_in_object(const nif_node* __restrict__ nodes,
+static __device__ __noinline__ int closest_in_object(const nif_node* __restrict__ nodes,
                                               const double* __restrict__ tris, int root, double ox,
                                               double oy, double oz, double dx, double dy,
                                               double dz, double eps, double* t_best_io,

@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include "common.h"
+#include "kernels.h"
 #include "nif_b200.h"
 #include "status.h"
 #include "tc.cuh"
@@ -475,18 +476,6 @@ __global__ void occ_init_kernel(const uint8_t* __restrict__ src, int64_t n,
                                 uint8_t* __restrict__ dst) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = src ? src[i] : 0;
-}
-
-int g_sm_count = 0;
-
-int sm_count() {
-  if (g_sm_count == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sm_count <= 0) g_sm_count = 148;
-  }
-  return g_sm_count;
 }
 
 size_t tc_smem_bytes(const FastLayout& l) {

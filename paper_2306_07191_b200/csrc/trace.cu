@@ -436,40 +436,32 @@ size_t cub_scan_bytes(int64_t n) {
 
 using namespace nif;
 
-extern "C" size_t nif_gather_workspace_bytes(int64_t n) {
+namespace nif {
+size_t gather_two_pass_workspace(int64_t n) {
   const size_t a = align_up((size_t)(n > 0 ? n : 1) * sizeof(uint64_t), 256);
   return 2 * a + align_up(cub_scan_bytes(n), 256) + 256;
 }
 
-extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
-                              const double* origins, const double* dirs, const double* tmaxs,
-                              int64_t n, const nif_gather_out* out, void* workspace,
-                              size_t workspace_bytes, void* stream) {
-  if (n < 0) return fail(NIF_ERR_VALUE, "ray count cannot be negative");
-  if (n >= (int64_t)1 << 31) return fail(NIF_ERR_VALUE, "at most 2^31-1 rays per gather");
-  if ((uint64_t)n * (uint64_t)(s->n_obj > 0 ? s->n_obj : 1) >= ((uint64_t)1 << 32))
-    return fail(NIF_ERR_VALUE, "gather exceeds 2^32 record slots; split the ray batch");
-  if (workspace_bytes < nif_gather_workspace_bytes(n))
-    return fail(NIF_ERR_VALUE, "gather workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
+// Two-pass gather (count -> device scan -> write); used when the scene has
+// more objects than the fused single-pass kernel keeps in its mask.
+int gather_two_pass(const nif_scene_view* s, const uint8_t* route, const double* origins,
+                    const double* dirs, const double* tmaxs, int64_t n, const nif_gather_out* out,
+                    void* workspace, size_t workspace_bytes, cudaStream_t st) {
   uint8_t* ws = (uint8_t*)workspace;
   const size_t a = align_up((size_t)(n > 0 ? n : 1) * sizeof(uint64_t), 256);
   uint64_t* cnt = (uint64_t*)ws;
   uint64_t* off = (uint64_t*)(ws + a);
   void* tmp = ws + 2 * a;
   size_t tmp_bytes = workspace_bytes - 2 * a;
-  if (n == 0) {
-    cudaMemsetAsync(out->counts, 0, 4 * sizeof(int64_t), st);
-    return check_launch("gather(empty)");
-  }
   gather_count_kernel<<<grid_for(n, kGatherThreads), kGatherThreads, 0, st>>>(
       *s, route, origins, dirs, tmaxs, n, cnt, out->bvh_occ);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)n, st);
   gather_totals_kernel<<<1, 32, 0, st>>>(cnt, off, n, out->counts);
   gather_write_kernel<<<grid_for(n, kGatherThreads), kGatherThreads, 0, st>>>(
       *s, route, origins, dirs, tmaxs, n, off, *out);
-  return check_launch("nif_gather_dev");
+  return check_launch("nif_gather_dev(two-pass)");
 }
+}  // namespace nif
 
 extern "C" int nif_label_visible_dev(const nif_scene_view* s, const int32_t* rec_obj,
                                      const int32_t* rec_ray, int64_t m, const double* origins,
