@@ -193,6 +193,46 @@ int nif_query_dev(const nif_family_view* f, const int32_t* obj, const int32_t* r
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */
 int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray, void* stream);
 
+/* ---- training (nif.py:682-749 _train_batch, mlp.py:82-167,
+ *      grids.py:31-56 / 171-202) ------------------------------------------
+ * One family's optimiser state. params/grad/m/v are flat fp32 buffers of
+ * identical layout; the family view's pos/dir/dist/w/b point into params
+ * at the given element offsets. Step counters are per object grid set and
+ * per MLP head (every tensor of a set steps together in the reference). */
+typedef struct nif_train_view {
+  float* params;
+  float* grad;
+  float* m;
+  float* v;
+  int64_t numel;
+  int64_t off_pos, off_dir, off_dist, off_w, off_b;
+  int64_t* grid_steps;  /* [n_obj]   */
+  int64_t* mlp_steps;   /* [n_heads] */
+  int32_t* counts;      /* [n_obj] rows per object in the current batch */
+} nif_train_view;
+
+/* Per-object row counts of one (global) batch: counts[o] = #{r: obj[idx[r]] == o}
+ * (idx NULL: identity). The reference normalises each object group's
+ * loss by its own size (nif.py:686-692, mlp.py:166).                    */
+int nif_batch_counts_dev(const int64_t* obj, const int64_t* idx, int64_t n_rows, int32_t n_obj,
+                         int32_t* counts, void* stream);
+
+/* Fused forward + L2 loss + backward for rows idx[row0 + k*row_step]
+ * (data-parallel ranks take interleaved rows of the global batch).
+ * Accumulates MLP and grid gradients into t->grad and the sum of squared
+ * errors into *sq_err (device fp64). coord: [n][4|5] f64, label: [n] f32. */
+int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_view* t, const int64_t* obj,
+                         const double* coord, const float* label, const int64_t* idx,
+                         int64_t n_rows, int64_t row0, int64_t row_step, double* sq_err,
+                         void* stream);
+
+/* Adam (grids.py:31-45) on every touched object's grids (dense, all
+ * cells) and on each touched MLP head; fp64 moments over fp32 storage,
+ * numba's integer power for the bias correction; clears the gradients of
+ * the stepped tensors and the batch counts.                              */
+int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, double lr, double beta1,
+                 double beta2, double eps, void* stream);
+
 /* ---- shadow-ray generation (renderer.py:743-805 sample_pass) ---------- */
 typedef struct nif_camera {
   double pos[3];

@@ -182,14 +182,28 @@ class Adam:
     step_count: int = 0
 
 
+def int_power(a: float, e: int) -> float:
+    """numba's float ** int (numba/cpython/numbers.py int_power_impl):
+    binary exponentiation up to 0x10000, libm pow beyond."""
+    if e > 0x10000:
+        return math.pow(a, float(e))
+    r = 1.0
+    while e:
+        if e & 1:
+            r *= a
+        e >>= 1
+        a *= a
+    return r
+
+
 def adam_update(param, grad, m, v, p: Adam):
     """grids.py:31-56: fp64 moments over fp32 storage, bias corrected,
-    gradient cleared."""
+    gradient cleared. `b1 ** t` is numba's integer power."""
     p.step_count += 1
     t = p.step_count
     b1, b2, lr, eps = p.beta1, p.beta2, p.learning_rate, p.epsilon
-    c1 = 1.0 - b1 ** t
-    c2 = 1.0 - b2 ** t
+    c1 = 1.0 - int_power(b1, t)
+    c2 = 1.0 - int_power(b2, t)
     g = grad.astype(np.float64)
     mi = b1 * m.astype(np.float64) + (1.0 - b1) * g
     vi = b2 * v.astype(np.float64) + (1.0 - b2) * g * g
@@ -361,8 +375,9 @@ class OModel:
             for gr in g.values():
                 gr.adam = Adam(lr, beta1, beta2, eps)
 
-    def train_batch(self, which, obj, coord, label) -> float:
-        """nif.py:682-749 _train_batch (shared sharing mode)."""
+    def train_batch(self, which, obj, coord, label, apply=True) -> float:
+        """nif.py:682-749 _train_batch (shared sharing mode). apply=False
+        stops before the Adam updates (gradients left in the .grad arrays)."""
         order = np.argsort(obj, kind="stable")
         obj, coord, label = obj[order], coord[order], label[order]
         bounds = np.flatnonzero(np.diff(obj)) + 1
@@ -400,6 +415,8 @@ class OModel:
                 grad_2d(g["inner_dir"], uv_d, gx[:, n_lat:2 * n_lat])
                 grad_1d(g["inner_dist"], r, gx[:, 2 * n_lat:])
             total += loss * (b - a)
+        if not apply:
+            return total / len(obj)
         for o in touched:
             g = self.grids[o]
             names = ("outer_pos", "outer_dir") if which == "outer" else (

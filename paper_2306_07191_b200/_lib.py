@@ -83,8 +83,10 @@ class PassOut(C.Structure):
 
 class TrainView(C.Structure):
     _fields_ = [
-        ("grad_pos", C.c_void_p), ("grad_dir", C.c_void_p), ("grad_dist", C.c_void_p),
-        ("grad_w", C.c_void_p), ("grad_b", C.c_void_p),
+        ("params", C.c_void_p), ("grad", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p),
+        ("numel", C.c_int64), ("off_pos", C.c_int64), ("off_dir", C.c_int64),
+        ("off_dist", C.c_int64), ("off_w", C.c_int64), ("off_b", C.c_int64),
+        ("grid_steps", C.c_void_p), ("mlp_steps", C.c_void_p), ("counts", C.c_void_p),
     ]
 
 
@@ -141,6 +143,10 @@ _SIGS = {
     "nif_fast_pack_dev": (C.c_int, [C.POINTER(FamilyView), P, P]),
     "nif_query_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, I32, P]),
     "nif_occ_init_dev": (C.c_int, [P, I64, P, P]),
+    "nif_batch_counts_dev": (C.c_int, [P, P, I64, I32, P, P]),
+    "nif_train_fwdbwd_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
+                                       I64, I64, I64, P, P]),
+    "nif_adam_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), D, D, D, D, P]),
     "nif_sample_pass_dev": (C.c_int, [C.POINTER(SceneView), C.POINTER(Camera),
                                       C.POINTER(LightsView), I64, I64, I32, I64, I64,
                                       C.POINTER(PassOut), P]),

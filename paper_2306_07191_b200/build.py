@@ -20,8 +20,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-EXACT_UNITS = ["trace.cu", "exact.cu", "gather.cu"]
-FAST_UNITS = ["query.cu", "train.cu"]
+EXACT_UNITS = ["trace.cu", "exact.cu", "gather.cu", "train.cu"]
+FAST_UNITS = ["query.cu"]
 HOST_UNITS = ["sah_builder.cpp", "api.cpp"]
 
 

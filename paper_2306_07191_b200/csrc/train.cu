@@ -1,0 +1,471 @@
+// Online training step on the device: per-object batch counts, the fused
+// encode -> MLP forward -> L2 loss -> backward -> grid-gradient scatter
+// kernel, and the multi-tensor Adam (nif.py:682-749 _train_batch,
+// mlp.py:82-167, grids.py:31-56 / 153-202).
+//
+// Compiled with -fmad=false so the grid interpolation weights and the
+// Adam update evaluate exactly the reference's fp64 expressions; the MLP
+// accumulations use explicit fmaf (fp32, like the reference's sgemm).
+//
+// Layout of the fused kernel: one CTA per RB rows (one row per thread).
+// Pre-activations of every hidden layer stay in shared memory (rows padded
+// to W+1 floats: conflict-free per-row access), so the backward pass needs
+// no recomputation; weight gradients are CTA-level reductions over the RB
+// rows (dz^T a), flushed with one fp32 atomic per weight per CTA. Grid
+// gradients are fp32 atomics of (fp64 weight * upstream) rounded to fp32,
+// the reference's np.add.at contributions.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+#include "kernels.h"
+#include "nif_b200.h"
+#include "status.h"
+
+namespace nif {
+namespace {
+
+constexpr float kSlope = 0.01f;
+constexpr int kMaxIn = 16;
+constexpr int kMaxOut = 4;
+
+__device__ __forceinline__ float leaky(float z) { return z > 0.f ? z : z * kSlope; }
+
+struct Axis {
+  int i0, i1;
+  double w;
+};
+
+// grids.py:125-138
+__device__ __forceinline__ Axis axis_indices(double x, int R, bool wrap) {
+  const double xc = x * (double)R - 0.5;
+  const double x0 = floor(xc);
+  Axis a;
+  a.w = xc - x0;
+  long long i0 = (long long)x0, i1 = i0 + 1;
+  if (wrap) {
+    i0 = ((i0 % R) + R) % R;
+    i1 = ((i1 % R) + R) % R;
+  } else {
+    i0 = i0 < 0 ? 0 : (i0 > R - 1 ? R - 1 : i0);
+    i1 = i1 < 0 ? 0 : (i1 > R - 1 ? R - 1 : i1);
+  }
+  a.i0 = (int)i0;
+  a.i1 = (int)i1;
+  return a;
+}
+
+struct Bil64 {
+  int c[4];        // flat cell index of corners 00, 01, 10, 11
+  double w[4];
+};
+
+__device__ __forceinline__ Bil64 bil64(double u, double v, int R) {
+  const Axis au = axis_indices(u, R, true), av = axis_indices(v, R, false);
+  Bil64 b;
+  b.c[0] = au.i0 * R + av.i0;
+  b.c[1] = au.i0 * R + av.i1;
+  b.c[2] = au.i1 * R + av.i0;
+  b.c[3] = au.i1 * R + av.i1;
+  b.w[0] = (1.0 - au.w) * (1.0 - av.w);
+  b.w[1] = (1.0 - au.w) * av.w;
+  b.w[2] = au.w * (1.0 - av.w);
+  b.w[3] = au.w * av.w;
+  return b;
+}
+
+struct TrainArgs {
+  nif_family_view f;
+  nif_train_view t;
+  const int64_t* obj;
+  const double* coord;
+  const float* label;
+  const int64_t* idx;
+  int64_t n_rows, row0, row_step;
+  double* sq_err;
+};
+
+template <int W>
+__global__ void train_fwdbwd_kernel(TrainArgs a) {
+  extern __shared__ float sm[];
+  const int RB = blockDim.x;
+  const int tid = threadIdx.x;
+  const int WP = W + 1;
+  const nif_family_view& f = a.f;
+  const int L = f.n_layers - 1;    // hidden layers
+  const int IN = f.dims[0];
+  const int OUT = f.dims[f.n_layers];
+  float* zs = sm;                          // [L][RB][WP]
+  float* dzA = zs + (size_t)L * RB * WP;   // [RB][WP]
+  float* dzB = dzA + (size_t)RB * WP;      // [RB][WP]
+  float* xs = dzB + (size_t)RB * WP;       // [RB][kMaxIn]
+  float* dh = xs + (size_t)RB * kMaxIn;    // [RB][kMaxOut]
+
+  const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
+  const int64_t g = a.row0 + k_row * a.row_step;
+  const bool valid = k_row * a.row_step + a.row0 < a.n_rows && g < a.n_rows;
+  const int64_t row = valid ? (a.idx ? a.idx[g] : g) : 0;
+  const int o = valid ? (int)a.obj[row] : 0;
+  const int head = f.n_heads > 1 ? o : 0;
+  const float* Wt = f.w + (size_t)head * f.w_stride;
+  const float* Bt = f.b + (size_t)head * f.b_stride;
+  float* gW = a.t.grad + a.t.off_w + (size_t)head * f.w_stride;
+  float* gB = a.t.grad + a.t.off_b + (size_t)head * f.b_stride;
+  const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
+
+  // ---- encode (grids.py:141-191: fp64 weights, fp64 sum, fp32 result) ----
+  float x[kMaxIn];
+#pragma unroll
+  for (int k = 0; k < kMaxIn; ++k) x[k] = 0.f;
+  Bil64 bp{}, bd{};
+  Axis ad{};
+  if (valid) {
+    const double* c = a.coord + row * cw;
+    const size_t g2 = (size_t)f.R * f.R * f.N;
+    const float* gp = f.pos + (size_t)o * g2;
+    const float* gd = f.dir + (size_t)o * g2;
+    bp = bil64(c[0], c[1], f.R);
+    bd = bil64(c[2], c[3], f.R);
+    for (int k = 0; k < f.N; ++k) {
+      const double sp = bp.w[0] * (double)gp[(size_t)bp.c[0] * f.N + k] +
+                        bp.w[1] * (double)gp[(size_t)bp.c[1] * f.N + k] +
+                        bp.w[2] * (double)gp[(size_t)bp.c[2] * f.N + k] +
+                        bp.w[3] * (double)gp[(size_t)bp.c[3] * f.N + k];
+      const double sd = bd.w[0] * (double)gd[(size_t)bd.c[0] * f.N + k] +
+                        bd.w[1] * (double)gd[(size_t)bd.c[1] * f.N + k] +
+                        bd.w[2] * (double)gd[(size_t)bd.c[2] * f.N + k] +
+                        bd.w[3] * (double)gd[(size_t)bd.c[3] * f.N + k];
+      x[k] = (float)sp;
+      x[f.N + k] = (float)sd;
+    }
+    if (f.family == NIF_FAMILY_INNER) {
+      ad = axis_indices(c[4], f.Rd, false);
+      const float* gr = f.dist + (size_t)o * f.Rd * f.Nd;
+      for (int k = 0; k < f.Nd; ++k) {
+        const double s = (1.0 - ad.w) * (double)gr[(size_t)ad.i0 * f.Nd + k] +
+                         ad.w * (double)gr[(size_t)ad.i1 * f.Nd + k];
+        x[2 * f.N + k] = (float)s;
+      }
+    }
+  }
+  for (int k = 0; k < IN; ++k) xs[tid * kMaxIn + k] = x[k];
+
+  // ---- forward -------------------------------------------------------------
+  {  // layer 0
+    float* z = zs + (size_t)tid * WP;
+    for (int j = 0; j < W; ++j) {
+      float acc = __ldg(Bt + j);
+      const float* wr = Wt + (size_t)j * IN;
+      for (int k = 0; k < IN; ++k) acc = fmaf(__ldg(wr + k), x[k], acc);
+      z[j] = acc;
+    }
+  }
+  size_t wo = (size_t)IN * W, bo = W;
+  for (int l = 1; l < L; ++l) {
+    const float* zp = zs + ((size_t)(l - 1) * RB + tid) * WP;
+    float* z = zs + ((size_t)l * RB + tid) * WP;
+    for (int j = 0; j < W; ++j) {
+      float acc = __ldg(Bt + bo + j);
+      const float* wr = Wt + wo + (size_t)j * W;
+      for (int k = 0; k < W; ++k) acc = fmaf(__ldg(wr + k), leaky(zp[k]), acc);
+      z[j] = acc;
+    }
+    wo += (size_t)W * W;
+    bo += W;
+  }
+  // head + loss (mlp.py:91-101, 159-167)
+  const size_t wo_h = wo, bo_h = bo;
+  {
+    const float* zp = zs + ((size_t)(L - 1) * RB + tid) * WP;
+    const int n_o = valid ? a.t.counts[o] : 1;
+    const float scale = (float)(2.0 / ((double)n_o * OUT));  // pred.dtype.type(2.0/diff.size)
+    double sq = 0.0;
+    for (int q = 0; q < OUT; ++q) {
+      float acc = __ldg(Bt + bo_h + q);
+      const float* wr = Wt + wo_h + (size_t)q * W;
+      for (int k = 0; k < W; ++k) acc = fmaf(__ldg(wr + k), leaky(zp[k]), acc);
+      float out, dz;
+      const float lab = valid ? a.label[row * OUT + q] : 0.f;
+      if (f.sigmoid_head) {
+        out = acc >= 0.f ? 1.f / (1.f + expf(-acc)) : expf(acc) / (1.f + expf(acc));
+        const float diff = out - lab;
+        sq += (double)diff * (double)diff;
+        const float gout = diff * scale;
+        dz = gout * out * (1.f - out);
+      } else {
+        out = acc;
+        const float diff = out - lab;
+        sq += (double)diff * (double)diff;
+        dz = diff * scale;
+      }
+      dh[tid * kMaxOut + q] = valid ? dz : 0.f;
+    }
+    if (valid) atomicAdd(a.sq_err, sq);
+  }
+  // da for the last hidden layer -> dz_{L-1}
+  {
+    const float* zp = zs + ((size_t)(L - 1) * RB + tid) * WP;
+    float* dz = dzA + (size_t)tid * WP;
+    for (int k = 0; k < W; ++k) {
+      float da = 0.f;
+      for (int q = 0; q < OUT; ++q) da = fmaf(dh[tid * kMaxOut + q], __ldg(Wt + wo_h + q * W + k), da);
+      dz[k] = zp[k] > 0.f ? da : da * kSlope;
+    }
+  }
+  __syncthreads();
+  // head gradients: gW[q][k] = sum_r dh[r][q] * a_{L-1}[r][k]
+  for (int e = tid; e < OUT * (W + 1); e += RB) {
+    const int q = e / (W + 1), k = e % (W + 1);
+    float s = 0.f;
+    if (k < W) {
+      for (int r = 0; r < RB; ++r)
+        s = fmaf(dh[r * kMaxOut + q], leaky(zs[((size_t)(L - 1) * RB + r) * WP + k]), s);
+      atomicAdd(gW + wo_h + q * W + k, s);
+    } else {
+      for (int r = 0; r < RB; ++r) s += dh[r * kMaxOut + q];
+      atomicAdd(gB + bo_h + q, s);
+    }
+  }
+  // hidden layers L-1 .. 1
+  float* dzc = dzA;
+  float* dzn = dzB;
+  for (int l = L - 1; l >= 1; --l) {
+    wo -= (size_t)W * W;
+    bo -= W;
+    // weight grads of dense layer l: sum_r dz_l[r][j] * a_{l-1}[r][k]
+    for (int e = tid; e < W * (W + 1); e += RB) {
+      const int j = e / (W + 1), k = e % (W + 1);
+      float s = 0.f;
+      if (k < W) {
+        for (int r = 0; r < RB; ++r)
+          s = fmaf(dzc[(size_t)r * WP + j], leaky(zs[((size_t)(l - 1) * RB + r) * WP + k]), s);
+        atomicAdd(gW + wo + (size_t)j * W + k, s);
+      } else {
+        for (int r = 0; r < RB; ++r) s += dzc[(size_t)r * WP + j];
+        atomicAdd(gB + bo + j, s);
+      }
+    }
+    // dz_{l-1} = mask(z_{l-1}) * (dz_l W_l)
+    {
+      const float* zp = zs + ((size_t)(l - 1) * RB + tid) * WP;
+      const float* dc = dzc + (size_t)tid * WP;
+      float* dn = dzn + (size_t)tid * WP;
+      for (int k = 0; k < W; ++k) {
+        float da = 0.f;
+        for (int j = 0; j < W; ++j) da = fmaf(dc[j], __ldg(Wt + wo + (size_t)j * W + k), da);
+        dn[k] = zp[k] > 0.f ? da : da * kSlope;
+      }
+    }
+    __syncthreads();
+    float* tmp = dzc;
+    dzc = dzn;
+    dzn = tmp;
+  }
+  // layer 0 weight grads: sum_r dz_0[r][j] * x[r][k]
+  for (int e = tid; e < W * (IN + 1); e += RB) {
+    const int j = e / (IN + 1), k = e % (IN + 1);
+    float s = 0.f;
+    if (k < IN) {
+      for (int r = 0; r < RB; ++r) s = fmaf(dzc[(size_t)r * WP + j], xs[r * kMaxIn + k], s);
+      atomicAdd(gW + (size_t)j * IN + k, s);
+    } else {
+      for (int r = 0; r < RB; ++r) s += dzc[(size_t)r * WP + j];
+      atomicAdd(gB + j, s);
+    }
+  }
+  if (!valid) return;
+  // input gradient dx = dz_0 W_0 -> grid scatter (grids.py:171-202)
+  float dx[kMaxIn];
+  for (int k = 0; k < IN; ++k) {
+    float s = 0.f;
+    const float* dc = dzc + (size_t)tid * WP;
+    for (int j = 0; j < W; ++j) s = fmaf(dc[j], __ldg(Wt + (size_t)j * IN + k), s);
+    dx[k] = s;
+  }
+  const size_t g2 = (size_t)f.R * f.R * f.N;
+  float* gpos = a.t.grad + a.t.off_pos + (size_t)o * g2;
+  float* gdir = a.t.grad + a.t.off_dir + (size_t)o * g2;
+  for (int c = 0; c < 4; ++c)
+    for (int k = 0; k < f.N; ++k) {
+      atomicAdd(gpos + (size_t)bp.c[c] * f.N + k, (float)(bp.w[c] * (double)dx[k]));
+      atomicAdd(gdir + (size_t)bd.c[c] * f.N + k, (float)(bd.w[c] * (double)dx[f.N + k]));
+    }
+  if (f.family == NIF_FAMILY_INNER) {
+    float* gr = a.t.grad + a.t.off_dist + (size_t)o * f.Rd * f.Nd;
+    for (int k = 0; k < f.Nd; ++k) {
+      atomicAdd(gr + (size_t)ad.i0 * f.Nd + k, (float)((1.0 - ad.w) * (double)dx[2 * f.N + k]));
+      atomicAdd(gr + (size_t)ad.i1 * f.Nd + k, (float)(ad.w * (double)dx[2 * f.N + k]));
+    }
+  }
+}
+
+__global__ void batch_counts_kernel(const int64_t* __restrict__ obj, const int64_t* __restrict__ idx,
+                                    int64_t n, int n_obj, int32_t* __restrict__ counts) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t o = obj[idx ? idx[r] : r];
+  if (o >= 0 && o < n_obj) atomicAdd(counts + o, 1);
+}
+
+// numba's float ** int (int_power_impl): binary exponentiation, libm pow
+// beyond 0x10000.
+__device__ __forceinline__ double int_power(double a, long long e) {
+  if (e > 0x10000) return pow(a, (double)e);
+  double r = 1.0;
+  while (e) {
+    if (e & 1) r *= a;
+    e >>= 1;
+    a *= a;
+  }
+  return r;
+}
+
+struct AdamSeg {
+  int64_t off, per, n_units;  // element offset, elements per unit, units
+  int kind;                   // 0 grid (unit = object), 1 mlp (unit = head)
+};
+
+__global__ void adam_steps_kernel(nif_train_view t, int n_obj, int n_heads, int shared) {
+  const int i = threadIdx.x + blockIdx.x * blockDim.x;
+  if (i < n_obj && t.counts[i] > 0) t.grid_steps[i] += 1;
+  if (i < n_heads) {
+    const bool touched = shared ? true : t.counts[i] > 0;
+    if (touched) t.mlp_steps[i] += 1;
+  }
+}
+
+// grids.py:31-45 _adam_update per element
+__global__ void adam_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1, AdamSeg s2, AdamSeg s3,
+                            AdamSeg s4, int nseg, int shared, double lr, double b1, double b2,
+                            double eps) {
+  const AdamSeg segs[5] = {s0, s1, s2, s3, s4};
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;; e += (int64_t)gridDim.x * blockDim.x) {
+    // locate the segment
+    int64_t base = 0;
+    int sid = -1;
+    int64_t local = 0;
+    for (int q = 0; q < nseg; ++q) {
+      const int64_t len = segs[q].per * segs[q].n_units;
+      if (e < base + len) {
+        sid = q;
+        local = e - base;
+        break;
+      }
+      base += len;
+    }
+    if (sid < 0) return;
+    const AdamSeg& sg = segs[sid];
+    const int64_t unit = local / sg.per;
+    int64_t step;
+    if (sg.kind == 0) {
+      if (t.counts[unit] <= 0) continue;
+      step = t.grid_steps[unit];
+    } else {
+      if (!shared && t.counts[unit] <= 0) continue;
+      step = t.mlp_steps[unit];
+    }
+    const double c1 = 1.0 - int_power(b1, step);
+    const double c2 = 1.0 - int_power(b2, step);
+    const int64_t p = sg.off + local;
+    const double g = (double)t.grad[p] * 1.0;
+    const double mi = b1 * ((double)t.m[p] * 1.0) + (1.0 - b1) * g;
+    const double vi = b2 * ((double)t.v[p] * 1.0) + (1.0 - b2) * g * g;
+    t.m[p] = (float)mi;
+    t.v[p] = (float)vi;
+    const double mh = mi / c1;
+    const double vh = vi / c2;
+    t.params[p] = (float)((double)t.params[p] - lr * mh / (sqrt(vh) + eps));
+    t.grad[p] = 0.f;
+  }
+}
+
+__global__ void clear_counts_kernel(int32_t* counts, int n) {
+  const int i = threadIdx.x + blockIdx.x * blockDim.x;
+  if (i < n) counts[i] = 0;
+}
+
+template <int W>
+int launch_fwdbwd(const TrainArgs& a, cudaStream_t st) {
+  const int L = a.f.n_layers - 1;
+  int rb = 128;
+  auto smem_for = [&](int r) {
+    return ((size_t)L * r * (W + 1) + 2 * (size_t)r * (W + 1) + (size_t)r * kMaxIn +
+            (size_t)r * kMaxOut) * sizeof(float);
+  };
+  while (rb > 32 && smem_for(rb) > 200 * 1024) rb /= 2;
+  const size_t smem = smem_for(rb);
+  if (smem > 220 * 1024) return fail(NIF_ERR_UNSUPPORTED, "MLP too large for the training kernel");
+  auto kern = train_fwdbwd_kernel<W>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
+  if (my_rows <= 0) return NIF_OK;
+  const unsigned grid = (unsigned)((my_rows + rb - 1) / rb);
+  kern<<<grid, rb, smem, st>>>(a);
+  return check_launch("nif_train_fwdbwd_dev");
+}
+
+}  // namespace
+}  // namespace nif
+
+using namespace nif;
+
+extern "C" int nif_batch_counts_dev(const int64_t* obj, const int64_t* idx, int64_t n_rows,
+                                    int32_t n_obj, int32_t* counts, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_rows <= 0) return NIF_OK;
+  batch_counts_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(obj, idx, n_rows, n_obj,
+                                                                        counts);
+  return check_launch("nif_batch_counts_dev");
+}
+
+extern "C" int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_view* t,
+                                    const int64_t* obj, const double* coord, const float* label,
+                                    const int64_t* idx, int64_t n_rows, int64_t row0,
+                                    int64_t row_step, double* sq_err, void* stream) {
+  if (n_rows <= 0) return NIF_OK;
+  if (f->n_layers < 2) return fail(NIF_ERR_UNSUPPORTED, "training needs at least one hidden layer");
+  if (f->dims[0] > kMaxIn) return fail(NIF_ERR_UNSUPPORTED, "input width above %d", kMaxIn);
+  if (f->dims[f->n_layers] > kMaxOut) return fail(NIF_ERR_UNSUPPORTED, "head wider than %d", kMaxOut);
+  for (int i = 2; i < f->n_layers; ++i)
+    if (f->dims[i] != f->dims[1]) return fail(NIF_ERR_UNSUPPORTED, "hidden widths must match");
+  if (row_step < 1 || row0 < 0) return fail(NIF_ERR_VALUE, "bad row partition");
+  TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err};
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->dims[1]) {
+    case 8: return launch_fwdbwd<8>(a, st);
+    case 16: return launch_fwdbwd<16>(a, st);
+    case 32: return launch_fwdbwd<32>(a, st);
+    case 48: return launch_fwdbwd<48>(a, st);
+    case 64: return launch_fwdbwd<64>(a, st);
+    case 96: return launch_fwdbwd<96>(a, st);
+    case 128: return launch_fwdbwd<128>(a, st);
+    default: return fail(NIF_ERR_UNSUPPORTED, "hidden width %d not instantiated", f->dims[1]);
+  }
+}
+
+extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, double lr,
+                            double beta1, double beta2, double eps, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_heads = f->n_heads;
+  const int shared = n_heads == 1;
+  const int n = f->n_obj > n_heads ? f->n_obj : n_heads;
+  adam_steps_kernel<<<(n + 127) / 128, 128, 0, st>>>(*t, f->n_obj, n_heads, shared);
+  AdamSeg s[5];
+  int ns = 0;
+  const int64_t g2 = (int64_t)f->R * f->R * f->N;
+  s[ns++] = {t->off_pos, g2, f->n_obj, 0};
+  s[ns++] = {t->off_dir, g2, f->n_obj, 0};
+  if (f->family == NIF_FAMILY_INNER) s[ns++] = {t->off_dist, (int64_t)f->Rd * f->Nd, f->n_obj, 0};
+  s[ns++] = {t->off_w, f->w_stride, n_heads, 1};
+  s[ns++] = {t->off_b, f->b_stride, n_heads, 1};
+  while (ns < 5) s[ns++] = {0, 1, 0, 1};
+  int64_t total = 0;
+  for (int q = 0; q < 5; ++q) total += s[q].per * s[q].n_units;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  adam_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(
+      *t, s[0], s[1], s[2], s[3], s[4], 5, shared, lr, beta1, beta2, eps);
+  clear_counts_kernel<<<(f->n_obj + 127) / 128, 128, 0, st>>>(t->counts, f->n_obj);
+  return check_launch("nif_adam_dev");
+}

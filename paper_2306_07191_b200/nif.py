@@ -212,11 +212,30 @@ class FamilyParams:
         self.grad = torch.zeros_like(self.params)
         self.m = torch.zeros_like(self.params)
         self.v = torch.zeros_like(self.params)
-        # per-tensor Adam step counters: one per object grid, one per head MLP
-        self.grid_steps = np.zeros(n_obj, np.int64)
-        self.mlp_steps = np.zeros(n_heads, np.int64)
+        # per-tensor Adam step counters (device): one per object grid set,
+        # one per head MLP; batch row counts per object
+        self.grid_steps = torch.zeros(n_obj, dtype=torch.int64, device=device)
+        self.mlp_steps = torch.zeros(n_heads, dtype=torch.int64, device=device)
+        self.counts = torch.zeros(n_obj, dtype=torch.int32, device=device)
         self._fast = None
         self.dirty = True
+
+    def train_view(self):
+        t = _lib.TrainView()
+        t.params = _lib.ptr(self.params)
+        t.grad = _lib.ptr(self.grad)
+        t.m = _lib.ptr(self.m)
+        t.v = _lib.ptr(self.v)
+        t.numel = self.numel
+        t.off_pos = self.offsets["pos"][0]
+        t.off_dir = self.offsets["dir"][0]
+        t.off_dist = self.offsets["dist"][0]
+        t.off_w = self.offsets["w"][0]
+        t.off_b = self.offsets["b"][0]
+        t.grid_steps = _lib.ptr(self.grid_steps)
+        t.mlp_steps = _lib.ptr(self.mlp_steps)
+        t.counts = _lib.ptr(self.counts)
+        return t
 
     def part(self, key, t=None):
         off, size = self.offsets[key]

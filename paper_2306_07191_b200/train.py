@@ -1,0 +1,270 @@
+"""Online training on the device: sample collection (BVH labels), the
+per-batch optimiser step and the epoch loop (nif.py:507-795).
+
+Samples stay in HBM. The epoch loop reproduces the reference's schedule
+exactly -- per-epoch RNG `default_rng(SeedSequence([seed, 0x7472])
+.spawn(epochs)[e])`, outer family permuted first then inner with the same
+generator, batches `perm[k:k+bs]` -- and every batch runs as four
+stream-ordered launches (batch counts, fused forward/backward + grid
+scatter, Adam over touched grids + MLP) with no host synchronisation until
+the epoch's losses are read back.
+
+Data parallel (torch.distributed over NCCL): every rank holds the same
+sample set and the same global permutation; rank r processes rows
+r, r+W, r+2W, ... of each global batch (per-object normalisation uses the
+global batch counts), the flat fp32 gradient buffer of the family plus the
+squared-error accumulator are summed with one all-reduce, and every rank
+applies the identical Adam update, so replicas stay identical without a
+broadcast.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .nif import NifModel
+from .scene import Scene
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class SampleSet:
+    """nif.py:507-529, arrays as device tensors (host copies on demand)."""
+
+    head: str
+    outer_obj: object
+    outer_coord: object   # (n, 4) f64
+    outer_label: object   # (n,) f32
+    outer_ray: object
+    inner_obj: object
+    inner_coord: object   # (m, 5) f64
+    inner_label: object
+    inner_ray: object
+    n_rays: int = 0
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def n_outer(self) -> int:
+        return int(self.outer_obj.shape[0])
+
+    @property
+    def n_inner(self) -> int:
+        return int(self.inner_obj.shape[0])
+
+    def host(self):
+        return {k: getattr(self, k).cpu().numpy() for k in (
+            "outer_obj", "outer_coord", "outer_label", "outer_ray", "inner_obj", "inner_coord",
+            "inner_label", "inner_ray")}
+
+    @staticmethod
+    def from_host(d: dict, head="occlusion", device=None) -> "SampleSet":
+        torch = _torch()
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        dt = {"outer_obj": np.int64, "inner_obj": np.int64, "outer_ray": np.int64,
+              "inner_ray": np.int64, "outer_coord": np.float64, "inner_coord": np.float64,
+              "outer_label": np.float32, "inner_label": np.float32}
+        t = {k: torch.from_numpy(np.ascontiguousarray(d[k], dt[k])).to(dev) for k in dt}
+        return SampleSet(head, **t)
+
+
+def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "importance",
+                    labeler=None, seed: Optional[int] = None,
+                    threads: Optional[int] = None) -> SampleSet:
+    """nif.py:569-674 on the device: per sample index, the primary pass,
+    every hit pixel's shadow ray (no cosine filter), the gather in the
+    reference's record order and per-object BVH labels (1 = visible)."""
+    torch = _torch()
+    from .pipeline import GatherBuffers, gather_dev, sample_pass_dev
+    camera = camera or scene.camera
+    if camera is None:
+        raise ValueError("no camera given and the scene has none")
+    if sampler not in ("importance", "uniform"):
+        raise ValueError(f"unknown sampler {sampler!r}")
+    if labeler not in (None,):
+        raise NotImplementedError("custom labelers / the geometry head are not on the device path")
+    if not scene.lights:
+        raise ValueError("sample collection needs at least one light")
+    seed = scene.seed if seed is None else seed
+    ds = scene.device()
+    dev = ds.device
+    route = scene.nif_enabled.copy()
+    n_pix = camera.width * camera.height
+    acc = {k: [] for k in ("oo", "oc", "ol", "or_", "io", "ic", "il", "ir")}
+    n_rays = shadow_rays = degenerate = 0
+    L = _lib.lib()
+    for s in range(spp):
+        data = sample_pass_dev(scene, camera, s, seed, sampler)
+        mask = data["hit"] != 0
+        idx = mask.nonzero().squeeze(1)
+        n = int(idx.numel())
+        if n == 0:
+            continue
+        o = data["point"][idx].contiguous()
+        d = data["ldir"][idx].contiguous()
+        t = data["tmax"][idx].contiguous()
+        buf = GatherBuffers(n, int(route.sum()), dev, interleaved=True)
+        gather_dev(ds, ds.route(route), o, d, t, n, buf)
+        counts = buf.counts.cpu().numpy()
+        m = int(counts[2])
+        shadow_rays += n
+        degenerate += int(counts[3])
+        if m == 0:
+            continue
+        rec_obj = buf.rec_obj[:m]
+        rec_ray = buf.rec_ray[:m]
+        vis = torch.empty(m, dtype=torch.uint8, device=dev)
+        L.nif_label_visible_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m, _lib.ptr(o),
+                                _lib.ptr(d), _lib.ptr(t), _lib.ptr(vis), _lib.stream_ptr())
+        kind = buf.rec_kind[:m]
+        coord = buf.rec_coord[:m * 5].view(m, 5)
+        ray_ids = s * n_pix + idx
+        for k, (ko, kc, kl, kr), width in ((0, ("oo", "oc", "ol", "or_"), 4),
+                                           (1, ("io", "ic", "il", "ir"), 5)):
+            sel = (kind == k).nonzero().squeeze(1)
+            if sel.numel() == 0:
+                continue
+            acc[ko].append(rec_obj[sel].long())
+            acc[kc].append(coord[sel, :width].contiguous())
+            acc[kl].append(vis[sel].float())
+            acc[kr].append(ray_ids[rec_ray[sel].long()])
+        n_rays += n
+
+    def cat(key, tail, dt):
+        if acc[key]:
+            return torch.cat(acc[key]).contiguous()
+        return torch.zeros((0,) + tail, dtype=dt, device=dev)
+
+    out = SampleSet("occlusion", cat("oo", (), torch.int64), cat("oc", (4,), torch.float64),
+                    cat("ol", (), torch.float32), cat("or_", (), torch.int64),
+                    cat("io", (), torch.int64), cat("ic", (5,), torch.float64),
+                    cat("il", (), torch.float32), cat("ir", (), torch.int64), n_rays=n_rays)
+    out.stats = {"pixel_samples": spp * n_pix, "shadow_rays": shadow_rays,
+                 "degenerate_queries": degenerate,
+                 "outer_per_object": np.bincount(out.outer_obj.cpu().numpy(),
+                                                 minlength=scene.n_objects),
+                 "inner_per_object": np.bincount(out.inner_obj.cpu().numpy(),
+                                                 minlength=scene.n_objects)}
+    return out
+
+
+collect_samples_dev = collect_samples
+
+
+class _Step:
+    """Launch helper for one family's optimiser step."""
+
+    def __init__(self, model: NifModel, which: str):
+        torch = _torch()
+        self.model = model
+        self.fam = model.family(which)
+        self.sq = torch.zeros(1, dtype=torch.float64, device=model.device)
+
+    def run(self, obj, coord, label, idx, n_rows, rank=0, world=1, group=None, stream=None):
+        """One optimiser step over rows idx[0:n_rows] (device tensors);
+        leaves this batch's squared-error sum added into self.sq."""
+        torch = _torch()
+        L = _lib.lib()
+        fam, model = self.fam, self.model
+        sp = _lib.stream_ptr(stream)
+        fv = fam.view()
+        tv = fam.train_view()
+        p = _lib.ptr
+        L.nif_batch_counts_dev(p(obj), p(idx), n_rows, fam.n_obj, p(fam.counts), sp)
+        if world > 1:
+            sq_local = torch.zeros(1, dtype=torch.float64, device=model.device)
+            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), p(idx), n_rows, rank,
+                                   world, p(sq_local), sp)
+            import torch.distributed as dist
+            dist.all_reduce(fam.grad, group=group)
+            dist.all_reduce(sq_local, group=group)
+            self.sq += sq_local
+        else:
+            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), p(idx), n_rows, 0, 1,
+                                   p(self.sq), sp)
+        a = model.config.adam
+        L.nif_adam_dev(fv, tv, model.learning_rate, a.beta1, a.beta2, a.epsilon, sp)
+        fam.dirty = True
+
+
+def train_batch(model: NifModel, which: str, obj, coord, label) -> float:
+    """nif.py:682-749 _train_batch with host arrays; returns the batch mean
+    loss (sum of squared errors / rows)."""
+    torch = _torch()
+    dev = model.device
+    obj = np.asarray(obj, np.int64)
+    n = len(obj)
+    if n == 0:
+        raise ValueError("empty batch")
+    for o in np.unique(obj):
+        model._check_object(int(o))
+    width = 4 if which == "outer" else 5
+    t_obj = torch.from_numpy(obj).to(dev)
+    t_coord = torch.from_numpy(np.ascontiguousarray(np.asarray(coord, np.float64)[:, :width])).to(dev)
+    lab = np.asarray(label, np.float32).reshape(n, -1)
+    t_lab = torch.from_numpy(np.ascontiguousarray(lab)).to(dev)
+    step = _Step(model, which)
+    step.run(t_obj, t_coord, t_lab, None, n)
+    return float(step.sq.item()) / (n * lab.shape[1])
+
+
+_train_batch = train_batch
+
+
+def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional[int] = None,
+          group=None) -> np.ndarray:
+    """nif.py:752-795: shuffled mini-batch epochs over both families; loss
+    curve (epochs, 3) = outer, inner, combined (NaN for an empty family).
+    With torch.distributed initialised (or `group` given) the batches are
+    split across ranks and gradients all-reduced once per step."""
+    torch = _torch()
+    if isinstance(samples, dict):
+        samples = SampleSet.from_host(samples, device=model.device)
+    if samples.head != model.config.head:
+        raise ValueError(f"sample head {samples.head!r} does not match the "
+                         f"model head {model.config.head!r}")
+    if samples.n_outer == 0 and samples.n_inner == 0:
+        raise ValueError("no training samples")
+    epochs = model.config.epochs if epochs is None else epochs
+    seed = model.config.seed if seed is None else seed
+    curve = np.zeros((epochs, 3))
+    if epochs == 0:
+        return curve
+    world, rank = 1, 0
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    epoch_ss = np.random.SeedSequence([seed, 0x7472]).spawn(epochs)
+    bo = model.config.outer.batch_size
+    bi = model.config.inner.batch_size
+    steps = {"outer": _Step(model, "outer"), "inner": _Step(model, "inner")}
+    fams = ((0, bo, "outer", samples.outer_obj, samples.outer_coord, samples.outer_label),
+            (1, bi, "inner", samples.inner_obj, samples.inner_coord, samples.inner_label))
+    for e in range(epochs):
+        rng = np.random.default_rng(epoch_ss[e])
+        sums = np.zeros(2)
+        counts = np.zeros(2, np.int64)
+        for fam, bs, which, obj, coord, label in fams:
+            n = int(obj.shape[0])
+            if n == 0:
+                continue
+            perm = torch.from_numpy(rng.permutation(n)).to(model.device)
+            st = steps[which]
+            st.sq.zero_()
+            for k in range(0, n, bs):
+                m = min(bs, n - k)
+                st.run(obj, coord, label, perm[k:k + m], m, rank, world, group)
+            sums[fam] = float(st.sq.item())
+            counts[fam] = n
+        om = sums[0] / counts[0] if counts[0] else math.nan
+        im = sums[1] / counts[1] if counts[1] else math.nan
+        curve[e] = (om, im, sums.sum() / counts.sum())
+    return curve
