@@ -129,13 +129,11 @@ def build_workload(args, rank):
     return synthetic.c2(args.width, args.height)
 
 
-def cpu_baseline_leg(scene, model, rays_np, max_rays=20000, budget_s=20.0):
-    """Oracle port of the reference CPU path on a bounded sample, all host
-    threads (gather + encode + row-sequential forward, cmd_bench method:
-    1 warm-up + median)."""
+def cpu_path_step(scene, model, rays_np, n):
+    """One step of the reference CPU path (oracle port) over the first n
+    rays: gather + encode + row-sequential forward + per-ray OR."""
     from oracle import oracle
-    n = min(len(rays_np[0]), max_rays)
-    o, d, t = (a[:n] for a in rays_np)
+    o, d, t = (np.ascontiguousarray(a[:n]) for a in rays_np)
     osc = oracle.OracleScene(scene.pack, scene.epsilon_t)
     route = scene.nif_route_mask(None)
     grids = model.host_grids()
@@ -162,6 +160,15 @@ def cpu_baseline_leg(scene, model, rays_np, max_rays=20000, budget_s=20.0):
                 occ[ray[sel][p[:, 0] < 0.5]] = True
         return occ
 
+    return one
+
+
+def cpu_baseline_leg(scene, model, rays_np, max_rays=20000, budget_s=20.0):
+    """Oracle port of the reference CPU path on a bounded sample, all host
+    threads (cmd_bench method: 1 warm-up + median of up to 5)."""
+    from oracle import oracle
+    n = min(len(rays_np[0]), max_rays)
+    one = cpu_path_step(scene, model, rays_np, n)
     one()
     times = []
     t_end = time.perf_counter() + budget_s
@@ -206,11 +213,19 @@ def run_reference(args, rank, ws):
 
     model = HostModel()
     n = min(len(rays[0]), 20000)
-    base = cpu_baseline_leg(scene, model, rays, max_rays=n, budget_s=10.0)
-    # steps: each step is the same bounded sample, timed individually
-    from bench import cpu_baseline_leg as _leg  # noqa: F401
-    per = n / base["value"]
-    value = base["value"]
+    step = cpu_path_step(scene, model, rays, n)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    per = float(np.sum(times)) / args.steps
+    value = n / per
+    base = {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
+            "sample": f"{n} C2 shadow rays per step (first {n} of the frame), "
+                      "gather + encode + row-sequential MLP, all host threads"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -29,6 +29,10 @@ namespace {
 constexpr float kSlope = 0.01f;  // mlp.py:17 HIDDEN_SLOPE
 constexpr int kTileRows = 128;
 constexpr int kK1 = 16;          // padded layer-1 K (features + bias column)
+// Tiles of 128 records a CTA advances in lockstep (one barrier / commit per
+// layer for all of them). Measured on B200 at C2: 1 beats 2 (more CTAs per
+// SM hide the MMA round trip better than batching it).
+constexpr int kTpc = 1;
 
 // ---------------------------------------------------------------------------
 // fast blob layout
@@ -67,7 +71,7 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   l.off_dist = al16(l.off_dir + tab);
   const size_t dtab = f.family == NIF_FAMILY_INNER ? (size_t)f.n_obj * f.Rd * l.NPd * 2 : 0;
   l.total = al16(l.off_dist + dtab);
-  int cols = l.W + 16;
+  int cols = kTpc * ((l.W + 31) / 32 * 32);  // kTpc tiles x W accumulator columns
   l.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   bool hidden_same = true;
   for (int i = 1; i < f.n_layers; ++i) hidden_same = hidden_same && f.dims[i] == l.W;
@@ -314,9 +318,145 @@ __device__ __forceinline__ void lookup16(const __half* tab, int R, float u, floa
   corner<NP>(tab + ((size_t)b.iu1 * R + b.iv1) * NP, b.w11, acc);
 }
 
+// Two-stage software pipeline of the per-record inputs: while tile k runs
+// its MMA chain, the latent-table corners of tile k+1 are in flight
+// (issued right after tile k's first MMA) and the record words of tile
+// k+2 are being fetched, so the dependent gathers (record -> indices ->
+// corners) never sit on the critical path of a tile.
+struct RecIn {
+  int obj, ray;
+  float4 c;
+  float r;
+  bool valid;
+};
+
+template <int NP>
+struct CornerT;
+template <>
+struct CornerT<4> {
+  using V = uint2;
+};
+template <>
+struct CornerT<8> {
+  using V = uint4;
+};
+
 template <int N, int ND>
-__global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
-  constexpr int NP = N <= 4 ? 4 : 8;
+struct EncIn {
+  static constexpr int NP = N <= 4 ? 4 : 8;
+  typename CornerT<NP>::V cp[4], cd[4];
+  uint2 cr[2];
+  float wp[4], wd[4], wr;
+  int ray;
+  bool valid;
+};
+
+__device__ __forceinline__ RecIn load_rec(const TcArgs& a, int64_t tile, int tid, int64_t n,
+                                          bool inner) {
+  RecIn r;
+  const int64_t row = tile * kTileRows + tid;
+  r.valid = row < n;
+  r.obj = 0;
+  r.ray = 0;
+  r.c = make_float4(0.f, 0.f, 0.f, 0.f);
+  r.r = 0.f;
+  if (r.valid) {
+    r.obj = __ldg(a.obj + row);
+    r.ray = __ldg(a.ray + row);
+    r.c = __ldg(reinterpret_cast<const float4*>(a.coord4) + row);
+    if (inner) r.r = __ldg(a.rr + row);
+  }
+  return r;
+}
+
+template <int N, int ND>
+__device__ __forceinline__ void issue_enc(EncIn<N, ND>& e, const RecIn& r, const __half* tpos,
+                                          const __half* tdir, const __half* tdist, int R, int Rd) {
+  constexpr int NP = EncIn<N, ND>::NP;
+  using V = typename CornerT<NP>::V;
+  e.valid = r.valid;
+  e.ray = r.ray;
+  if (!r.valid) return;
+  const size_t g2 = (size_t)R * R * NP;
+  const Bil bp = bilinear(r.c.x, r.c.y, R), bd = bilinear(r.c.z, r.c.w, R);
+  const V* P = reinterpret_cast<const V*>(tpos + (size_t)r.obj * g2);
+  const V* D = reinterpret_cast<const V*>(tdir + (size_t)r.obj * g2);
+  e.cp[0] = __ldg(P + (size_t)bp.iu0 * R + bp.iv0);
+  e.cp[1] = __ldg(P + (size_t)bp.iu0 * R + bp.iv1);
+  e.cp[2] = __ldg(P + (size_t)bp.iu1 * R + bp.iv0);
+  e.cp[3] = __ldg(P + (size_t)bp.iu1 * R + bp.iv1);
+  e.cd[0] = __ldg(D + (size_t)bd.iu0 * R + bd.iv0);
+  e.cd[1] = __ldg(D + (size_t)bd.iu0 * R + bd.iv1);
+  e.cd[2] = __ldg(D + (size_t)bd.iu1 * R + bd.iv0);
+  e.cd[3] = __ldg(D + (size_t)bd.iu1 * R + bd.iv1);
+  e.wp[0] = bp.w00; e.wp[1] = bp.w01; e.wp[2] = bp.w10; e.wp[3] = bp.w11;
+  e.wd[0] = bd.w00; e.wd[1] = bd.w01; e.wd[2] = bd.w10; e.wd[3] = bd.w11;
+  if constexpr (ND > 0) {
+    const Lin li = linear1(r.r, Rd);
+    const uint2* G = reinterpret_cast<const uint2*>(tdist + (size_t)r.obj * Rd * 4);
+    e.cr[0] = __ldg(G + li.i0);
+    e.cr[1] = __ldg(G + li.i1);
+    e.wr = li.w;
+  }
+}
+
+__device__ __forceinline__ void acc_h2(uint32_t u, float w, float& a0, float& a1) {
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u));
+  a0 = fmaf(w, f.x, a0);
+  a1 = fmaf(w, f.y, a1);
+}
+
+template <int NP>
+__device__ __forceinline__ void acc_corner(const typename CornerT<NP>::V& q, float w, float* acc) {
+  if constexpr (NP == 4) {
+    acc_h2(q.x, w, acc[0], acc[1]);
+    acc_h2(q.y, w, acc[2], acc[3]);
+  } else {
+    acc_h2(q.x, w, acc[0], acc[1]);
+    acc_h2(q.y, w, acc[2], acc[3]);
+    acc_h2(q.z, w, acc[4], acc[5]);
+    acc_h2(q.w, w, acc[6], acc[7]);
+  }
+}
+
+template <int N, int ND>
+__device__ __forceinline__ void finish_enc(const EncIn<N, ND>& e, float (&x)[16]) {
+  constexpr int NP = EncIn<N, ND>::NP;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = 0.f;
+  if (e.valid) {
+    float ap[NP], ad[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) ap[i] = ad[i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc_corner<NP>(e.cp[c], e.wp[c], ap);
+      acc_corner<NP>(e.cd[c], e.wd[c], ad);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      x[i] = ap[i];
+      x[N + i] = ad[i];
+    }
+    if constexpr (ND > 0) {
+      float ar[4] = {0.f, 0.f, 0.f, 0.f};
+      acc_corner<4>(e.cr[0], 1.f - e.wr, ar);
+      acc_corner<4>(e.cr[1], e.wr, ar);
+#pragma unroll
+      for (int i = 0; i < ND; ++i) x[2 * N + i] = ar[i];
+    }
+  }
+  x[2 * N + ND] = 1.f;
+}
+
+// kTpc tiles of 128 records per CTA advance in lockstep: one barrier, one
+// batch of MMAs (one M=128 MMA chain per tile, issued back to back) and
+// one commit per layer cover kTpc*128 rows. Each tile owns W TMEM columns;
+// the N=16 head accumulates into the first 16 of them once the last hidden
+// layer has been drained.
+
+template <int N, int ND>
+__global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
   constexpr bool INNER = ND > 0;
   constexpr int IN = 2 * N + ND;
   static_assert(IN + 1 <= 16, "layer-1 inputs plus bias must fit K = 16");
@@ -324,13 +464,30 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
   const FastLayout& l = a.l;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  const int tt = warp >> 2;             // tile of this warpgroup
+  const int trow = tid & (kTileRows - 1);
   const int W = l.W, Kp = l.Kp, L = l.L;
   const size_t w_al = al16(l.w_bytes);
+  const size_t a1_bytes = (size_t)kTileRows * kK1 * 2, a2_bytes = (size_t)kTileRows * Kp * 2;
   uint8_t* sW = smem;
-  uint8_t* sA1 = smem + w_al;
-  uint8_t* sA2 = sA1 + kTileRows * kK1 * 2;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sA2 + (size_t)kTileRows * Kp * 2);
+  uint8_t* sA1 = smem + w_al + (size_t)tt * (a1_bytes + a2_bytes);
+  uint8_t* sA2 = sA1 + a1_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + w_al + kTpc * (a1_bytes + a2_bytes));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
+  const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
+  const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
+  const int64_t n = min(*a.count, a.cap);
+  const int64_t n_super = (n + kTpc * kTileRows - 1) / (kTpc * kTileRows);
+  const int64_t stride = gridDim.x;
+  auto tile_of = [&](int64_t sup) { return sup * kTpc + tt; };
+
+  // prologue of the input pipeline (overlaps the setup below)
+  EncIn<N, ND> ea;
+  issue_enc<N, ND>(ea, load_rec(a, tile_of(blockIdx.x), trow, n, INNER), tpos, tdir, tdist, l.R,
+                   l.Rd);
+  RecIn rb = load_rec(a, tile_of(blockIdx.x + stride), trow, n, INNER);
 
   // weights -> smem (resident for the kernel's lifetime)
   {
@@ -342,7 +499,7 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
   for (int c = W / 8; c < Kp / 8; ++c) {
     uint4 v = make_uint4(0, 0, 0, 0);
     if (c == W / 8) v.x = h2u(__halves2half2(__float2half_rn(1.f), __float2half_rn(0.f)));
-    store_chunk(sA2, tid, c, Kp, v);
+    store_chunk(sA2, trow, c, Kp, v);
   }
   if (tid == 0) {
     tc::mbar_init(bar, 1);
@@ -354,51 +511,25 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tslot;
-  const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+  const int Wc = (W + 31) / 32 * 32;  // TMEM column stride per tile
+  const uint32_t my_acc = tbase + (uint32_t)(tt * Wc);
+  const uint32_t lane_base = my_acc + ((uint32_t)((warp & 3) * 32) << 16);
 
-  const uint32_t sA1a = tc::smem_u32(sA1), sA2a = tc::smem_u32(sA2), sWa = tc::smem_u32(sW);
-  const uint64_t dA1 = tc::smem_desc(sA1a, 128, kK1 * 16);
+  const uint32_t base_a = tc::smem_u32(smem + w_al), sWa = tc::smem_u32(sW);
+  const uint32_t tile_stride = (uint32_t)(a1_bytes + a2_bytes);
   const uint64_t dW1 = tc::smem_desc(sWa + (uint32_t)l.off_w1, 128, kK1 * 16);
   const uint32_t idW = tc::idesc_f16(W), id16 = tc::idesc_f16(16);
   const __half2 slope2 = __float2half2_rn(kSlope);
 
-  const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
-  const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
-  const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
-  const size_t g2 = (size_t)l.R * l.R * NP;
-
-  const int64_t n = min(*a.count, a.cap);
-  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
   uint32_t phase = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t row = tile * kTileRows + tid;
-    const bool valid = row < n;
+  for (int64_t sup = blockIdx.x; sup < n_super; sup += stride) {
+    const int64_t row = tile_of(sup) * kTileRows + trow;
+    const bool valid = ea.valid;
+    const int my_ray = ea.ray;
     // ---- encode: 16 fp16 inputs (features, 1, zeros) ------------------------
-    float x[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = 0.f;
-    if (valid) {
-      const int o = a.obj[row];
-      const float4 c = reinterpret_cast<const float4*>(a.coord4)[row];
-      float acc[NP];
-      lookup16<NP>(tpos + (size_t)o * g2, l.R, c.x, c.y, acc);
-#pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = acc[i];
-      lookup16<NP>(tdir + (size_t)o * g2, l.R, c.z, c.w, acc);
-#pragma unroll
-      for (int i = 0; i < N; ++i) x[N + i] = acc[i];
-      if constexpr (INNER) {
-        const Lin li = linear1(a.rr[row], l.Rd);
-        const __half* g = tdist + (size_t)o * l.Rd * 4;
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        corner<4>(g + (size_t)li.i0 * 4, 1.f - li.w, d);
-        corner<4>(g + (size_t)li.i1 * 4, li.w, d);
-#pragma unroll
-        for (int i = 0; i < ND; ++i) x[2 * N + i] = d[i];
-      }
-    }
-    x[IN] = 1.f;
     {
+      float x[16];
+      finish_enc<N, ND>(ea, x);
       uint4 v0, v1;
       v0.x = h2u(__floats2half2_rn(x[0], x[1]));
       v0.y = h2u(__floats2half2_rn(x[2], x[3]));
@@ -408,17 +539,23 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
       v1.y = h2u(__floats2half2_rn(x[10], x[11]));
       v1.z = h2u(__floats2half2_rn(x[12], x[13]));
       v1.w = h2u(__floats2half2_rn(x[14], x[15]));
-      store_chunk(sA1, tid, 0, kK1, v0);
-      store_chunk(sA1, tid, 1, kK1, v1);
+      store_chunk(sA1, trow, 0, kK1, v0);
+      store_chunk(sA1, trow, 1, kK1, v1);
     }
     tc::fence_async_smem();
     tc::fence_before_sync();
     __syncthreads();
     if (tid == 0) {
       tc::fence_after_sync();
-      tc::mma_f16(tbase, dA1, dW1, idW, 0);
+#pragma unroll
+      for (int q = 0; q < kTpc; ++q)
+        tc::mma_f16(tbase + q * Wc, tc::smem_desc(base_a + q * tile_stride, 128, kK1 * 16), dW1,
+                    idW, 0);
       tc::mma_commit(bar);
     }
+    // next tiles' inputs go in flight while this tile's MMA chain runs
+    issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+    rb = load_rec(a, tile_of(sup + 2 * stride), trow, n, INNER);
     tc::mbar_wait(bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
@@ -435,8 +572,8 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
           q = __hmax2(q, __hmul2(q, slope2));
           h[i] = h2u(q);
         }
-        store_chunk(sA2, tid, 2 * cc, Kp, make_uint4(h[0], h[1], h[2], h[3]));
-        store_chunk(sA2, tid, 2 * cc + 1, Kp, make_uint4(h[4], h[5], h[6], h[7]));
+        store_chunk(sA2, trow, 2 * cc, Kp, make_uint4(h[0], h[1], h[2], h[3]));
+        store_chunk(sA2, trow, 2 * cc + 1, Kp, make_uint4(h[4], h[5], h[6], h[7]));
       }
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -444,16 +581,14 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
       if (tid == 0) {
         tc::fence_after_sync();
         const int steps = Kp / 16;
-        if (layer < L) {
-          const uint32_t wb = sWa + (uint32_t)(l.off_hidden + (size_t)(layer - 1) * W * Kp * 2);
+        const bool hid = layer < L;
+        const uint32_t wb = hid ? sWa + (uint32_t)(l.off_hidden + (size_t)(layer - 1) * W * Kp * 2)
+                                : sWa + (uint32_t)l.off_head;
+        for (int q = 0; q < kTpc; ++q) {
+          const uint32_t a2 = base_a + q * tile_stride + (uint32_t)a1_bytes;
           for (int s = 0; s < steps; ++s)
-            tc::mma_f16(tbase, tc::smem_desc(sA2a + s * 256, 128, Kp * 16),
-                        tc::smem_desc(wb + s * 256, 128, Kp * 16), idW, s > 0);
-        } else {
-          const uint32_t wb = sWa + (uint32_t)l.off_head;
-          for (int s = 0; s < steps; ++s)
-            tc::mma_f16(tbase + W, tc::smem_desc(sA2a + s * 256, 128, Kp * 16),
-                        tc::smem_desc(wb + s * 256, 128, Kp * 16), id16, s > 0);
+            tc::mma_f16(tbase + q * Wc, tc::smem_desc(a2 + s * 256, 128, Kp * 16),
+                        tc::smem_desc(wb + s * 256, 128, Kp * 16), hid ? idW : id16, s > 0);
         }
         tc::mma_commit(bar);
       }
@@ -461,10 +596,10 @@ __global__ void __launch_bounds__(128) query_tc_kernel(TcArgs a) {
       phase ^= 1;
       tc::fence_after_sync();
     }
-    const float logit = tc::tmem_ld1(lane_base + W);
+    const float logit = tc::tmem_ld1(lane_base);
     if (valid) {
       if (a.logits) a.logits[row] = logit;
-      if (a.occ && logit < 0.f) a.occ[a.ray[row]] = 1;
+      if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
     }
     tc::fence_before_sync();
   }
@@ -479,7 +614,8 @@ __global__ void occ_init_kernel(const uint8_t* __restrict__ src, int64_t n,
 }
 
 size_t tc_smem_bytes(const FastLayout& l) {
-  return al16(l.w_bytes) + (size_t)kTileRows * kK1 * 2 + (size_t)kTileRows * l.Kp * 2 + 64;
+  return al16(l.w_bytes) + kTpc * ((size_t)kTileRows * kK1 * 2 + (size_t)kTileRows * l.Kp * 2) +
+         64;
 }
 
 template <int N, int ND>
@@ -494,11 +630,11 @@ int launch_tc(const TcArgs& a, cudaStream_t st) {
   int per_sm = per_sm_tmem < per_sm_smem ? per_sm_tmem : per_sm_smem;
   if (per_sm > 8) per_sm = 8;
   if (per_sm < 1) per_sm = 1;
-  const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
+  const int64_t max_super = (a.cap + kTpc * kTileRows - 1) / (kTpc * kTileRows);
   int64_t grid = (int64_t)sm_count() * per_sm;
-  if (grid > max_tiles) grid = max_tiles;
+  if (grid > max_super) grid = max_super;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, 128, smem, st>>>(a);
+  kern<<<(unsigned)grid, 128 * kTpc, smem, st>>>(a);
   return check_launch("nif_query_dev(tcgen05)");
 }
 
