@@ -190,6 +190,10 @@ int nif_query_dev(const nif_family_view* f, const int32_t* obj, const int32_t* r
 #define NIF_IMPL_SIMT 1    /* fp32 CUDA-core reference kernel */
 #define NIF_IMPL_TCGEN05 2 /* fused tcgen05/TMEM fp16 kernel   */
 
+/* Diagnostics: when buf != NULL the tcgen05 query kernel records clock64()
+ * phase stamps of its first 4 tiles per CTA into buf[cta][4][16].      */
+int nif_debug_set_prof(void* buf);
+
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */
 int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray, void* stream);
 

@@ -143,6 +143,7 @@ _SIGS = {
     "nif_fast_pack_dev": (C.c_int, [C.POINTER(FamilyView), P, P]),
     "nif_query_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, I32, P]),
     "nif_occ_init_dev": (C.c_int, [P, I64, P, P]),
+    "nif_debug_set_prof": (C.c_int, [P]),
     "nif_batch_counts_dev": (C.c_int, [P, P, I64, I32, P, P]),
     "nif_train_fwdbwd_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
                                        I64, I64, I64, P, P]),

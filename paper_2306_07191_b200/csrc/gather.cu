@@ -122,6 +122,7 @@ __device__ __forceinline__ uint64_t pack(uint64_t flag, uint64_t o, uint64_t i) 
 // rays with no |d_a| below 1e-20 (fp32 reciprocal overflow).
 struct RayF {
   float ix, iy, iz, ox_i, oy_i, oz_i, dt, tmax_ru;
+  float ox, oy, oz;
 };
 
 __device__ __forceinline__ bool prefilter(const RayF& q, const float4 lo, const float4 hi) {
@@ -131,6 +132,85 @@ __device__ __forceinline__ bool prefilter(const RayF& q, const float4 lo, const 
   const float t0 = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fminf(az, bz)) - q.dt;
   const float t1 = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fmaxf(az, bz)) + q.dt;
   return t1 >= t0 && t1 >= -1e-6f && t0 <= q.tmax_ru;
+}
+
+// Warp-level conservative culling. With origins in [ol, oh], reciprocal
+// directions in [il, ih] (one sign per axis) and t_max <= tm over the
+// warp, interval arithmetic bounds every ray's slab entry from below (E)
+// and exit from above (X) per box; a box is a candidate for some ray only if
+// max_a E_a <= min_a X_a, min_a X_a >= -tol and max_a E_a <= tm, which is
+// what the per-ray candidate test requires (axes decoupled: conservative).
+// The same dt margin as the per-ray prefilter covers fp32 rounding. Lane k
+// evaluates object k; the ballot is the warp-uniform survivor mask.
+__device__ __forceinline__ float wmin(float v) {
+  float r;
+  asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float wmax(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+__device__ __forceinline__ void interval_slab(float lo, float hi, float ol, float oh, float il,
+                                              float ih, float& E, float& X) {
+  if (!(il > 0.f || ih < 0.f)) return;  // mixed signs: no bound from this axis
+  const float a0 = lo - oh, a1 = lo - ol, b0 = hi - oh, b1 = hi - ol;
+  const float p0 = a0 * il, p1 = a0 * ih, p2 = a1 * il, p3 = a1 * ih;
+  const float q0 = b0 * il, q1 = b0 * ih, q2 = b1 * il, q3 = b1 * ih;
+  const float ta_lo = fminf(fminf(p0, p1), fminf(p2, p3)), ta_hi = fmaxf(fmaxf(p0, p1), fmaxf(p2, p3));
+  const float tb_lo = fminf(fminf(q0, q1), fminf(q2, q3)), tb_hi = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3));
+  E = fmaxf(E, fminf(ta_lo, tb_lo));
+  X = fminf(X, fmaxf(ta_hi, tb_hi));
+}
+
+__device__ __forceinline__ uint32_t warp_bundle_mask(const RayF& q, bool use_pf, bool valid,
+                                                     int lane, int n_obj, const float4* flo,
+                                                     const float4* fhi, uint32_t all_obj,
+                                                     float absmax) {
+  const unsigned full = 0xffffffffu;
+  const uint32_t vmask = __ballot_sync(full, valid);
+  if (n_obj <= 1 || vmask == 0 || !__all_sync(full, use_pf || !valid)) return all_obj;
+  // invalid lanes borrow the first valid lane's ray (neutral for min/max)
+  const int src = __ffs(vmask) - 1;
+  float ox = __shfl_sync(full, q.ox, src), oy = __shfl_sync(full, q.oy, src),
+        oz = __shfl_sync(full, q.oz, src);
+  float ix = __shfl_sync(full, q.ix, src), iy = __shfl_sync(full, q.iy, src),
+        iz = __shfl_sync(full, q.iz, src);
+  float tm = __shfl_sync(full, q.tmax_ru, src);
+  if (valid) {
+    ox = q.ox; oy = q.oy; oz = q.oz;
+    ix = q.ix; iy = q.iy; iz = q.iz;
+    tm = q.tmax_ru;
+  }
+  const float oxl = wmin(ox), oxh = wmax(ox), oyl = wmin(oy), oyh = wmax(oy);
+  const float ozl = wmin(oz), ozh = wmax(oz);
+  const float ixl = wmin(ix), ixh = wmax(ix), iyl = wmin(iy), iyh = wmax(iy);
+  const float izl = wmin(iz), izh = wmax(iz);
+  const float tmh = wmax(tm);
+  // margin from warp-wide maxima: every interval endpoint product pairs some
+  // lane's origin with some lane's reciprocal
+  const float omax = fmaxf(fmaxf(fmaxf(fabsf(oxl), fabsf(oxh)), fmaxf(fabsf(oyl), fabsf(oyh))),
+                           fmaxf(fabsf(ozl), fabsf(ozh)));
+  const float imax = fmaxf(fmaxf(fmaxf(fabsf(ixl), fabsf(ixh)), fmaxf(fabsf(iyl), fabsf(iyh))),
+                           fmaxf(fabsf(izl), fabsf(izh)));
+  const float dth = 1e-5f * (absmax + omax + 1e-30f) * imax;
+  if (!isfinite(dth)) return all_obj;
+  bool pass = false;
+  if (lane < n_obj) {
+    const float4 lo = flo[lane], hi = fhi[lane];
+    float E = -CUDART_INF_F, X = CUDART_INF_F;
+    interval_slab(lo.x, hi.x, oxl, oxh, ixl, ixh, E, X);
+    interval_slab(lo.y, hi.y, oyl, oyh, iyl, iyh, E, X);
+    interval_slab(lo.z, hi.z, ozl, ozh, izl, izh, E, X);
+    E -= dth;
+    X += dth;
+    pass = E <= X && X >= -1e-6f && E <= tmh;
+  }
+  uint32_t m = __ballot_sync(full, pass);
+  if (n_obj > 32) m = 0xffffffffu;
+  return m;
 }
 
 template <bool EXACT>
@@ -199,6 +279,9 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       q.ix = (float)r.ix;
       q.iy = (float)r.iy;
       q.iz = (float)r.iz;
+      q.ox = (float)r.ox;
+      q.oy = (float)r.oy;
+      q.oz = (float)r.oz;
       q.ox_i = -(float)r.ox * q.ix;
       q.oy_i = -(float)r.oy * q.iy;
       q.oz_i = -(float)r.oz * q.iz;
@@ -215,9 +298,27 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   uint32_t hyb = 0;    // routed-away candidates
   int n_out = 0, n_in = 0;
   const bool test_box = n_obj > 1;
+  const uint32_t all_obj = n_obj >= 32 ? 0xffffffffu : ((1u << n_obj) - 1u);
+  // (1) warp-cooperative culling: lane k tests object k against the whole
+  //     warp's ray bundle (warp_bundle_mask); (2) per-ray fp32 prefilter over
+  //     the survivors; (3) exact fp64 classification of what is left.
+  const uint32_t wmask =
+      warp_bundle_mask(q, use_pf, valid, lane, n_obj, flo, fhi, all_obj, s_absmax);
+  uint32_t pmask = 0;
   if (valid) {
-    for (int k = 0; k < n_obj; ++k) {
-      if (use_pf && !prefilter(q, flo[k], fhi[k])) continue;
+    if (use_pf) {
+      uint32_t w = wmask;
+      while (w) {
+        const int k = __ffs(w) - 1;
+        w &= w - 1;
+        pmask |= (uint32_t)prefilter(q, flo[k], fhi[k]) << k;
+      }
+    } else {
+      pmask = all_obj;
+    }
+    while (pmask) {
+      const int k = __ffs(pmask) - 1;
+      pmask &= pmask - 1;
       double t0;
       const int kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
       if (kind == 0) continue;

@@ -275,7 +275,10 @@ struct TcArgs {
   int64_t cap;
   uint8_t* occ;
   float* logits;
+  long long* prof;  // diagnostic phase timestamps (nif_debug_set_prof), or NULL
 };
+
+long long* g_prof = nullptr;
 
 __device__ __forceinline__ void store_chunk(uint8_t* base, int row, int chunk, int kp,
                                             uint4 v) {
@@ -522,7 +525,12 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
   const __half2 slope2 = __float2half2_rn(kSlope);
 
   uint32_t phase = 0;
-  for (int64_t sup = blockIdx.x; sup < n_super; sup += stride) {
+  int it = 0;
+#define NIF_PROF(k)                                                      \
+  if (a.prof != nullptr && tid == 0 && it < 4)                          \
+    a.prof[((int64_t)blockIdx.x * 4 + it) * 16 + (k)] = clock64();
+  for (int64_t sup = blockIdx.x; sup < n_super; sup += stride, ++it) {
+    NIF_PROF(0);
     const int64_t row = tile_of(sup) * kTileRows + trow;
     const bool valid = ea.valid;
     const int my_ray = ea.ray;
@@ -542,9 +550,11 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
       store_chunk(sA1, trow, 0, kK1, v0);
       store_chunk(sA1, trow, 1, kK1, v1);
     }
+    NIF_PROF(1);
     tc::fence_async_smem();
     tc::fence_before_sync();
     __syncthreads();
+    NIF_PROF(2);
     if (tid == 0) {
       tc::fence_after_sync();
 #pragma unroll
@@ -556,9 +566,11 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
     // next tiles' inputs go in flight while this tile's MMA chain runs
     issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
     rb = load_rec(a, tile_of(sup + 2 * stride), trow, n, INNER);
+    NIF_PROF(3);
     tc::mbar_wait(bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
+    NIF_PROF(4);
 
     for (int layer = 1; layer <= L; ++layer) {
       // epilogue: TMEM accumulators -> leaky ReLU (fp16) -> next A tile
@@ -575,9 +587,11 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
         store_chunk(sA2, trow, 2 * cc, Kp, make_uint4(h[0], h[1], h[2], h[3]));
         store_chunk(sA2, trow, 2 * cc + 1, Kp, make_uint4(h[4], h[5], h[6], h[7]));
       }
+      NIF_PROF(3 + 3 * layer);
       tc::fence_async_smem();
       tc::fence_before_sync();
       __syncthreads();
+      NIF_PROF(4 + 3 * layer);
       if (tid == 0) {
         tc::fence_after_sync();
         const int steps = Kp / 16;
@@ -595,6 +609,7 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
       tc::mbar_wait(bar, phase);
       phase ^= 1;
       tc::fence_after_sync();
+      NIF_PROF(5 + 3 * layer);
     }
     const float logit = tc::tmem_ld1(lane_base);
     if (valid) {
@@ -676,7 +691,7 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
       return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernel");
     if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
     TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
-             logits};
+             logits, g_prof};
     if (f->family == NIF_FAMILY_OUTER && f->N == 3) return launch_tc<3, 0>(a, st);
     if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 3) return launch_tc<5, 3>(a, st);
     if (f->family == NIF_FAMILY_OUTER && f->N == 2) return launch_tc<2, 0>(a, st);
@@ -702,4 +717,9 @@ extern "C" int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_
   occ_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(bvh_occ, n,
                                                                                   occ_ray);
   return check_launch("nif_occ_init_dev");
+}
+
+extern "C" int nif_debug_set_prof(void* buf) {
+  g_prof = (long long*)buf;
+  return NIF_OK;
 }
