@@ -517,7 +517,10 @@ class DeviceScene:
         self.tris = up(tris)
         self.normals = up(norms)
         self.obox = up(obox)
-        self.t_order = up(scene.dfs_order.astype(np.int32))
+        dfs = getattr(scene, "dfs_order", None)
+        if dfs is None:  # a reference niftrace.Scene
+            dfs = top_dfs_order(scene.top)
+        self.t_order = up(np.asarray(dfs, np.int32))
         self.roots = up(pk.roots.astype(np.int32))
         self.albedo = up(scene.albedo)
         top = scene.top
