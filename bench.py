@@ -438,9 +438,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n)},
-        # per step: gather_fused, occ_init, query_tc outer, query_tc inner
+        # per step: gather_fused, query_tc outer (side stream), query_tc inner
         # (plus two memset nodes for the gather's counters / scan state)
-        "gpu_launches": args.steps * 4,
+        "gpu_launches": args.steps * 3,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line))

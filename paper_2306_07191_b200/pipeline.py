@@ -203,7 +203,10 @@ class VisibilityEngine:
         self.dirs = torch.empty((capacity, 3), dtype=torch.float64, device=dev)
         self.tmaxs = torch.empty(capacity, dtype=torch.float64, device=dev)
         self.buf = GatherBuffers(capacity, int(route.sum()), dev)
-        self.occ = torch.empty(capacity, dtype=torch.uint8, device=dev)
+        # the gather writes the hybrid any-hit result straight into the
+        # per-ray answer, which the query kernels then OR into
+        self.occ = self.buf.bvh_occ
+        self.side = torch.cuda.Stream(device=dev)
         self._views = None
         self.graphs = {}
 
@@ -229,18 +232,23 @@ class VisibilityEngine:
     def run(self, n: int, stream=None):
         L = _lib.lib()
         sp = _lib.stream_ptr(stream)
+        torch = _torch()
         b = self.buf
         gather_dev(self.ds, self.route, self.origins, self.dirs, self.tmaxs, n, b, stream)
-        L.nif_occ_init_dev(_lib.ptr(b.bvh_occ), n, _lib.ptr(self.occ), sp)
         if self.model is None:
             return
         vo, vi = self._family_views()
         p = _lib.ptr
         cnt = b.counts.data_ptr()
+        # the two families are independent: outer on a side stream, inner on
+        # the main one, joined before returning (fork/join is graph-capturable)
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self.side.wait_stream(main)
         L.nif_query_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None, cnt,
-                        b.cap, p(self.occ), None, self.impl, sp)
+                        b.cap, p(self.occ), None, self.impl, self.side.cuda_stream)
         L.nif_query_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord), p(b.inner_r),
                         cnt + 8, b.cap, p(self.occ), None, self.impl, sp)
+        main.wait_stream(self.side)
 
     def capture(self, n: int):
         """CUDA-graph the pass for a fixed ray count (replayed by `replay`)."""
