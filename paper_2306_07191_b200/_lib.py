@@ -13,7 +13,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libnif_b200.so"
+LIB_PATH = Path(os.environ.get("NIF_B200_LIB", _HERE / "libnif_b200.so"))
 
 NIF_OK = 0
 NIF_ERR_VALUE = 1

@@ -29,6 +29,9 @@ namespace nif {
 namespace {
 
 constexpr int kThreads = 256;    // rays per tile (one per thread)
+#ifndef NIF_GATHER_MINB
+#define NIF_GATHER_MINB 3        // resident CTAs per SM the register budget targets
+#endif
 constexpr int kMaxObjFused = 32; // 2 bits per object in a 64-bit mask
 
 struct ObjC {
@@ -102,6 +105,25 @@ __device__ __forceinline__ void sph32(double x, double y, double z, double n, fl
   zz = fminf(fmaxf(zz, -1.0f), 1.0f);
   *u = uu;
   *v = acosf(zz) * (1.0f / CUDART_PI_F);
+}
+
+__device__ __forceinline__ void sph32f(float x, float y, float z, float n, float* u, float* v) {
+  float uu = (atan2f(y, x) + CUDART_PI_F) * (0.5f / CUDART_PI_F);
+  if (uu >= 1.0f) uu -= 1.0f;
+  else if (uu < 0.0f) uu += 1.0f;
+  const float zz = fminf(fmaxf(__fdividef(z, n), -1.0f), 1.0f);
+  *u = uu;
+  *v = acosf(zz) * (1.0f / CUDART_PI_F);
+}
+
+// The reference's degenerate test sqrt(r.r) < 1e-9 in fp64, exactly: the
+// squared norm is the reference's expression; the fp64 sqrt is only taken
+// when r.r < 1e-17 (otherwise sqrt >= 3.1e-9 and the test is false). The
+// returned norm is fp32 (it only feeds fp32 coordinates).
+__device__ __forceinline__ bool degenerate_f32(double rx, double ry, double rz, float* rn) {
+  const double r2 = rx * rx + ry * ry + rz * rz;
+  *rn = sqrtf((float)r2);
+  return r2 < 1e-17 && sqrt(r2) < kDegenerateRadius;
 }
 
 constexpr uint64_t kFlagA = 1ull << 62;
@@ -214,12 +236,12 @@ __device__ __forceinline__ uint32_t warp_bundle_mask(const RayF& q, bool use_pf,
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, NIF_GATHER_MINB)
 gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
                     const double* __restrict__ org, const double* __restrict__ dir,
                     const double* __restrict__ tms, int64_t n, nif_gather_out out,
                     unsigned long long* __restrict__ status, int* __restrict__ tile_ctr,
-                    int64_t n_tiles) {
+                    int64_t n_tiles, long long* __restrict__ prof) {
   __shared__ ObjC objs[kMaxObjFused];
   __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
   __shared__ float s_absmax;
@@ -259,6 +281,9 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   const int64_t tile = s_tile;
   const int64_t i = tile * kThreads + tid;
   const bool valid = i < n;
+#define NIF_GPROF(k) \
+  if (prof != nullptr && tid == 0 && tile < 8192) prof[tile * 8 + (k)] = clock64();
+  NIF_GPROF(0);
 
   RayX r{};
   RayF q{};
@@ -331,6 +356,7 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       }
     }
   }
+  NIF_GPROF(1);
   // ---- block scan of (outer, inner) counts, packed 16|16 ------------------
   const int packed = (n_out << 16) | n_in;
   int incl = packed;
@@ -341,6 +367,7 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   }
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
+  NIF_GPROF(2);
   int warp_base = 0, block_total = 0;
 #pragma unroll
   for (int w = 0; w < kThreads / 32; ++w) {
@@ -363,6 +390,7 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     }
     out.bvh_occ[i] = occ ? 1 : 0;
   }
+  NIF_GPROF(3);
   // ---- decoupled look-back, one warp, 32 predecessors per probe -----------
   if (warp == 0) {
     uint32_t ex_o = 0, ex_i = 0;
@@ -396,14 +424,16 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       s_excl = ((uint64_t)ex_o << 32) | ex_i;
     }
   }
+  NIF_GPROF(4);
   __syncthreads();
+  NIF_GPROF(5);
   if (!valid) return;
   // ---- write records -------------------------------------------------------
   int64_t jo = (int64_t)(s_excl >> 32) + (excl_in_block >> 16);
   int64_t ji = (int64_t)(s_excl & 0xffffffffu) + (excl_in_block & 0xffff);
   int64_t jt = jo + ji;
   float du = 0.f, dv = 0.f;
-  if (!EXACT && mask != 0) sph32(r.dx, r.dy, r.dz, 1.0, &du, &dv);
+  if (!EXACT && mask != 0) sph32f((float)r.dx, (float)r.dy, (float)r.dz, 1.0f, &du, &dv);
   int deg_count = 0;
   uint64_t m = mask;
   while (m != 0) {
@@ -424,10 +454,10 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy,
                      ez = r.oz + hh.t0 * r.dz;
         const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
-        const double rn = sqrt(rx * rx + ry * ry + rz * rz);
-        deg = rn < kDegenerateRadius;
+        float rnf;
+        deg = degenerate_f32(rx, ry, rz, &rnf);
         if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; }
-        else sph32(rx, ry, rz, rn, &c4[0], &c4[1]);
+        else sph32f((float)rx, (float)ry, (float)rz, rnf, &c4[0], &c4[1]);
         c4[2] = du;
         c4[3] = dv;
       }
@@ -436,12 +466,12 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         deg = transform_inner(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, b.lo, b.hi, cc);
       } else {
         const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
-        const double rn = sqrt(rx * rx + ry * ry + rz * rz);
-        deg = rn < kDegenerateRadius;
+        float rnf;
+        deg = degenerate_f32(rx, ry, rz, &rnf);
         if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; rr = 0.f; }
         else {
-          sph32(rx, ry, rz, rn, &c4[0], &c4[1]);
-          rr = (float)fmin(rn / b.hn, 1.0);
+          sph32f((float)rx, (float)ry, (float)rz, rnf, &c4[0], &c4[1]);
+          rr = fminf(rnf / (float)b.hn, 1.0f);
         }
         c4[2] = du;
         c4[3] = dv;
@@ -479,8 +509,11 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     ++jt;
     deg_count += deg ? 1 : 0;
   }
+  NIF_GPROF(6);
   if (deg_count) atomicAdd((unsigned long long*)(out.counts + 3), (unsigned long long)deg_count);
 }
+
+long long* g_gprof = nullptr;  // diagnostic phase stamps (nif_debug_set_prof_gather)
 
 size_t fused_ws(int64_t n) {
   const int64_t tiles = (n + kThreads - 1) / kThreads;
@@ -520,9 +553,14 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
   cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
   if (out->rec_kind != nullptr)
     gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
-        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
+        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
   else
     gather_fused_kernel<false><<<(unsigned)tiles, kThreads, 0, st>>>(
-        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
+        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
   return check_launch("nif_gather_dev");
+}
+
+extern "C" int nif_debug_set_prof_gather(void* buf) {
+  g_gprof = (long long*)buf;
+  return NIF_OK;
 }

@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
     issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
     rb = load_rec(a, tile_of(sup + 2 * stride), trow, n, INNER);
     NIF_PROF(3);
-    tc::mbar_wait(bar, phase);
+    tc::mbar_spin(bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
     NIF_PROF(4);
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
         }
         tc::mma_commit(bar);
       }
-      tc::mbar_wait(bar, phase);
+      tc::mbar_spin(bar, phase);
       phase ^= 1;
       tc::fence_after_sync();
       NIF_PROF(5 + 3 * layer);
