@@ -193,6 +193,11 @@ int nif_query_dev(const nif_family_view* f, const int32_t* obj, const int32_t* r
 /* Diagnostics: when buf != NULL the tcgen05 query kernel records clock64()
  * phase stamps of its first 4 tiles per CTA into buf[cta][4][16].      */
 int nif_debug_set_prof(void* buf);
+/* Same for the gather (one-tile-per-CTA variant): buf[tile][8].        */
+int nif_debug_set_prof_gather(void* buf);
+/* Gather hot-path variant: 0 persistent pipelined (default), 1 one tile
+ * per CTA. Both produce identical records.                             */
+int nif_debug_set_gather_variant(int v);
 
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */
 int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray, void* stream);

@@ -513,7 +513,373 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   if (deg_count) atomicAdd((unsigned long long*)(out.counts + 3), (unsigned long long)deg_count);
 }
 
+// ===========================================================================
+// Persistent, software-pipelined variant of the hot-path gather (queues only).
+//
+// Each CTA claims 256-ray tiles in increasing order and keeps three in
+// flight: the rays of tile j+1 (and j+2) stream into shared memory through
+// cp.async.bulk (TMA bulk copies completing on an mbarrier) while tile j is
+// classified; tile j's records are written one iteration later, after its
+// decoupled look-back, so the look-back wait overlaps tile j+1's
+// classification instead of stalling the CTA. Deadlock-free: a CTA waiting
+// on the predecessors of tile a only holds unpublished tiles claimed after
+// a (larger ids), so waits always point to smaller tiles.
+// ===========================================================================
+__device__ __forceinline__ uint32_t tc_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+constexpr int kStages = 3;
+constexpr int kRayBytes = 56;  // origin 24 + direction 24 + tmax 8
+constexpr int kStageBytes = kThreads * kRayBytes;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(tc_smem(dst)),
+      "l"(src), "r"(bytes), "r"(tc_smem(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc_smem(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITG_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITG_%=;\n\t}" ::"r"(tc_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct TileRays {
+  const double* o;  // origins of ray 0 of the tile (smem or global)
+  const double* d;
+  const double* t;
+};
+
+__device__ __forceinline__ TileRays tile_rays(uint8_t* stage, bool staged, const double* org,
+                                              const double* dir, const double* tms,
+                                              int64_t tile) {
+  if (staged) {
+    return {reinterpret_cast<const double*>(stage),
+            reinterpret_cast<const double*>(stage + kThreads * 24),
+            reinterpret_cast<const double*>(stage + kThreads * 48)};
+  }
+  const int64_t r0 = tile * kThreads;
+  return {org + r0 * 3, dir + r0 * 3, tms + r0};
+}
+
+__global__ void __launch_bounds__(kThreads, NIF_GATHER_MINB)
+gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
+                      const double* __restrict__ org, const double* __restrict__ dir,
+                      const double* __restrict__ tms, int64_t n, nif_gather_out out,
+                      unsigned long long* __restrict__ status, int* __restrict__ tile_ctr,
+                      int64_t n_tiles) {
+  extern __shared__ __align__(128) uint8_t dsm[];  // kStages x kStageBytes ray buffers
+  __shared__ ObjC objs[kMaxObjFused];
+  __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
+  __shared__ float s_absmax;
+  __shared__ int s_warp[kThreads / 32];
+  __shared__ unsigned long long s_excl;
+  __shared__ uint64_t sbar[kStages];
+  __shared__ long long s_tiles[kStages];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int n_obj = s.n_obj;
+  const int64_t n_full = n / kThreads;  // tiles whose rays are bulk-copied
+  if (tid == 0) s_absmax = 0.f;
+  __syncthreads();
+  if (tid < n_obj) {
+    ObjC& b = objs[tid];
+    const int ob = s.t_order[tid];
+    const double* bx = s.obox + (size_t)ob * 6;
+    float am = 0.f;
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = bx[a];
+      b.hi[a] = bx[3 + a];
+      b.lt[a] = bx[a] - s.tol;
+      b.ht[a] = bx[3 + a] + s.tol;
+      b.c[a] = 0.5 * (bx[a] + bx[3 + a]);
+      am = fmaxf(am, fmaxf(fabsf((float)bx[a]), fabsf((float)bx[3 + a])));
+    }
+    flo[tid] = make_float4((float)bx[0], (float)bx[1], (float)bx[2], 0.f);
+    fhi[tid] = make_float4((float)bx[3], (float)bx[4], (float)bx[5], 0.f);
+    const double hx = 0.5 * (bx[3] - bx[0]), hy = 0.5 * (bx[4] - bx[1]),
+                 hz = 0.5 * (bx[5] - bx[2]);
+    b.hn = sqrt(hx * hx + hy * hy + hz * hz);
+    b.id = ob;
+    b.route = route[ob];
+    b.root = s.roots[ob];
+    atomicMax(reinterpret_cast<int*>(&s_absmax), __float_as_int(am));
+  }
+  auto claim = [&](int st) {  // thread 0: claim the next tile for stage st
+    const long long t = atomicAdd(tile_ctr, 1);
+    s_tiles[st] = t < n_tiles ? t : -1;
+    if (t < n_full) {
+      uint8_t* dst = dsm + st * kStageBytes;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(sbar + st, kStageBytes);
+      bulk_g2s(dst, org + t * kThreads * 3, kThreads * 24, sbar + st);
+      bulk_g2s(dst + kThreads * 24, dir + t * kThreads * 3, kThreads * 24, sbar + st);
+      bulk_g2s(dst + kThreads * 48, tms + t * kThreads, kThreads * 8, sbar + st);
+    }
+  };
+  if (tid == 0) {
+    for (int st = 0; st < kStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem(sbar + st)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    claim(0);
+    claim(1);
+  }
+  __syncthreads();
+  const bool test_box = n_obj > 1;
+  const uint32_t all_obj = n_obj >= 32 ? 0xffffffffu : ((1u << n_obj) - 1u);
+  uint32_t phases = 0;  // parity bit per stage
+
+  // state of the previous tile (written one iteration late)
+  long long p_tile = -1;
+  uint64_t p_mask = 0;
+  int p_excl = 0;
+  uint32_t p_agg = 0;
+
+  for (int j = 0;; ++j) {
+    const int st = j % kStages;
+    const long long tile = s_tiles[st];
+    long long cur_tile = tile;
+    uint64_t mask = 0;
+    int excl_in_block = 0;
+    uint32_t block_total = 0;
+    if (tile >= 0) {
+      const bool staged = tile < n_full;
+      if (staged) {
+        mbar_wait_parity(sbar + st, (phases >> st) & 1u);
+        phases ^= 1u << st;
+      }
+      const TileRays tr = tile_rays(dsm + st * kStageBytes, staged, org, dir, tms, tile);
+      const int64_t i = tile * kThreads + tid;
+      const bool valid = i < n;
+      RayX r{};
+      RayF q{};
+      bool use_pf = false;
+      if (valid) {
+        r.ox = tr.o[tid * 3 + 0];
+        r.oy = tr.o[tid * 3 + 1];
+        r.oz = tr.o[tid * 3 + 2];
+        r.dx = tr.d[tid * 3 + 0];
+        r.dy = tr.d[tid * 3 + 1];
+        r.dz = tr.d[tid * 3 + 2];
+        r.tmax = tr.t[tid];
+        r.ix = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
+        r.iy = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
+        r.iz = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
+        use_pf = n_obj > 1 && fabs(r.dx) > 1e-20 && fabs(r.dy) > 1e-20 && fabs(r.dz) > 1e-20;
+        if (use_pf) {
+          q.ix = (float)r.ix;
+          q.iy = (float)r.iy;
+          q.iz = (float)r.iz;
+          q.ox = (float)r.ox;
+          q.oy = (float)r.oy;
+          q.oz = (float)r.oz;
+          q.ox_i = -(float)r.ox * q.ix;
+          q.oy_i = -(float)r.oy * q.iy;
+          q.oz_i = -(float)r.oz * q.iz;
+          const float S = s_absmax + fmaxf(fmaxf(fabsf(q.ox), fabsf(q.oy)), fabsf(q.oz)) + 1e-30f;
+          const float imax = fmaxf(fmaxf(fabsf(q.ix), fabsf(q.iy)), fabsf(q.iz));
+          q.dt = 1e-5f * S * imax;
+          q.tmax_ru = __double2float_ru(r.tmax);
+          use_pf = isfinite(q.dt);
+        }
+      }
+      uint32_t hyb = 0;
+      int n_out = 0, n_in = 0;
+      const uint32_t wmask =
+          warp_bundle_mask(q, use_pf, valid, lane, n_obj, flo, fhi, all_obj, s_absmax);
+      if (valid) {
+        uint32_t pmask = 0;
+        if (use_pf) {
+          uint32_t w = wmask;
+          while (w) {
+            const int k = __ffs(w) - 1;
+            w &= w - 1;
+            pmask |= (uint32_t)prefilter(q, flo[k], fhi[k]) << k;
+          }
+        } else {
+          pmask = all_obj;
+        }
+        while (pmask) {
+          const int k = __ffs(pmask) - 1;
+          pmask &= pmask - 1;
+          double t0;
+          const int kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
+          if (kind == 0) continue;
+          if (objs[k].route == 1) {
+            mask |= (uint64_t)kind << (2 * k);
+            if (kind == 1) ++n_out;
+            else ++n_in;
+          } else {
+            hyb |= 1u << k;
+          }
+        }
+      }
+      const int packed = (n_out << 16) | n_in;
+      int incl = packed;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();
+      int warp_base = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        if (w < warp) warp_base += s_warp[w];
+        tot += s_warp[w];
+      }
+      excl_in_block = warp_base + incl - packed;
+      block_total = (uint32_t)tot;
+      if (tid == 0)
+        atomicExch(status + tile, pack(tile == 0 ? kFlagP : kFlagA, block_total >> 16,
+                                       block_total & 0xffff));
+      if (valid) {
+        bool occ = false;
+        uint32_t h = hyb;
+        while (h != 0 && !occ) {
+          const int k = __ffs(h) - 1;
+          h &= h - 1;
+          occ = occluded_in_object(s.nodes, s.tris, objs[k].root, r.ox, r.oy, r.oz, r.dx, r.dy,
+                                   r.dz, s.eps, r.tmax);
+        }
+        out.bvh_occ[i] = occ ? 1 : 0;
+      }
+    }
+    // ---- previous tile: look-back, then its records -------------------------
+    if (p_tile >= 0) {
+      if (warp == 0) {
+        const uint64_t agg_o = p_agg >> 16, agg_i = p_agg & 0xffff;
+        uint32_t ex_o = 0, ex_i = 0;
+        if (p_tile > 0) {
+          int64_t base = p_tile - 1;
+          while (true) {
+            const int64_t jj = base - lane;
+            uint64_t v = kFlagP;
+            if (jj >= 0) {
+              do {
+                v = *reinterpret_cast<volatile unsigned long long*>(status + jj);
+              } while ((v >> 62) == 0);
+            }
+            const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+            const int stop = pm ? __ffs(pm) - 1 : 31;
+            const uint32_t co = lane <= stop ? (uint32_t)((v >> 31) & kCntMask) : 0u;
+            const uint32_t ci = lane <= stop ? (uint32_t)(v & kCntMask) : 0u;
+            ex_o += __reduce_add_sync(0xffffffffu, co);
+            ex_i += __reduce_add_sync(0xffffffffu, ci);
+            if (pm) break;
+            base -= 32;
+          }
+          if (lane == 0) atomicExch(status + p_tile, pack(kFlagP, ex_o + agg_o, ex_i + agg_i));
+        }
+        if (lane == 0) {
+          if (p_tile == n_tiles - 1) {
+            out.counts[0] = (int64_t)(ex_o + agg_o);
+            out.counts[1] = (int64_t)(ex_i + agg_i);
+            out.counts[2] = (int64_t)(ex_o + agg_o) + (int64_t)(ex_i + agg_i);
+          }
+          s_excl = ((uint64_t)ex_o << 32) | ex_i;
+        }
+      }
+      __syncthreads();
+      const int64_t i = p_tile * kThreads + tid;
+      if (i < n && p_mask != 0) {
+        const int pst = (j + kStages - 1) % kStages;
+        const TileRays tr =
+            tile_rays(dsm + pst * kStageBytes, p_tile < n_full, org, dir, tms, p_tile);
+        RayX r{};
+        r.ox = tr.o[tid * 3 + 0];
+        r.oy = tr.o[tid * 3 + 1];
+        r.oz = tr.o[tid * 3 + 2];
+        r.dx = tr.d[tid * 3 + 0];
+        r.dy = tr.d[tid * 3 + 1];
+        r.dz = tr.d[tid * 3 + 2];
+        r.tmax = tr.t[tid];
+        int64_t jo = (int64_t)(s_excl >> 32) + (p_excl >> 16);
+        int64_t ji = (int64_t)(s_excl & 0xffffffffu) + (p_excl & 0xffff);
+        float du, dv;
+        sph32f((float)r.dx, (float)r.dy, (float)r.dz, 1.0f, &du, &dv);
+        bool have_inv = false;
+        int deg_count = 0;
+        uint64_t m = p_mask;
+        while (m != 0) {
+          const int bit = __ffsll((long long)m) - 1;
+          const int k = bit >> 1;
+          const int kind = (int)((m >> (2 * k)) & 3);
+          m &= ~(3ull << (2 * k));
+          const ObjC& b = objs[k];
+          float c0, c1, rr = 0.f;
+          float rnf;
+          bool deg;
+          if (kind == 1) {
+            if (!have_inv) {
+              r.ix = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
+              r.iy = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
+              r.iz = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
+              have_inv = true;
+            }
+            const Hit3 hh = slab(r, b);
+            const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy,
+                         ez = r.oz + hh.t0 * r.dz;
+            const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
+            deg = degenerate_f32(rx, ry, rz, &rnf);
+            if (deg) { c0 = 0.5f; c1 = 0.5f; }
+            else sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+            if (jo < out.cap_outer) {
+              out.outer_obj[jo] = b.id;
+              out.outer_ray[jo] = (int32_t)i;
+              reinterpret_cast<float4*>(out.outer_coord)[jo] = make_float4(c0, c1, du, dv);
+            }
+            ++jo;
+          } else {
+            const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
+            deg = degenerate_f32(rx, ry, rz, &rnf);
+            if (deg) { c0 = 0.5f; c1 = 0.5f; rr = 0.f; }
+            else {
+              sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+              rr = fminf(rnf / (float)b.hn, 1.0f);
+            }
+            if (ji < out.cap_inner) {
+              out.inner_obj[ji] = b.id;
+              out.inner_ray[ji] = (int32_t)i;
+              reinterpret_cast<float4*>(out.inner_coord)[ji] = make_float4(c0, c1, du, dv);
+              out.inner_r[ji] = rr;
+            }
+            ++ji;
+          }
+          deg_count += deg ? 1 : 0;
+        }
+        if (deg_count)
+          atomicAdd((unsigned long long*)(out.counts + 3), (unsigned long long)deg_count);
+      }
+    }
+    if (cur_tile < 0) break;  // uniform: no tile this iteration, previous drained
+    __syncthreads();          // stage (j-1) % kStages fully consumed
+    if (tid == 0) claim((j + 2) % kStages);
+    p_tile = cur_tile;
+    p_mask = mask;
+    p_excl = excl_in_block;
+    p_agg = block_total;
+    __syncthreads();          // s_tiles of the next iterations visible
+  }
+}
+
 long long* g_gprof = nullptr;  // diagnostic phase stamps (nif_debug_set_prof_gather)
+int g_gather_variant = 0;      // 0 persistent pipelined, 1 one tile per CTA (diagnostics)
 
 size_t fused_ws(int64_t n) {
   const int64_t tiles = (n + kThreads - 1) / kThreads;
@@ -554,13 +920,31 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
   if (out->rec_kind != nullptr)
     gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
-  else
+  else if (g_gprof != nullptr || g_gather_variant == 1)
     gather_fused_kernel<false><<<(unsigned)tiles, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
+  else {
+    const int smem = kStages * kStageBytes;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gather_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem);
+      attr = true;
+    }
+    int64_t grid = (int64_t)sm_count() * NIF_GATHER_MINB;
+    if (grid > tiles) grid = tiles;
+    gather_persist_kernel<<<(unsigned)grid, kThreads, smem, st>>>(
+        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
+  }
   return check_launch("nif_gather_dev");
 }
 
 extern "C" int nif_debug_set_prof_gather(void* buf) {
   g_gprof = (long long*)buf;
+  return NIF_OK;
+}
+
+extern "C" int nif_debug_set_gather_variant(int v) {
+  g_gather_variant = v;
   return NIF_OK;
 }
