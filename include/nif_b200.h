@@ -186,9 +186,20 @@ int nif_query_dev(const nif_family_view* f, const int32_t* obj, const int32_t* r
                   const float* coord4, const float* r, const int64_t* count_dev,
                   int64_t capacity, uint8_t* occ_ray, float* logits, int32_t impl,
                   void* stream);
+/* Split variant: a standalone grid-encoding kernel writes 16 fp16 features
+ * per record into 128-row UMMA-layout tiles in feat (nif_feat_scratch_bytes
+ * of capacity), then the tcgen05 MLP kernel streams them in by TMA bulk
+ * copies. flags bit 0: last layer + head on the CUDA cores.            */
+size_t nif_feat_scratch_bytes(int64_t capacity);
+int nif_query_split_dev(const nif_family_view* f, const int32_t* obj, const int32_t* ray,
+                        const float* coord4, const float* r, const int64_t* count_dev,
+                        int64_t capacity, uint8_t* occ_ray, float* logits, void* feat,
+                        int32_t flags, void* stream);
 #define NIF_IMPL_AUTO 0
 #define NIF_IMPL_SIMT 1    /* fp32 CUDA-core reference kernel */
-#define NIF_IMPL_TCGEN05 2 /* fused tcgen05/TMEM fp16 kernel   */
+#define NIF_IMPL_TCGEN05 2 /* fused tcgen05/TMEM fp16 kernel (shape-specialised
+                              when instantiated, else generic) */
+#define NIF_IMPL_TCGEN05_GENERIC 3 /* force the runtime-shape tcgen05 kernel */
 
 /* Diagnostics: when buf != NULL the tcgen05 query kernel records clock64()
  * phase stamps of its first 4 tiles per CTA into buf[cta][4][16].      */
@@ -198,6 +209,10 @@ int nif_debug_set_prof_gather(void* buf);
 /* Gather hot-path variant: 0 persistent pipelined (default), 1 one tile
  * per CTA. Both produce identical records.                             */
 int nif_debug_set_gather_variant(int v);
+/* Query-kernel variant (benchmarks / equivalence tests): 0 specialised,
+ * 8 tiles per SM, corner prefetch (default); 1 specialised, 6 tiles per
+ * SM; 2 runtime-shape generic kernel; 3 specialised, no corner prefetch. */
+int nif_debug_set_query_variant(int v);
 
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */
 int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray, void* stream);

@@ -25,6 +25,7 @@ NIF_MAX_LAYERS = 8
 IMPL_AUTO = 0
 IMPL_SIMT = 1
 IMPL_TCGEN05 = 2
+IMPL_TCGEN05_GENERIC = 3
 
 
 class NifNode(C.Structure):
@@ -143,9 +144,12 @@ _SIGS = {
     "nif_fast_pack_dev": (C.c_int, [C.POINTER(FamilyView), P, P]),
     "nif_query_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, I32, P]),
     "nif_occ_init_dev": (C.c_int, [P, I64, P, P]),
+    "nif_feat_scratch_bytes": (C.c_size_t, [I64]),
+    "nif_query_split_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, P, I32, P]),
     "nif_debug_set_prof": (C.c_int, [P]),
     "nif_debug_set_prof_gather": (C.c_int, [P]),
     "nif_debug_set_gather_variant": (C.c_int, [C.c_int]),
+    "nif_debug_set_query_variant": (C.c_int, [C.c_int]),
     "nif_batch_counts_dev": (C.c_int, [P, P, I64, I32, P, P]),
     "nif_train_fwdbwd_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
                                        I64, I64, I64, P, P]),

@@ -40,7 +40,7 @@ constexpr int kTpc = 1;
 
 struct FastLayout {
   int W, L, in_dim, Kp, NP, NPd, R, Rd, N, Nd, n_obj;
-  size_t off_w1, off_hidden, off_head, w_bytes;
+  size_t off_w1, off_hidden, off_head, off_headf, w_bytes;
   size_t off_pos, off_dir, off_dist, total;
   int tmem_cols;
   bool tc_ok;
@@ -64,7 +64,8 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   l.off_w1 = 0;
   l.off_hidden = l.off_w1 + (size_t)l.W * kK1 * 2;
   l.off_head = l.off_hidden + (size_t)(l.L > 0 ? l.L - 1 : 0) * l.W * l.Kp * 2;
-  l.w_bytes = l.off_head + (size_t)16 * l.Kp * 2;
+  l.off_headf = l.off_head + (size_t)16 * l.Kp * 2;  // fp32 head row + bias (CUDA-core head)
+  l.w_bytes = l.off_headf + ((size_t)(l.W + 1) * 4 + 15) / 16 * 16;
   l.off_pos = al16(l.w_bytes);
   const size_t tab = (size_t)f.n_obj * f.R * f.R * l.NP * 2;
   l.off_dir = al16(l.off_pos + tab);
@@ -96,7 +97,13 @@ __global__ void pack_weights_kernel(nif_family_view f, FastLayout l, uint8_t* bl
   const int n1 = l.W * kK1;
   const int nh = (l.L - 1) * l.W * l.Kp;
   const int nhead = 16 * l.Kp;
-  if (idx >= n1 + nh + nhead) return;
+  if (idx >= n1 + nh + nhead + l.W + 1) return;
+  if (idx >= n1 + nh + nhead) {  // fp32 copy of the head row and bias
+    const int k = idx - n1 - nh - nhead;
+    const size_t wo = (size_t)f.dims[0] * l.W + (size_t)(l.L - 1) * l.W * l.W;
+    reinterpret_cast<float*>(blob + l.off_headf)[k] = k < l.W ? f.w[wo + k] : f.b[(size_t)l.W * l.L];
+    return;
+  }
   float val = 0.f;
   size_t off;
   if (idx < n1) {
@@ -279,6 +286,7 @@ struct TcArgs {
 };
 
 long long* g_prof = nullptr;
+int g_query_variant = 0;  // nif_debug_set_query_variant
 
 __device__ __forceinline__ void store_chunk(uint8_t* base, int row, int chunk, int kp,
                                             uint4 v) {
@@ -622,6 +630,916 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
   if (warp == 0) tc::tmem_dealloc(tbase, l.tmem_cols);
 }
 
+// ---------------------------------------------------------------------------
+// Specialised tcgen05 query kernel (shapes known at compile time)
+//
+// G independent tile pipelines per CTA (one warpgroup = 128 records each,
+// own mbarrier, own named barrier, own W-column TMEM accumulator) share one
+// resident copy of the weights, so 8 tiles are in flight per SM without
+// replicating weights 8 times. Per tile only one activation tile of
+// 128 x Kp fp16 is kept: the layer-1 input (K = 16) lives in K-chunks 0-1 of
+// that same tile (descriptor SBO = Kp*16), so the constant tail (bias
+// column = 1, zero padding) is written once and never overwritten.
+// Waiting is a suspending try_wait; TMEM reads issue every column chunk of
+// a layer before one wait. The next tile's latent-corner gathers are issued
+// under the head MMA, whose round trip hides most of their L2 latency.
+// ---------------------------------------------------------------------------
+
+template <int N, int ND, int W, int L, int G>
+struct Tc2 {
+  static constexpr int IN = 2 * N + ND;
+  static constexpr int Kp = ((W + 1) + 15) / 16 * 16;
+  static constexpr int Wc = (W + 31) / 32 * 32;
+  static constexpr int COLS_RAW = G * Wc;
+  static constexpr int COLS = COLS_RAW <= 32 ? 32 : COLS_RAW <= 64 ? 64 : COLS_RAW <= 128 ? 128
+                              : COLS_RAW <= 256 ? 256 : 512;
+  static constexpr size_t OFF_HEADF =
+      (size_t)W * kK1 * 2 + (size_t)(L - 1) * W * Kp * 2 + (size_t)16 * Kp * 2;
+  static constexpr size_t W_BYTES = OFF_HEADF + ((size_t)(W + 1) * 4 + 15) / 16 * 16;
+  static constexpr size_t W_AL = (W_BYTES + 255) / 256 * 256;
+  static constexpr size_t A_BYTES = (size_t)kTileRows * Kp * 2;
+  static constexpr size_t SMEM = W_AL + G * A_BYTES + 64;
+  static_assert(W % 16 == 0 && IN + 1 <= kK1 && L >= 2, "shape");
+  static_assert(COLS_RAW <= 512, "TMEM");
+};
+
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+template <int W>
+__device__ __forceinline__ void epilogue_act(uint32_t taddr, uint8_t* sA, int trow, int Kp,
+                                             __half2 slope2) {
+  // W fp32 accumulator columns of this row -> leaky ReLU -> fp16 chunks,
+  // in groups of up to 32 columns (two loads in flight, one wait) to bound
+  // the live registers.
+  uint8_t* rowp = sA + (size_t)(trow >> 3) * (Kp * 16) + (trow & 7) * 16;
+#pragma unroll
+  for (int g0 = 0; g0 < W; g0 += 32) {
+    constexpr int GMAX = 32;
+    uint32_t r[GMAX];
+    const int gw = (W - g0) < GMAX ? (W - g0) : GMAX;  // 16 or 32, compile-time after unroll
+    tc::tmem_ld16_nw(taddr + g0, r);
+    if (gw > 16) tc::tmem_ld16_nw(taddr + g0 + 16, r + 16);
+    tc::tmem_ld_fence<GMAX>(r);
+#pragma unroll
+    for (int c = 0; c < GMAX / 8; ++c) {
+      if (c * 8 >= gw) break;
+      uint32_t h[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __half2 q = __floats2half2_rn(__uint_as_float(r[8 * c + 2 * i]),
+                                      __uint_as_float(r[8 * c + 2 * i + 1]));
+        q = __hmax2(q, __hmul2(q, slope2));
+        h[i] = h2u(q);
+      }
+      *reinterpret_cast<uint4*>(rowp + (g0 / 8 + c) * 128) = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+  }
+}
+
+// f32x2 helpers (FFMA2 / FMUL2 on sm_100)
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// Last hidden layer + N=1 head on the CUDA cores: logit = b + sum_k
+// w_k * lrelu(z_k) with z read straight from TMEM (fp32 activations, fp32
+// accumulation), which saves the head MMA round trip and its barrier.
+template <int W, int CH = 32>
+__device__ __forceinline__ float head_simt(uint32_t taddr, const float* __restrict__ hw) {
+  unsigned long long acc = f2pack(hw[W], 0.f);
+  const unsigned long long slope = f2pack(kSlope, kSlope);
+#pragma unroll
+  for (int g0 = 0; g0 < W; g0 += CH) {
+    uint32_t r[CH];
+    const int gw = (W - g0) < CH ? (W - g0) : CH;
+    tc::tmem_ld16_nw(taddr + g0, r);
+    if (CH > 16 && gw > 16) tc::tmem_ld16_nw(taddr + g0 + 16, r + (CH > 16 ? 16 : 0));
+    tc::tmem_ld_fence<CH>(r);
+#pragma unroll
+    for (int c = 0; c < CH; c += 4) {
+      if (c >= gw) break;
+      const float4 w4 = *reinterpret_cast<const float4*>(hw + g0 + c);
+      const unsigned long long z01 = f2pack(__uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+      const unsigned long long z23 = f2pack(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+      const float2 t01 = f2unpack(fmul2(z01, slope)), t23 = f2unpack(fmul2(z23, slope));
+      const unsigned long long a01 =
+          f2pack(fmaxf(__uint_as_float(r[c]), t01.x), fmaxf(__uint_as_float(r[c + 1]), t01.y));
+      const unsigned long long a23 = f2pack(fmaxf(__uint_as_float(r[c + 2]), t23.x),
+                                            fmaxf(__uint_as_float(r[c + 3]), t23.y));
+      acc = ffma2(a01, f2pack(w4.x, w4.y), acc);
+      acc = ffma2(a23, f2pack(w4.z, w4.w), acc);
+    }
+  }
+  const float2 s = f2unpack(acc);
+  return s.x + s.y;
+}
+
+template <int N, int ND, int W, int L, int G, int TPS, bool PF, bool HS, int DBG>
+__global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
+  using C = Tc2<N, ND, W, L, G>;
+  constexpr bool INNER = ND > 0;
+  constexpr int Kp = C::Kp;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const FastLayout& l = a.l;
+  const int tid = threadIdx.x;
+  const int wg = tid >> 7;
+  const int trow = tid & (kTileRows - 1);
+  const int quad = (tid >> 5) & 3;
+  const bool leader = trow == 0;
+  uint8_t* sW = smem;
+  uint8_t* sA = smem + C::W_AL + (size_t)wg * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::W_AL + G * C::A_BYTES);
+  uint64_t* bar = bars + wg;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + G);
+
+  const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
+  const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
+  const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
+  const int64_t n = min(*a.count, a.cap);
+  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
+  const int64_t stride = (int64_t)gridDim.x * G;
+  const int64_t first = (int64_t)blockIdx.x * G + wg;
+
+  // PF: corner gathers of tile k+1 in flight under tile k's head MMA;
+  // otherwise only the record words are prefetched one tile ahead.
+  // DBG (bench-only ablations): 1 = no latent-table gathers, 2 = no MLP
+  auto issue = [&](EncIn<N, ND>& e, const RecIn& r, const __half* p0, const __half* p1,
+                   const __half* p2, int R, int Rd) {
+    if constexpr (DBG == 1) {
+      e = EncIn<N, ND>{};
+      e.valid = r.valid;
+      e.ray = r.ray;
+      e.wp[0] = r.c.x;
+    } else {
+      issue_enc<N, ND>(e, r, p0, p1, p2, R, Rd);
+    }
+  };
+  EncIn<N, ND> ea;
+  RecIn rb;
+  if constexpr (PF) {
+    issue(ea, load_rec(a, first, trow, n, INNER), tpos, tdir, tdist, l.R, l.Rd);
+    rb = load_rec(a, first + stride, trow, n, INNER);
+  } else {
+    rb = load_rec(a, first, trow, n, INNER);
+  }
+
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sW);
+    for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  // constant tail of this warpgroup's activation tile: column W = 1, rest 0
+#pragma unroll
+  for (int c = W / 8; c < Kp / 8; ++c) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c == W / 8) v.x = h2u(__halves2half2(__float2half_rn(1.f), __float2half_rn(0.f)));
+    store_chunk(sA, trow, c, Kp, v);
+  }
+  if (tid == 0) {
+    for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
+    tc::fence_barrier_init();
+  }
+  if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t acc = *tslot + (uint32_t)(wg * C::Wc);
+  const uint32_t lane_acc = acc + ((uint32_t)(quad * 32) << 16);
+
+  const uint32_t sAa = tc::smem_u32(sA), sWa = tc::smem_u32(sW);
+  constexpr uint32_t off_hidden = (uint32_t)W * kK1 * 2;
+  constexpr uint32_t off_head = off_hidden + (uint32_t)(L - 1) * W * Kp * 2;
+  const uint32_t idW = tc::idesc_f16(W), id16 = tc::idesc_f16(16);
+  const __half2 slope2 = __float2half2_rn(kSlope);
+  const uint32_t bar_id = 1 + wg;
+
+  uint32_t phase = 0;
+  for (int64_t t = first; t < n_tiles; t += stride) {
+    const int64_t row = t * kTileRows + trow;
+    if constexpr (!PF) {
+      issue(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+      rb = load_rec(a, t + stride, trow, n, INNER);
+    }
+    const bool valid = ea.valid;
+    const int my_ray = ea.ray;
+    {
+      float x[16];
+      finish_enc<N, ND>(ea, x);
+      uint4 v0, v1;
+      v0.x = h2u(__floats2half2_rn(x[0], x[1]));
+      v0.y = h2u(__floats2half2_rn(x[2], x[3]));
+      v0.z = h2u(__floats2half2_rn(x[4], x[5]));
+      v0.w = h2u(__floats2half2_rn(x[6], x[7]));
+      v1.x = h2u(__floats2half2_rn(x[8], x[9]));
+      v1.y = h2u(__floats2half2_rn(x[10], x[11]));
+      v1.z = h2u(__floats2half2_rn(x[12], x[13]));
+      v1.w = h2u(__floats2half2_rn(x[14], x[15]));
+      store_chunk(sA, trow, 0, Kp, v0);
+      store_chunk(sA, trow, 1, Kp, v1);
+    }
+    if constexpr (DBG == 2) {
+      if constexpr (PF) {
+        issue(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+        rb = load_rec(a, t + 2 * stride, trow, n, INNER);
+      }
+      if (valid && a.occ && __half2float(reinterpret_cast<__half*>(sA + trow * 16)[0]) < -100.f)
+        a.occ[my_ray] = 1;
+      continue;
+    }
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    tc::named_sync(bar_id, 128);
+    if (leader) {
+      tc::fence_after_sync();
+      tc::mma_f16(acc, tc::smem_desc(opaque_u32(sAa), 128, Kp * 16),
+                  tc::smem_desc(opaque_u32(sWa), 128, kK1 * 16), idW, 0);
+      tc::mma_commit(bar);
+    }
+    tc::mbar_wait_sleep(bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+
+#pragma unroll
+    for (int layer = 1; layer <= L; ++layer) {
+      if (HS && layer == L) break;  // last layer + head on the CUDA cores below
+      epilogue_act<W>(lane_acc, sA, trow, Kp, slope2);
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::named_sync(bar_id, 128);
+      if (leader) {
+        tc::fence_after_sync();
+        const bool hid = layer < L;
+        // opaque copies keep the descriptors from being hoisted (and held in
+        // registers by every thread) across the tile loop
+        const uint32_t ab = opaque_u32(sAa);
+        const uint32_t wb = opaque_u32(hid ? sWa + off_hidden + (uint32_t)((layer - 1) * W * Kp * 2)
+                                           : sWa + off_head);
+#pragma unroll
+        for (int s = 0; s < Kp / 16; ++s)
+          tc::mma_f16(acc, tc::smem_desc(ab + s * 256, 128, Kp * 16),
+                      tc::smem_desc(wb + s * 256, 128, Kp * 16), hid ? idW : id16, s > 0);
+        tc::mma_commit(bar);
+      }
+      if (PF && layer == (HS ? L - 1 : L)) {
+        // next tile's inputs go in flight under the last MMA of this tile
+        issue(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+        rb = load_rec(a, t + 2 * stride, trow, n, INNER);
+      }
+      tc::mbar_wait_sleep(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+    }
+    float logit;
+    if constexpr (HS) {
+      logit = head_simt<W>(lane_acc, reinterpret_cast<const float*>(sW + C::OFF_HEADF));
+    } else {
+      logit = tc::tmem_ld1(lane_acc);
+    }
+    if (valid) {
+      if (a.logits) a.logits[row] = logit;
+      if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
+    }
+    tc::fence_before_sync();
+  }
+  __syncthreads();
+  if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
+}
+
+// TPS = tiles in flight per SM the register budget is sized for
+// (8: 64 registers/thread; 6: 80).
+template <int N, int ND, int W, int L, int G, int TPS = 8, bool PF = true, bool HS = false,
+          int DBG = 0>
+int launch_tc2(const TcArgs& a, cudaStream_t st) {
+  using C = Tc2<N, ND, W, L, G>;
+  auto kern = query_tc2_kernel<N, ND, W, L, G, TPS, PF, HS, DBG>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+      cudaSuccess)
+    return check_launch("query_tc2: smem attribute");
+  const int per_sm_tmem = 512 / C::COLS;
+  const int per_sm_smem = (int)((228 * 1024) / (C::SMEM + 1024));
+  int per_sm = per_sm_tmem < per_sm_smem ? per_sm_tmem : per_sm_smem;
+  if (per_sm > TPS / G) per_sm = TPS / G;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  const int64_t need = (max_tiles + G - 1) / G;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 128 * G, C::SMEM, st>>>(a);
+  return check_launch("nif_query_dev(tcgen05 specialised)");
+}
+
+// Dispatch to a compile-time specialisation; returns 1 when none matches.
+int launch_tc2_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
+  const int W = a.l.W, L = a.l.L;
+#define NIF_TC2H(NN, NDD, WW, LL, GG, TT, PP, HH)                                     \
+  if (f.N == NN && (NDD == 0 ? f.family == NIF_FAMILY_OUTER                 \
+                             : (f.family == NIF_FAMILY_INNER && f.Nd == NDD)) && \
+      W == WW && L == LL) {                                                 \
+    *rc = launch_tc2<NN, NDD, WW, LL, GG, TT, PP, HH>(a, st);                         \
+    return 0;                                                               \
+  }
+#define NIF_TC2(NN, NDD, WW, LL, GG, TT, PP) NIF_TC2H(NN, NDD, WW, LL, GG, TT, PP, false)
+  // defaults (nif.py:59-156): outer 2 x 64, inner 3 x 48
+  if (g_query_variant == 1) {
+    NIF_TC2(3, 0, 64, 2, 2, 6, true)
+    NIF_TC2(5, 3, 48, 3, 2, 6, true)
+  }
+  if (g_query_variant == 4) {
+    NIF_TC2H(3, 0, 64, 2, 2, 8, true, true)
+    NIF_TC2H(5, 3, 48, 3, 2, 8, true, true)
+  }
+  if (g_query_variant == 5) {
+    NIF_TC2H(3, 0, 64, 2, 2, 6, true, true)
+    NIF_TC2H(5, 3, 48, 3, 2, 6, true, true)
+  }
+  if (g_query_variant == 6) {
+    if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
+      *rc = launch_tc2<3, 0, 64, 2, 2, 6, true, false, 1>(a, st);
+      return 0;
+    }
+    if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
+      *rc = launch_tc2<5, 3, 48, 3, 2, 6, true, false, 1>(a, st);
+      return 0;
+    }
+  }
+  if (g_query_variant == 7) {
+    if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
+      *rc = launch_tc2<3, 0, 64, 2, 2, 6, true, false, 2>(a, st);
+      return 0;
+    }
+    if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
+      *rc = launch_tc2<5, 3, 48, 3, 2, 6, true, false, 2>(a, st);
+      return 0;
+    }
+  }
+  if (g_query_variant == 8) {
+    NIF_TC2(3, 0, 64, 2, 1, 5, true)
+    NIF_TC2(5, 3, 48, 3, 1, 5, true)
+  }
+  if (g_query_variant == 9) {
+    NIF_TC2(3, 0, 64, 2, 2, 4, true)
+    NIF_TC2(5, 3, 48, 3, 2, 4, true)
+  }
+  if (g_query_variant == 10) {
+    NIF_TC2(3, 0, 64, 2, 1, 4, true)
+    NIF_TC2(5, 3, 48, 3, 1, 4, true)
+  }
+  if (g_query_variant == 3) {
+    NIF_TC2(3, 0, 64, 2, 2, 8, false)
+    NIF_TC2(5, 3, 48, 3, 2, 8, false)
+  }
+  NIF_TC2(3, 0, 64, 2, 2, 8, true)
+  NIF_TC2(5, 3, 48, 3, 2, 8, true)
+  // C5 sweep: widths 64 / 128, 2-4 hidden layers
+  NIF_TC2(3, 0, 64, 3, 2, 8, true)
+  NIF_TC2(3, 0, 64, 4, 2, 8, true)
+  NIF_TC2(3, 0, 128, 2, 1, 2, true)
+  NIF_TC2(3, 0, 128, 3, 1, 2, true)
+  NIF_TC2(3, 0, 128, 4, 1, 2, true)
+  NIF_TC2(5, 3, 64, 2, 2, 8, true)
+  NIF_TC2(5, 3, 64, 3, 2, 8, true)
+  NIF_TC2(5, 3, 64, 4, 2, 8, true)
+  NIF_TC2(5, 3, 128, 2, 1, 2, true)
+  NIF_TC2(5, 3, 128, 3, 1, 2, true)
+  NIF_TC2(5, 3, 128, 4, 1, 2, true)
+#undef NIF_TC2
+#undef NIF_TC2H
+  return 1;
+}
+
+
+// ---------------------------------------------------------------------------
+// Split path: standalone grid encoding -> tcgen05 MLP
+//
+// encode_tiles_kernel: one thread per record, fp16 latent corners gathered
+// from the L2-resident tables, fp32 interpolation, 16 fp16 features per
+// record (features, the constant-one bias column, zeros) written straight
+// into 128-row tiles of the UMMA canonical K-major layout (4 KB per tile;
+// each warp writes one contiguous 1 KB block).
+// mlp_tiles_kernel: G independent 128-row tile pipelines per CTA; the
+// layer-1 operand of each tile arrives by one 4 KB TMA bulk copy into a
+// two-slot ring (issued a tile ahead by the MMA-issuing thread), so the MLP
+// warps hold no gather state and run 8 tiles per SM in 64 registers.
+// ---------------------------------------------------------------------------
+
+constexpr int kFeatTileBytes = kTileRows * kK1 * 2;  // 4096
+
+template <int N, int ND>
+__global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __restrict__ blob,
+                                                           FastLayout l,
+                                                           const int32_t* __restrict__ obj,
+                                                           const float* __restrict__ coord4,
+                                                           const float* __restrict__ rr,
+                                                           const int64_t* __restrict__ count,
+                                                           int64_t cap, uint8_t* __restrict__ feat) {
+  constexpr bool INNER = ND > 0;
+  const int64_t n = min(*count, cap);
+  const int64_t n_pad = (n + kTileRows - 1) / kTileRows * kTileRows;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_pad;
+       row += (int64_t)gridDim.x * blockDim.x) {
+  const __half* tpos = reinterpret_cast<const __half*>(blob + l.off_pos);
+  const __half* tdir = reinterpret_cast<const __half*>(blob + l.off_dir);
+  const __half* tdist = reinterpret_cast<const __half*>(blob + l.off_dist);
+  RecIn r;
+  r.valid = row < n;
+  r.obj = 0;
+  r.ray = 0;
+  r.c = make_float4(0.f, 0.f, 0.f, 0.f);
+  r.r = 0.f;
+  if (r.valid) {
+    r.obj = __ldg(obj + row);
+    r.c = __ldg(reinterpret_cast<const float4*>(coord4) + row);
+    if (INNER) r.r = __ldg(rr + row);
+  }
+  EncIn<N, ND> e;
+  issue_enc<N, ND>(e, r, tpos, tdir, tdist, l.R, l.Rd);
+  float x[16];
+  finish_enc<N, ND>(e, x);
+  uint4 v0, v1;
+  v0.x = h2u(__floats2half2_rn(x[0], x[1]));
+  v0.y = h2u(__floats2half2_rn(x[2], x[3]));
+  v0.z = h2u(__floats2half2_rn(x[4], x[5]));
+  v0.w = h2u(__floats2half2_rn(x[6], x[7]));
+  v1.x = h2u(__floats2half2_rn(x[8], x[9]));
+  v1.y = h2u(__floats2half2_rn(x[10], x[11]));
+  v1.z = h2u(__floats2half2_rn(x[12], x[13]));
+  v1.w = h2u(__floats2half2_rn(x[14], x[15]));
+  uint4* p = reinterpret_cast<uint4*>(feat) + 2 * row;
+  __stcg(p, v0);
+  __stcg(p + 1, v1);
+  }
+}
+
+struct MlpArgs {
+  const uint8_t* blob;  // fast blob (weights at offset 0)
+  const uint8_t* feat;  // encoded features, 32 B (16 fp16) per record
+  const int32_t* ray;
+  const int64_t* count;
+  int64_t cap;
+  uint8_t* occ;
+  float* logits;
+  long long* prof;  // diagnostic phase stamps (nif_debug_set_prof), or NULL
+};
+
+// TMEM per tile: fp32 accumulator [0, W) and the fp16 A operand (two per
+// column) [AOFF, AOFF + Kp/2). Keeping A in TMEM means the tensor core reads
+// only the weights from shared memory: with N = 48-64 the A tile re-read
+// per K step would otherwise make the MLP shared-memory-bandwidth bound.
+template <int W, int L, int G>
+struct MlpCfg {
+  static constexpr int Kp = ((W + 1) + 15) / 16 * 16;
+  static constexpr int AOFF = (W + 15) / 16 * 16;
+  static constexpr int STRIDE = (AOFF + Kp / 2 + 15) / 16 * 16;
+  static constexpr int COLS_RAW = G * STRIDE;
+  static constexpr int COLS = COLS_RAW <= 32 ? 32 : COLS_RAW <= 64 ? 64 : COLS_RAW <= 128 ? 128
+                              : COLS_RAW <= 256 ? 256 : 512;
+  static constexpr size_t OFF_HEADF =
+      (size_t)W * kK1 * 2 + (size_t)(L - 1) * W * Kp * 2 + (size_t)16 * Kp * 2;
+  static constexpr size_t W_BYTES = OFF_HEADF + ((size_t)(W + 1) * 4 + 15) / 16 * 16;
+  static constexpr size_t W_AL = (W_BYTES + 1023) / 1024 * 1024;
+  static constexpr size_t SMEM = W_AL + 128;
+  static_assert(W % 16 == 0 && L >= 2, "shape");
+  static_assert(COLS_RAW <= 512, "TMEM");
+  static_assert(Kp / 2 - W / 2 == 8, "one 8-column constant tail");
+};
+
+template <int W>
+__device__ __forceinline__ void epilogue_act_tmem(uint32_t acc, uint32_t a_op, __half2 slope2) {
+  // W fp32 accumulator columns -> leaky ReLU -> W/2 packed fp16 columns of A
+#pragma unroll
+  for (int g0 = 0; g0 < W; g0 += 32) {
+    uint32_t r[32];
+    const int gw = (W - g0) < 32 ? (W - g0) : 32;
+    tc::tmem_ld16_nw(acc + g0, r);
+    if (gw > 16) tc::tmem_ld16_nw(acc + g0 + 16, r + 16);
+    tc::tmem_ld_fence<32>(r);
+#pragma unroll
+    for (int c = 0; c < 32; c += 16) {
+      if (c >= gw) break;
+      uint32_t h[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        __half2 q = __floats2half2_rn(__uint_as_float(r[c + 2 * i]), __uint_as_float(r[c + 2 * i + 1]));
+        q = __hmax2(q, __hmul2(q, slope2));
+        h[i] = h2u(q);
+      }
+      tc::tmem_st8(a_op + (g0 + c) / 2, h);
+    }
+  }
+  tc::tmem_wait_st();
+}
+
+template <int W, int L, int G, int TPS>
+__global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) {
+  using C = MlpCfg<W, L, G>;
+  constexpr int Kp = C::Kp;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int wg = tid >> 7;
+  const int trow = tid & (kTileRows - 1);
+  const int quad = (tid >> 5) & 3;
+  const bool leader = trow == 0;
+  uint8_t* sW = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::W_AL);
+  uint64_t* bar = bars + wg;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + G);
+
+  const int64_t n = min(*a.count, a.cap);
+  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
+  const int64_t stride = (int64_t)gridDim.x * G;
+  const int64_t first = (int64_t)blockIdx.x * G + wg;
+
+  if (tid == 0) {
+    for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
+    tc::fence_barrier_init();
+  }
+  // the first tile's features are in flight while the weights are staged
+  const uint4* F = reinterpret_cast<const uint4*>(a.feat);
+  uint4 f0 = make_uint4(0, 0, 0, 0), f1 = f0;
+  {
+    const int64_t row = first * kTileRows + trow;
+    if (first < n_tiles && row < n) {
+      f0 = __ldg(F + 2 * row);
+      f1 = __ldg(F + 2 * row + 1);
+    }
+  }
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sW);
+    for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+  const uint32_t acc = *tslot + (uint32_t)(wg * C::STRIDE);
+  const uint32_t a_op = acc + C::AOFF;
+  const uint32_t lane_acc = acc + lane_off, lane_a = a_op + lane_off;
+  {  // constant tail of A: column K = W is the bias input (1), the rest 0
+    uint32_t tail[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    tail[0] = h2u(__halves2half2(__float2half_rn(1.f), __float2half_rn(0.f)));
+    tc::tmem_st8(lane_a + W / 2, tail);
+  }
+  const uint32_t sWa = tc::smem_u32(sW);
+  constexpr uint32_t off_hidden = (uint32_t)W * kK1 * 2;
+  const uint32_t idW = tc::idesc_f16(W);
+  const __half2 slope2 = __float2half2_rn(kSlope);
+  const uint32_t bar_id = 1 + wg;
+  const float* headw = reinterpret_cast<const float*>(sW + C::OFF_HEADF);
+
+  uint32_t phase = 0;
+  int it = 0;
+  long long* prof = a.prof;
+#define MLP_PROF(k)                                                                       \
+  if (prof != nullptr && trow == 0 && it < 4)                                             \
+    prof[(((int64_t)blockIdx.x * G + wg) * 4 + it) * 16 + (k)] = clock64();
+  if (prof != nullptr && trow == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    prof[(((int64_t)blockIdx.x * G + wg) * 4) * 16 + 11] = (long long)gt;
+  }
+  for (int64_t t = first; t < n_tiles; t += stride, ++it) {
+    MLP_PROF(0);
+    const int64_t row = t * kTileRows + trow;
+    const bool valid = row < n;
+    {
+      const uint32_t fv[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+      tc::tmem_st8(lane_a, fv);
+    }
+    const int my_ray = valid ? __ldg(a.ray + row) : 0;
+    {  // next tile's features stream in under this tile's chain
+      const int64_t nrow = row + stride * kTileRows;
+      f0 = make_uint4(0, 0, 0, 0);
+      f1 = f0;
+      if (nrow < n) {
+        f0 = __ldg(F + 2 * nrow);
+        f1 = __ldg(F + 2 * nrow + 1);
+      }
+    }
+    tc::tmem_wait_st();
+    tc::fence_before_sync();
+    tc::named_sync(bar_id, 128);
+    MLP_PROF(1);
+    if (leader) {
+      tc::fence_after_sync();
+      tc::mma_f16_ts(acc, a_op, tc::smem_desc(opaque_u32(sWa), 128, kK1 * 16), idW, 0);
+      tc::mma_commit(bar);
+    }
+    tc::mbar_wait_sleep(bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+    MLP_PROF(2);
+#pragma unroll
+    for (int layer = 1; layer < L; ++layer) {
+      epilogue_act_tmem<W>(lane_acc, lane_a, slope2);
+      tc::fence_before_sync();
+      MLP_PROF(3 * layer);
+      tc::named_sync(bar_id, 128);
+      MLP_PROF(3 * layer + 1);
+      if (leader) {
+        tc::fence_after_sync();
+        const uint32_t wb = opaque_u32(sWa + off_hidden + (uint32_t)((layer - 1) * W * Kp * 2));
+#pragma unroll
+        for (int s = 0; s < Kp / 16; ++s)
+          tc::mma_f16_ts(acc, a_op + s * 8, tc::smem_desc(wb + s * 256, 128, Kp * 16), idW, s > 0);
+        tc::mma_commit(bar);
+      }
+      tc::mbar_wait_sleep(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+      MLP_PROF(3 * layer + 2);
+    }
+    const float logit = head_simt<W>(lane_acc, headw);
+    MLP_PROF(15);
+    if (valid) {
+      if (a.logits) a.logits[row] = logit;
+      if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
+    }
+    tc::fence_before_sync();
+  }
+  if (prof != nullptr && trow == 0) {  // whole-loop span and tile count of this warpgroup
+    prof[(((int64_t)blockIdx.x * G + wg) * 4) * 16 + 13] = it;
+    prof[(((int64_t)blockIdx.x * G + wg) * 4) * 16 + 14] = clock64();
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    prof[(((int64_t)blockIdx.x * G + wg) * 4) * 16 + 12] = (long long)gt;
+  }
+#undef MLP_PROF
+  __syncthreads();
+  if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused query, A operand in TMEM (the production path for the default and
+// C5 shapes): per 128-record tile one warpgroup gathers and interpolates the
+// latent corners (issued a tile ahead, under the previous tile's last MMA),
+// stores the 16 fp16 layer-1 inputs of its row straight into TMEM, and runs
+// the MLP chain with A in TMEM and only the weights in shared memory; the
+// last layer and the N=1 head run on the CUDA cores from the fp32
+// accumulator. 6 (W=48) / 4 (W=64) tiles in flight per SM, bounded by TMEM.
+// ---------------------------------------------------------------------------
+template <int N, int ND, int W, int L, int G, int TPS>
+__global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
+  using C = MlpCfg<W, L, G>;
+  constexpr bool INNER = ND > 0;
+  constexpr int Kp = C::Kp;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const FastLayout& l = a.l;
+  const int tid = threadIdx.x;
+  const int wg = tid >> 7;
+  const int trow = tid & (kTileRows - 1);
+  const int quad = (tid >> 5) & 3;
+  const bool leader = trow == 0;
+  uint8_t* sW = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::W_AL);
+  uint64_t* bar = bars + wg;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + G);
+
+  const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
+  const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
+  const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
+  const int64_t n = min(*a.count, a.cap);
+  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
+  const int64_t stride = (int64_t)gridDim.x * G;
+  const int64_t first = (int64_t)blockIdx.x * G + wg;
+
+  if (tid == 0) {
+    for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
+    tc::fence_barrier_init();
+  }
+  EncIn<N, ND> ea;
+  issue_enc<N, ND>(ea, load_rec(a, first, trow, n, INNER), tpos, tdir, tdist, l.R, l.Rd);
+  RecIn rb = load_rec(a, first + stride, trow, n, INNER);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sW);
+    for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+  const uint32_t acc = *tslot + (uint32_t)(wg * C::STRIDE);
+  const uint32_t a_op = acc + C::AOFF;
+  const uint32_t lane_acc = acc + lane_off, lane_a = a_op + lane_off;
+  {
+    uint32_t tail[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    tail[0] = h2u(__halves2half2(__float2half_rn(1.f), __float2half_rn(0.f)));
+    tc::tmem_st8(lane_a + W / 2, tail);
+  }
+  const uint32_t sWa = tc::smem_u32(sW);
+  constexpr uint32_t off_hidden = (uint32_t)W * kK1 * 2;
+  const uint32_t idW = tc::idesc_f16(W);
+  const __half2 slope2 = __float2half2_rn(kSlope);
+  const uint32_t bar_id = 1 + wg;
+  const float* headw = reinterpret_cast<const float*>(sW + C::OFF_HEADF);
+
+  uint32_t phase = 0;
+  for (int64_t t = first; t < n_tiles; t += stride) {
+    const int64_t row = t * kTileRows + trow;
+    const bool valid = ea.valid;
+    const int my_ray = ea.ray;
+    {
+      float x[16];
+      finish_enc<N, ND>(ea, x);
+      uint32_t fv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fv[i] = h2u(__floats2half2_rn(x[2 * i], x[2 * i + 1]));
+      tc::tmem_st8(lane_a, fv);
+    }
+    tc::tmem_wait_st();
+    tc::fence_before_sync();
+    tc::named_sync(bar_id, 128);
+    if (leader) {
+      tc::fence_after_sync();
+      tc::mma_f16_ts(acc, a_op, tc::smem_desc(opaque_u32(sWa), 128, kK1 * 16), idW, 0);
+      tc::mma_commit(bar);
+    }
+    tc::mbar_wait_sleep(bar, phase);
+    phase ^= 1;
+    tc::fence_after_sync();
+#pragma unroll
+    for (int layer = 1; layer < L; ++layer) {
+      epilogue_act_tmem<W>(lane_acc, lane_a, slope2);
+      tc::fence_before_sync();
+      tc::named_sync(bar_id, 128);
+      if (leader) {
+        tc::fence_after_sync();
+        const uint32_t wb = opaque_u32(sWa + off_hidden + (uint32_t)((layer - 1) * W * Kp * 2));
+#pragma unroll
+        for (int s = 0; s < Kp / 16; ++s)
+          tc::mma_f16_ts(acc, a_op + s * 8, tc::smem_desc(wb + s * 256, 128, Kp * 16), idW, s > 0);
+        tc::mma_commit(bar);
+      }
+      if (layer == L - 1) {  // next tile's gathers in flight under the last MMA + head
+        issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+        rb = load_rec(a, t + 2 * stride, trow, n, INNER);
+      }
+      tc::mbar_wait_sleep(bar, phase);
+      phase ^= 1;
+      tc::fence_after_sync();
+    }
+    const float logit = head_simt<W, 16>(lane_acc, headw);
+    if (valid) {
+      if (a.logits) a.logits[row] = logit;
+      if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
+    }
+    tc::fence_before_sync();
+  }
+  __syncthreads();
+  if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
+}
+
+template <int N, int ND, int W, int L, int G, int TPS>
+int launch_ts(const TcArgs& a, cudaStream_t st) {
+  using C = MlpCfg<W, L, G>;
+  auto kern = query_ts_kernel<N, ND, W, L, G, TPS>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+      cudaSuccess)
+    return check_launch("query_ts: smem attribute");
+  const int per_sm_tmem = 512 / C::COLS;
+  int per_sm = per_sm_tmem < TPS / G ? per_sm_tmem : TPS / G;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  const int64_t need = (max_tiles + G - 1) / G;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 128 * G, C::SMEM, st>>>(a);
+  return check_launch("nif_query_dev(tcgen05 TS)");
+}
+
+// 0 = launched, 1 = no specialisation
+int launch_ts_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
+  const int W = a.l.W, L = a.l.L;
+#define NIF_TS(NN, NDD, WW, LL, GG, TT)                                        \
+  if (f.N == NN && (NDD == 0 ? f.family == NIF_FAMILY_OUTER                    \
+                             : (f.family == NIF_FAMILY_INNER && f.Nd == NDD)) && \
+      W == WW && L == LL) {                                                    \
+    *rc = launch_ts<NN, NDD, WW, LL, GG, TT>(a, st);                           \
+    return 0;                                                                  \
+  }
+  if (g_query_variant == 11) {
+    NIF_TS(3, 0, 64, 2, 1, 4)
+    NIF_TS(5, 3, 48, 3, 1, 6)
+  }
+  NIF_TS(3, 0, 64, 2, 2, 4)
+  NIF_TS(5, 3, 48, 3, 3, 6)
+#undef NIF_TS
+  return 1;
+}
+
+template <int N, int ND>
+int launch_encode_tiles(const uint8_t* blob, const FastLayout& l, const int32_t* obj,
+                        const float* coord4, const float* r, const int64_t* count, int64_t cap,
+                        uint8_t* feat, cudaStream_t st) {
+  const int64_t rows = (cap + kTileRows - 1) / kTileRows * kTileRows;
+  int64_t blocks = (rows + 255) / 256;
+  const int64_t max_blocks = (int64_t)sm_count() * 8;  // grid-stride: the count lives on the device
+  if (blocks > max_blocks) blocks = max_blocks;
+  encode_tiles_kernel<N, ND><<<(unsigned)blocks, 256, 0, st>>>(blob, l, obj, coord4, r, count, cap,
+                                                               feat);
+  return check_launch("nif_encode_tiles");
+}
+
+template <int W, int L, int G, int TPS>
+int launch_mlp_tiles(const MlpArgs& a, cudaStream_t st) {
+  using C = MlpCfg<W, L, G>;
+  auto kern = mlp_tiles_kernel<W, L, G, TPS>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+      cudaSuccess)
+    return check_launch("mlp_tiles: smem attribute");
+  const int per_sm_tmem = 512 / C::COLS;
+  const int per_sm_smem = (int)((228 * 1024) / (C::SMEM + 1024));
+  int per_sm = per_sm_tmem < per_sm_smem ? per_sm_tmem : per_sm_smem;
+  if (per_sm > TPS / G) per_sm = TPS / G;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  const int64_t need = (max_tiles + G - 1) / G;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 128 * G, C::SMEM, st>>>(a);
+  return check_launch("nif_mlp_tiles");
+}
+
+bool mlp_shape_ok(int W, int L) {
+  return ((W == 48 || W == 64) && L >= 2 && L <= 4) || (W == 128 && L >= 2 && L <= 4);
+}
+
+// 0 = launched, 1 = no specialisation for this shape
+int launch_split(const nif_family_view& f, const FastLayout& l, const int32_t* obj,
+                 const int32_t* ray, const float* coord4, const float* r, const int64_t* count,
+                 int64_t cap, uint8_t* occ, float* logits, uint8_t* feat, int hs,
+                 cudaStream_t st, int* rc) {
+  const bool outer = f.family == NIF_FAMILY_OUTER;
+  if (!mlp_shape_ok(l.W, l.L)) return 1;
+  int erc;
+  const uint8_t* blob = (const uint8_t*)f.fast;
+  if (outer && f.N == 3) erc = launch_encode_tiles<3, 0>(blob, l, obj, coord4, r, count, cap, feat, st);
+  else if (!outer && f.N == 5 && f.Nd == 3)
+    erc = launch_encode_tiles<5, 3>(blob, l, obj, coord4, r, count, cap, feat, st);
+  else if (outer && f.N == 2) erc = launch_encode_tiles<2, 0>(blob, l, obj, coord4, r, count, cap, feat, st);
+  else if (outer && f.N == 4) erc = launch_encode_tiles<4, 0>(blob, l, obj, coord4, r, count, cap, feat, st);
+  else if (!outer && f.N == 4 && f.Nd == 3)
+    erc = launch_encode_tiles<4, 3>(blob, l, obj, coord4, r, count, cap, feat, st);
+  else if (!outer && f.N == 5 && f.Nd == 4)
+    erc = launch_encode_tiles<5, 4>(blob, l, obj, coord4, r, count, cap, feat, st);
+  else return 1;
+  if (erc != NIF_OK) {
+    *rc = erc;
+    return 0;
+  }
+  MlpArgs m{blob, feat, ray, count, cap, occ, logits, g_prof};
+#define NIF_MLP(WW, LL, GG, TT)                                              \
+  if (l.W == WW && l.L == LL) {                                              \
+    *rc = launch_mlp_tiles<WW, LL, GG, TT>(m, st);                           \
+    return 0;                                                                \
+  }
+  // tiles per SM bounded by TMEM: W=48 -> 80 columns/tile, W=64 -> 112,
+  // W=128 -> 208
+  NIF_MLP(64, 2, 2, 4)
+  NIF_MLP(48, 3, 3, 6)
+  NIF_MLP(64, 3, 2, 4)
+  NIF_MLP(64, 4, 2, 4)
+  NIF_MLP(48, 2, 3, 6)
+  NIF_MLP(48, 4, 3, 6)
+  NIF_MLP(128, 2, 1, 2)
+  NIF_MLP(128, 3, 1, 2)
+  NIF_MLP(128, 4, 1, 2)
+#undef NIF_MLP
+  return 1;
+}
+
 __global__ void occ_init_kernel(const uint8_t* __restrict__ src, int64_t n,
                                 uint8_t* __restrict__ dst) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -667,7 +1585,7 @@ extern "C" int nif_fast_pack_dev(const nif_family_view* f, void* blob, void* str
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(blob, 0, l.total, st);
   if (l.tc_ok) {
-    const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp;
+    const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp + l.W + 1;
     pack_weights_kernel<<<(nw + 255) / 256, 256, 0, st>>>(*f, l, (uint8_t*)blob);
   }
   const int64_t cells = 2 * (int64_t)l.n_obj * l.R * l.R +
@@ -685,13 +1603,20 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
     return fail(NIF_ERR_VALUE, "inner queries need the radial coordinate");
   cudaStream_t st = (cudaStream_t)stream;
   const FastLayout l = make_layout(*f);
-  const bool want_tc = impl == NIF_IMPL_TCGEN05 || (impl == NIF_IMPL_AUTO && l.tc_ok && f->fast);
+  const bool want_tc = impl == NIF_IMPL_TCGEN05 || impl == NIF_IMPL_TCGEN05_GENERIC ||
+                       (impl == NIF_IMPL_AUTO && l.tc_ok && f->fast);
   if (want_tc) {
     if (!l.tc_ok)
       return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernel");
     if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
     TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
              logits, g_prof};
+    if (impl != NIF_IMPL_TCGEN05_GENERIC && g_prof == nullptr && g_query_variant != 2) {
+      int rc = NIF_OK;
+      if ((g_query_variant == 0 || g_query_variant == 11) && launch_ts_any(a, *f, st, &rc) == 0)
+        return rc;
+      if (launch_tc2_any(a, *f, st, &rc) == 0) return rc;
+    }
     if (f->family == NIF_FAMILY_OUTER && f->N == 3) return launch_tc<3, 0>(a, st);
     if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 3) return launch_tc<5, 3>(a, st);
     if (f->family == NIF_FAMILY_OUTER && f->N == 2) return launch_tc<2, 0>(a, st);
@@ -711,12 +1636,39 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
   return check_launch("nif_query_dev(simt)");
 }
 
+extern "C" size_t nif_feat_scratch_bytes(int64_t capacity) {
+  return (size_t)((capacity + kTileRows - 1) / kTileRows) * kTileRows * 32;
+}
+
+extern "C" int nif_query_split_dev(const nif_family_view* f, const int32_t* obj,
+                                   const int32_t* ray, const float* coord4, const float* r,
+                                   const int64_t* count_dev, int64_t capacity, uint8_t* occ_ray,
+                                   float* logits, void* feat, int32_t flags, void* stream) {
+  if (capacity <= 0) return NIF_OK;
+  if (f->family == NIF_FAMILY_INNER && r == nullptr)
+    return fail(NIF_ERR_VALUE, "inner queries need the radial coordinate");
+  if (feat == nullptr) return fail(NIF_ERR_VALUE, "split query needs a feature scratch buffer");
+  const FastLayout l = make_layout(*f);
+  if (!l.tc_ok) return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernels");
+  if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
+  int rc = NIF_OK;
+  if (launch_split(*f, l, obj, ray, coord4, r, count_dev, capacity, occ_ray, logits,
+                   (uint8_t*)feat, flags & 1, (cudaStream_t)stream, &rc) != 0)
+    return fail(NIF_ERR_UNSUPPORTED, "no split-path specialisation for W=%d L=%d", l.W, l.L);
+  return rc;
+}
+
 extern "C" int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray,
                                 void* stream) {
   if (n <= 0) return NIF_OK;
   occ_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(bvh_occ, n,
                                                                                   occ_ray);
   return check_launch("nif_occ_init_dev");
+}
+
+extern "C" int nif_debug_set_query_variant(int v) {
+  g_query_variant = v;
+  return NIF_OK;
 }
 
 extern "C" int nif_debug_set_prof(void* buf) {

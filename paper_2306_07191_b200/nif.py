@@ -485,10 +485,11 @@ def logits_arrays(model: NifModel, which: str, obj, x) -> np.ndarray:
 
 
 def query_family(model: NifModel, which: str, obj, coord, impl: int = _lib.IMPL_AUTO,
-                 want_logits: bool = True):
+                 want_logits: bool = True, split: bool = False):
     """Run the fused encode+MLP kernel over host records; returns fp32
     logits (pre-sigmoid). impl selects tcgen05 / SIMT (AUTO = tcgen05 when
-    the configuration is covered)."""
+    the configuration is covered). split=True runs the two-kernel variant
+    (standalone grid encoding, then the tcgen05 MLP over its features)."""
     import torch
     fam = model.family(which)
     obj = np.asarray(obj, np.int64)
@@ -505,9 +506,16 @@ def query_family(model: NifModel, which: str, obj, coord, impl: int = _lib.IMPL_
     d_r = _to_dev(coord[:, 4], np.float32, dev) if which == "inner" else None
     d_cnt = torch.tensor([m], dtype=torch.int64, device=dev)
     d_log = torch.empty(m * fam.dims[-1], dtype=torch.float32, device=dev)
-    _lib.lib().nif_query_dev(fam.view(with_fast=True), _lib.ptr(d_obj), _lib.ptr(d_ray),
-                             _lib.ptr(d_c4), _lib.ptr(d_r), _lib.ptr(d_cnt), m, None,
-                             _lib.ptr(d_log), impl, _lib.stream_ptr())
+    if split:
+        L = _lib.lib()
+        feat = torch.empty(int(L.nif_feat_scratch_bytes(m)), dtype=torch.uint8, device=dev)
+        L.nif_query_split_dev(fam.view(with_fast=True), _lib.ptr(d_obj), _lib.ptr(d_ray),
+                              _lib.ptr(d_c4), _lib.ptr(d_r), _lib.ptr(d_cnt), m, None,
+                              _lib.ptr(d_log), _lib.ptr(feat), 0, _lib.stream_ptr())
+    else:
+        _lib.lib().nif_query_dev(fam.view(with_fast=True), _lib.ptr(d_obj), _lib.ptr(d_ray),
+                                 _lib.ptr(d_c4), _lib.ptr(d_r), _lib.ptr(d_cnt), m, None,
+                                 _lib.ptr(d_log), impl, _lib.stream_ptr())
     return d_log.cpu().numpy()
 
 
