@@ -206,12 +206,15 @@ int nif_query_split_dev(const nif_family_view* f, const int32_t* obj, const int3
 int nif_debug_set_prof(void* buf);
 /* Same for the gather (one-tile-per-CTA variant): buf[tile][8].        */
 int nif_debug_set_prof_gather(void* buf);
-/* Gather hot-path variant: 0 persistent pipelined (default), 1 one tile
- * per CTA. Both produce identical records.                             */
+/* Gather hot-path variant: 0 unordered warp-chunk compaction (default;
+ * queue order is arbitrary, per-ray results identical), 1 one tile per CTA
+ * with look-back (reference order), 2 persistent TMA-pipelined look-back
+ * (reference order). All produce the same records.                     */
 int nif_debug_set_gather_variant(int v);
-/* Query-kernel variant (benchmarks / equivalence tests): 0 specialised,
- * 8 tiles per SM, corner prefetch (default); 1 specialised, 6 tiles per
- * SM; 2 runtime-shape generic kernel; 3 specialised, no corner prefetch. */
+/* Query-kernel variant (benchmarks / equivalence tests): 0 fused with the
+ * A operand in TMEM (default); 1 / 9 shared-memory-operand specialisations
+ * (6 / 4 tiles per SM); 2 runtime-shape generic kernel; 3 no corner
+ * prefetch; 11 TMEM operand, one tile per CTA.                          */
 int nif_debug_set_query_variant(int v);
 
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */

@@ -107,13 +107,53 @@ __device__ __forceinline__ void sph32(double x, double y, double z, double n, fl
   *v = acosf(zz) * (1.0f / CUDART_PI_F);
 }
 
+// Hot-path spherical map (geometry.py:233-246) with minimax polynomials in
+// place of atan2f / acosf (a quarter of the gather's instructions):
+//   atan(a) = a * P(a^2) on [0, 1], |err| < 1e-7 rad (degree 7 in a^2);
+//   acos(z) = sqrt(1 - z) * Q(z) on [0, 1], |err| < 3e-8 (degree 7),
+// with the quadrant / sign logic of atan2 (signed zeros included, so
+// atan2(+0, -0) = pi as in the reference) and acos(-z) = pi - acos(z).
+// The queue coordinates stay within 2e-7 of the fp64 reference map.
+__device__ __forceinline__ float fast_atan2(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+  const float s = a * a;
+  float p = -0.0047803754f;
+  p = fmaf(p, s, 0.02455685f);
+  p = fmaf(p, s, -0.059904344f);
+  p = fmaf(p, s, 0.09942734f);
+  p = fmaf(p, s, -0.14029412f);
+  p = fmaf(p, s, 0.19971374f);
+  p = fmaf(p, s, -0.33332095f);
+  p = fmaf(p, s, 0.99999994f);
+  float r = p * a;
+  if (ay > ax) r = 1.57079632679f - r;
+  if (signbit(x)) r = 3.14159265359f - r;
+  return copysignf(r, y);
+}
+
+__device__ __forceinline__ float fast_acos(float z) {
+  const float za = fminf(fabsf(z), 1.0f);
+  float q = -0.0012628123f;
+  q = fmaf(q, za, 0.006671229f);
+  q = fmaf(q, za, -0.017089725f);
+  q = fmaf(q, za, 0.030892996f);
+  q = fmaf(q, za, -0.050174695f);
+  q = fmaf(q, za, 0.08897905f);
+  q = fmaf(q, za, -0.2145988f);
+  q = fmaf(q, za, 1.5707963f);
+  const float r = sqrtf(1.0f - za) * q;
+  return z < 0.f ? 3.14159265359f - r : r;
+}
+
 __device__ __forceinline__ void sph32f(float x, float y, float z, float n, float* u, float* v) {
-  float uu = (atan2f(y, x) + CUDART_PI_F) * (0.5f / CUDART_PI_F);
+  float uu = fmaf(fast_atan2(y, x), 0.5f / CUDART_PI_F, 0.5f);
   if (uu >= 1.0f) uu -= 1.0f;
   else if (uu < 0.0f) uu += 1.0f;
   const float zz = fminf(fmaxf(__fdividef(z, n), -1.0f), 1.0f);
   *u = uu;
-  *v = acosf(zz) * (1.0f / CUDART_PI_F);
+  *v = fast_acos(zz) * (1.0f / CUDART_PI_F);
 }
 
 // The reference's degenerate test sqrt(r.r) < 1e-9 in fp64, exactly: the
@@ -878,8 +918,227 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   }
 }
 
+
+// ===========================================================================
+// Hot-path gather with unordered (warp-granular) compaction.
+//
+// The visibility pass only needs, per ray, the OR of its records' bits, so
+// the hot-path queues need not be in the reference's ray-major order (the
+// API gather above keeps it). Each warp takes 32-ray chunks (static stride,
+// no CTA-wide barriers at all), classifies exactly as above, reserves its
+// records with one atomicAdd per queue, and writes them contiguously (rays
+// of a chunk stay adjacent, which keeps the query kernels' latent gathers
+// coherent). No scan, no look-back, no staging: a warp never waits on
+// another. Per-ray results are identical to the ordered kernels.
+// ===========================================================================
+#ifndef NIF_GATHER_MINB_U
+#define NIF_GATHER_MINB_U 3
+#endif
+
+__global__ void __launch_bounds__(kThreads, NIF_GATHER_MINB_U)
+gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
+                   const double* __restrict__ org, const double* __restrict__ dir,
+                   const double* __restrict__ tms, int64_t n, nif_gather_out out,
+                   unsigned long long* __restrict__ reserve, unsigned int* __restrict__ done) {
+  __shared__ ObjC objs[kMaxObjFused];
+  __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
+  __shared__ float s_absmax;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int n_obj = s.n_obj;
+  if (tid == 0) s_absmax = 0.f;
+  __syncthreads();
+  if (tid < n_obj) {
+    ObjC& b = objs[tid];
+    const int ob = s.t_order[tid];
+    const double* bx = s.obox + (size_t)ob * 6;
+    float am = 0.f;
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = bx[a];
+      b.hi[a] = bx[3 + a];
+      b.lt[a] = bx[a] - s.tol;
+      b.ht[a] = bx[3 + a] + s.tol;
+      b.c[a] = 0.5 * (bx[a] + bx[3 + a]);
+      am = fmaxf(am, fmaxf(fabsf((float)bx[a]), fabsf((float)bx[3 + a])));
+    }
+    flo[tid] = make_float4((float)bx[0], (float)bx[1], (float)bx[2], 0.f);
+    fhi[tid] = make_float4((float)bx[3], (float)bx[4], (float)bx[5], 0.f);
+    const double hx = 0.5 * (bx[3] - bx[0]), hy = 0.5 * (bx[4] - bx[1]),
+                 hz = 0.5 * (bx[5] - bx[2]);
+    b.hn = sqrt(hx * hx + hy * hy + hz * hz);
+    b.id = ob;
+    b.route = route[ob];
+    b.root = s.roots[ob];
+    atomicMax(reinterpret_cast<int*>(&s_absmax), __float_as_int(am));
+  }
+  __syncthreads();
+  const bool test_box = n_obj > 1;
+  const uint32_t all_obj = n_obj >= 32 ? 0xffffffffu : ((1u << n_obj) - 1u);
+  const int64_t n_chunks = (n + 31) / 32;
+  const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
+  const float absmax = s_absmax;
+  int deg_count = 0;
+  for (int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + warp; c < n_chunks; c += nw) {
+    const int64_t i = c * 32 + lane;
+    const bool valid = i < n;
+    RayX r{};
+    RayF q{};
+    bool use_pf = false;
+    if (valid) {
+      r.ox = __ldg(org + i * 3 + 0);
+      r.oy = __ldg(org + i * 3 + 1);
+      r.oz = __ldg(org + i * 3 + 2);
+      r.dx = __ldg(dir + i * 3 + 0);
+      r.dy = __ldg(dir + i * 3 + 1);
+      r.dz = __ldg(dir + i * 3 + 2);
+      r.tmax = __ldg(tms + i);
+      r.ix = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
+      r.iy = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
+      r.iz = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
+      use_pf = n_obj > 1 && fabs(r.dx) > 1e-20 && fabs(r.dy) > 1e-20 && fabs(r.dz) > 1e-20;
+      if (use_pf) {
+        q.ix = (float)r.ix;
+        q.iy = (float)r.iy;
+        q.iz = (float)r.iz;
+        q.ox = (float)r.ox;
+        q.oy = (float)r.oy;
+        q.oz = (float)r.oz;
+        q.ox_i = -q.ox * q.ix;
+        q.oy_i = -q.oy * q.iy;
+        q.oz_i = -q.oz * q.iz;
+        const float S = absmax + fmaxf(fmaxf(fabsf(q.ox), fabsf(q.oy)), fabsf(q.oz)) + 1e-30f;
+        const float imax = fmaxf(fmaxf(fabsf(q.ix), fabsf(q.iy)), fabsf(q.iz));
+        q.dt = 1e-5f * S * imax;
+        q.tmax_ru = __double2float_ru(r.tmax);
+        use_pf = isfinite(q.dt);
+      }
+    }
+    uint64_t mask = 0;
+    uint32_t hyb = 0;
+    int n_out = 0, n_in = 0;
+    const uint32_t wmask = warp_bundle_mask(q, use_pf, valid, lane, n_obj, flo, fhi, all_obj, absmax);
+    if (valid) {
+      uint32_t pmask = 0;
+      if (use_pf) {
+        uint32_t w = wmask;
+        while (w) {
+          const int k = __ffs(w) - 1;
+          w &= w - 1;
+          pmask |= (uint32_t)prefilter(q, flo[k], fhi[k]) << k;
+        }
+      } else {
+        pmask = all_obj;
+      }
+      while (pmask) {
+        const int k = __ffs(pmask) - 1;
+        pmask &= pmask - 1;
+        double t0;
+        const int kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
+        if (kind == 0) continue;
+        if (objs[k].route == 1) {
+          mask |= (uint64_t)kind << (2 * k);
+          if (kind == 1) ++n_out;
+          else ++n_in;
+        } else {
+          hyb |= 1u << k;
+        }
+      }
+      bool occ = false;
+      uint32_t h = hyb;
+      while (h != 0 && !occ) {
+        const int k = __ffs(h) - 1;
+        h &= h - 1;
+        occ = occluded_in_object(s.nodes, s.tris, objs[k].root, r.ox, r.oy, r.oz, r.dx, r.dy,
+                                 r.dz, s.eps, r.tmax);
+      }
+      out.bvh_occ[i] = occ ? 1 : 0;
+    }
+    // warp-level reservation of this chunk's records
+    const int packed = (n_out << 16) | n_in;
+    int incl = packed;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot == 0) continue;
+    // one 64-bit atomic per chunk reserves both queues: outer count in the
+    // high word, inner in the low word (each < 2^31 by the slot bound)
+    unsigned long long base = 0;
+    if (lane == 0)
+      base = atomicAdd(reserve, ((unsigned long long)(tot >> 16) << 32) |
+                                    (unsigned long long)(tot & 0xffff));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const int64_t base_o = (int64_t)(base >> 32);
+    const int64_t base_i = (int64_t)(base & 0xffffffffull);
+    if (mask == 0) continue;
+    const int excl = incl - packed;
+    int64_t jo = base_o + (excl >> 16);
+    int64_t ji = base_i + (excl & 0xffff);
+    float du, dv;
+    sph32f((float)r.dx, (float)r.dy, (float)r.dz, 1.0f, &du, &dv);
+    uint64_t m = mask;
+    while (m != 0) {
+      const int bit = __ffsll((long long)m) - 1;
+      const int k = bit >> 1;
+      const int kind = (int)((m >> (2 * k)) & 3);
+      m &= ~(3ull << (2 * k));
+      const ObjC& b = objs[k];
+      float c0, c1, rr = 0.f;
+      float rnf;
+      bool deg;
+      if (kind == 1) {
+        const Hit3 hh = slab(r, b);
+        const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy, ez = r.oz + hh.t0 * r.dz;
+        const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
+        deg = degenerate_f32(rx, ry, rz, &rnf);
+        if (deg) { c0 = 0.5f; c1 = 0.5f; }
+        else sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+        if (jo < out.cap_outer) {
+          out.outer_obj[jo] = b.id;
+          out.outer_ray[jo] = (int32_t)i;
+          reinterpret_cast<float4*>(out.outer_coord)[jo] = make_float4(c0, c1, du, dv);
+        }
+        ++jo;
+      } else {
+        const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
+        deg = degenerate_f32(rx, ry, rz, &rnf);
+        if (deg) { c0 = 0.5f; c1 = 0.5f; rr = 0.f; }
+        else {
+          sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+          rr = fminf(rnf / (float)b.hn, 1.0f);
+        }
+        if (ji < out.cap_inner) {
+          out.inner_obj[ji] = b.id;
+          out.inner_ray[ji] = (int32_t)i;
+          reinterpret_cast<float4*>(out.inner_coord)[ji] = make_float4(c0, c1, du, dv);
+          out.inner_r[ji] = rr;
+        }
+        ++ji;
+      }
+      deg_count += deg ? 1 : 0;
+    }
+  }
+  const int dsum = __reduce_add_sync(0xffffffffu, deg_count);
+  if (lane == 0 && dsum)
+    atomicAdd((unsigned long long*)(out.counts + 3), (unsigned long long)dsum);
+  // the last CTA to finish publishes the queue lengths
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && tid == 0) {
+    const unsigned long long v = atomicAdd(reserve, 0ull);
+    out.counts[0] = (int64_t)(v >> 32);
+    out.counts[1] = (int64_t)(v & 0xffffffffull);
+    out.counts[2] = out.counts[0] + out.counts[1];
+  }
+}
+
 long long* g_gprof = nullptr;  // diagnostic phase stamps (nif_debug_set_prof_gather)
-int g_gather_variant = 0;      // 0 persistent pipelined, 1 one tile per CTA (diagnostics)
+int g_gather_variant = 0;  // 0 unordered warp chunks, 1 one tile per CTA, 2 persistent ordered
 
 size_t fused_ws(int64_t n) {
   const int64_t tiles = (n + kThreads - 1) / kThreads;
@@ -916,14 +1175,23 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
   uint8_t* ws = (uint8_t*)workspace;
   unsigned long long* status = (unsigned long long*)ws;
   int* ctr = (int*)(ws + align_up((size_t)tiles * 8, 256));
-  cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
+  const bool unordered = out->rec_kind == nullptr && g_gprof == nullptr && g_gather_variant == 0;
+  if (!unordered) cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
+  else cudaMemsetAsync(ctr, 0, 16, st);  // reservation counter + done counter
   if (out->rec_kind != nullptr)
     gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
   else if (g_gprof != nullptr || g_gather_variant == 1)
     gather_fused_kernel<false><<<(unsigned)tiles, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
-  else {
+  else if (g_gather_variant == 0) {
+    const int64_t chunks = (n + 31) / 32;
+    int64_t grid = (int64_t)sm_count() * NIF_GATHER_MINB_U;
+    if (grid * (kThreads / 32) > chunks) grid = (chunks + kThreads / 32 - 1) / (kThreads / 32);
+    gather_warp_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
+        *s, route, origins, dirs, tmaxs, n, *out, (unsigned long long*)ctr,
+        (unsigned int*)((unsigned long long*)ctr + 1));
+  } else {
     const int smem = kStages * kStageBytes;
     static bool attr = false;
     if (!attr) {

@@ -102,10 +102,20 @@ def test_fast_queue_coords_close_to_exact(cuda):
     oc = buf.outer_coord[:no * 4].view(no, 4).cpu().numpy()
     ic = buf.inner_coord[:ni * 4].view(ni, 4).cpu().numpy()
     ir = buf.inner_r[:ni].cpu().numpy()
-    ex_o = rec.coord[rec.kind == 0]
-    ex_i = rec.coord[rec.kind == 1]
-    np.testing.assert_array_equal(buf.outer_ray[:no].cpu().numpy(), rec.ray[rec.kind == 0])
-    np.testing.assert_array_equal(buf.inner_obj[:ni].cpu().numpy(), rec.obj[rec.kind == 1])
+    # the hot-path queues are unordered: bring both sides to (ray, object)
+    # order first
+    ko, ki = rec.kind == 0, rec.kind == 1
+    qo = np.lexsort((rec.obj[ko], rec.ray[ko]))
+    qi = np.lexsort((rec.obj[ki], rec.ray[ki]))
+    ex_o, ex_i = rec.coord[ko][qo], rec.coord[ki][qi]
+    oray, oobj = buf.outer_ray[:no].cpu().numpy(), buf.outer_obj[:no].cpu().numpy()
+    iray, iobj = buf.inner_ray[:ni].cpu().numpy(), buf.inner_obj[:ni].cpu().numpy()
+    po, pi = np.lexsort((oobj, oray)), np.lexsort((iobj, iray))
+    oc, ic, ir = oc[po], ic[pi], ir[pi]
+    np.testing.assert_array_equal(oray[po], rec.ray[ko][qo])
+    np.testing.assert_array_equal(oobj[po], rec.obj[ko][qo])
+    np.testing.assert_array_equal(iobj[pi], rec.obj[ki][qi])
+    np.testing.assert_array_equal(iray[pi], rec.ray[ki][qi])
     # u wraps at 1 -> compare on the circle
     def cdist(a, b):
         dd = np.abs(a - b)
