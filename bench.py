@@ -38,6 +38,17 @@ METRIC = "NIF shadow-ray queries/s per GPU; secondary-ray cast ms/frame vs BVH"
 UNIT = "shadow rays/s"
 WORKLOAD = ("C2: 12x icosphere(6) + NIF plane, 983,042 tris, 13 objects, 1920x1080, "
             "1 spp point-light shadow rays, inference only")
+WORKLOADS = {
+    "c1": "C1: icosphere(5) + BVH-routed plane, 20,480 NIF tris, 256x256, 1 spp shadow rays",
+    "c2": WORKLOAD,
+    "c3": ("C3: 24x icosphere(8) + NIF plane, 31,457,282 tris, 25 objects, 1920x1080, "
+           "1 spp point-light shadow rays, inference"),
+}
+# kernels of one visibility pass (names as ncu reports them) and their
+# algorithmic work: see DESIGN.md section 4
+K_GATHER = "gather_warp_kernel"
+K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4>"
+K_INNER = "query_ts_kernel<5, 3, 48, 3, 3, 6>"
 
 
 def parse():
@@ -230,7 +241,7 @@ def run_reference(args, rank, ws):
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": WORKLOAD, "rays_per_frame": int(len(rays[0])),
+            "config": {"workload": WORKLOADS[args.config], "rays_per_frame": int(len(rays[0])),
                        "sample_rays_per_step": n},
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -388,30 +399,38 @@ def main():
                 + cfgm.inner.hidden_width)
     # algorithmic bytes of one gather launch: rays in (origins, dirs, tmaxs
     # f64 = 56 B), bvh_occ out (1 B), records out (outer obj+ray+coord4 = 24 B,
-    # inner + r = 28 B)
+    # inner + r = 28 B); algorithmic FLOPs of the MLPs (useful MACs only)
     gather_bytes = 56 * n + 1 * n + 24 * n_outer + 28 * n_inner
-    dominant = max(("gather", "query_outer", "query_inner"), key=lambda k: kt[k])
-    if dominant == "gather":
-        roof = {"bound": "hbm", "kernel": "nif_gather (count+scan+write)",
-                "achieved": gather_bytes / (kt["gather"] / 1e3) / 1e9,
-                "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-    else:
-        nrec = n_outer if dominant == "query_outer" else n_inner
-        fl = fl_o if dominant == "query_outer" else fl_i
-        roof = {"bound": "tensor", "kernel": f"query_tc_kernel ({dominant})",
-                "achieved": nrec * fl / (kt[dominant] / 1e3) / 1e12,
-                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    tr = {}
     tj = ROOT / "profiles" / "traffic.json"
     if tj.exists():
         tr = json.loads(tj.read_text())
-        key = {"gather": "gather_fused_kernel", "query_outer": "query_tc_kernel<3, 0>",
-               "query_inner": "query_tc_kernel<5, 3>"}[dominant]
+
+    def roof_of(k):
+        if k == "gather":
+            r = {"bound": "hbm", "kernel": f"{K_GATHER} (classify + unordered compaction)",
+                 "achieved": gather_bytes / (kt["gather"] / 1e3) / 1e9,
+                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "work_per_launch_bytes": gather_bytes}
+            key = K_GATHER
+        else:
+            nrec = n_outer if k == "query_outer" else n_inner
+            fl = fl_o if k == "query_outer" else fl_i
+            key = K_OUTER if k == "query_outer" else K_INNER
+            r = {"bound": "tensor", "kernel": f"{key} (fused encode + MLP, {k})",
+                 "achieved": nrec * fl / (kt[k] / 1e3) / 1e12,
+                 "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                 "work_per_launch_flop": nrec * fl}
+        r["frac"] = r["achieved"] / r["peak"]
+        r["traffic"] = None
         if key in tr:
-            roof["traffic"] = tr[key]["dram_bytes_read"] + tr[key]["dram_bytes_write"]
-            roof["traffic_source"] = tr["_source"]
-    roof["peak_source"] = "MEASURED_PEAKS.json (burst)"
+            r["traffic"] = tr[key]["dram_bytes_read"] + tr[key]["dram_bytes_write"]
+            r["traffic_source"] = tr["_source"]
+        r["peak_source"] = "MEASURED_PEAKS.json (burst)"
+        return r
+
+    dominant = max(("gather", "query_outer", "query_inner"), key=lambda k: kt[k])
+    roof = roof_of(dominant)
+    rooflines = {k: roof_of(k) for k in ("gather", "query_outer", "query_inner")}
 
     cpu = None
     if not args.no_cpu_baseline and not args.profile:
@@ -427,7 +446,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp16-mma/fp32-acc (fp64 gather)",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "rays_per_frame_per_gpu": n, "outer_records": n_outer,
+        "config": {"workload": WORKLOADS[args.config], "rays_per_frame_per_gpu": n,
+                   "outer_records": n_outer,
                    "inner_records": n_inner, "model": "NifConfig() defaults (R 256/128)",
                    "trained_epochs": args.train_epochs, "l2": "flushed (256 MiB write) per step",
                    "parallelism": f"{ws} independent frames (sample index = rank)"},
@@ -435,6 +455,7 @@ def main():
         "bvh_ms_per_frame": kt["bvh_anyhit"],
         "kernel_ms": kt,
         "roofline": roof,
+        "rooflines": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n)},

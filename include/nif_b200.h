@@ -187,9 +187,10 @@ int nif_query_dev(const nif_family_view* f, const int32_t* obj, const int32_t* r
                   int64_t capacity, uint8_t* occ_ray, float* logits, int32_t impl,
                   void* stream);
 /* Split variant: a standalone grid-encoding kernel writes 16 fp16 features
- * per record into 128-row UMMA-layout tiles in feat (nif_feat_scratch_bytes
- * of capacity), then the tcgen05 MLP kernel streams them in by TMA bulk
- * copies. flags bit 0: last layer + head on the CUDA cores.            */
+ * per record (32 B, row-major) into feat (nif_feat_scratch_bytes of
+ * capacity), then the tcgen05 MLP kernel (A operand in TMEM) reads them
+ * row by row. flags: bit 1 runs only the encoding kernel, bit 2 only the
+ * MLP kernel (over features already in feat) -- for per-stage timing.  */
 size_t nif_feat_scratch_bytes(int64_t capacity);
 int nif_query_split_dev(const nif_family_view* f, const int32_t* obj, const int32_t* ray,
                         const float* coord4, const float* r, const int64_t* count_dev,

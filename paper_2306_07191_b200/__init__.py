@@ -9,6 +9,7 @@ every entry point raises.
 """
 
 from . import _lib
+from .checkpoint import SceneFormatError, load_checkpoint, save_checkpoint
 from .meshgen import ground_plane, icosphere, mesh_arrays, torus
 from .nif import (
     AdamParams, InnerConfig, NifConfig, NifModel, OuterConfig, build_model,

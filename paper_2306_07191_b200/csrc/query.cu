@@ -1499,12 +1499,14 @@ bool mlp_shape_ok(int W, int L) {
 // 0 = launched, 1 = no specialisation for this shape
 int launch_split(const nif_family_view& f, const FastLayout& l, const int32_t* obj,
                  const int32_t* ray, const float* coord4, const float* r, const int64_t* count,
-                 int64_t cap, uint8_t* occ, float* logits, uint8_t* feat, int hs,
+                 int64_t cap, uint8_t* occ, float* logits, uint8_t* feat, int flags,
                  cudaStream_t st, int* rc) {
   const bool outer = f.family == NIF_FAMILY_OUTER;
   if (!mlp_shape_ok(l.W, l.L)) return 1;
-  int erc;
+  int erc = NIF_OK;
   const uint8_t* blob = (const uint8_t*)f.fast;
+  const bool enc_only = (flags & 2) != 0, mlp_only = (flags & 4) != 0;
+  if (mlp_only) goto mlp;
   if (outer && f.N == 3) erc = launch_encode_tiles<3, 0>(blob, l, obj, coord4, r, count, cap, feat, st);
   else if (!outer && f.N == 5 && f.Nd == 3)
     erc = launch_encode_tiles<5, 3>(blob, l, obj, coord4, r, count, cap, feat, st);
@@ -1515,10 +1517,11 @@ int launch_split(const nif_family_view& f, const FastLayout& l, const int32_t* o
   else if (!outer && f.N == 5 && f.Nd == 4)
     erc = launch_encode_tiles<5, 4>(blob, l, obj, coord4, r, count, cap, feat, st);
   else return 1;
-  if (erc != NIF_OK) {
+  if (erc != NIF_OK || enc_only) {
     *rc = erc;
     return 0;
   }
+mlp:
   MlpArgs m{blob, feat, ray, count, cap, occ, logits, g_prof};
 #define NIF_MLP(WW, LL, GG, TT)                                              \
   if (l.W == WW && l.L == LL) {                                              \
@@ -1653,7 +1656,7 @@ extern "C" int nif_query_split_dev(const nif_family_view* f, const int32_t* obj,
   if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
   int rc = NIF_OK;
   if (launch_split(*f, l, obj, ray, coord4, r, count_dev, capacity, occ_ray, logits,
-                   (uint8_t*)feat, flags & 1, (cudaStream_t)stream, &rc) != 0)
+                   (uint8_t*)feat, flags, (cudaStream_t)stream, &rc) != 0)
     return fail(NIF_ERR_UNSUPPORTED, "no split-path specialisation for W=%d L=%d", l.W, l.L);
   return rc;
 }

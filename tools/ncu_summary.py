@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py full  gpurun_out/prof.ncu-rep  > profiles/x.md
     python tools/ncu_summary.py launches gpurun_out/launches.csv > profiles/x_launches.md
+    python tools/ncu_summary.py traffic gpurun_out/prof.ncu-rep "source" > profiles/traffic.json
 """
 
 from __future__ import annotations
@@ -56,6 +57,25 @@ def full(path):
     print("\n".join(out))
 
 
+def traffic(path, source="ncu --set full"):
+    """DRAM bytes per launch of each kernel (last launch captured), keyed by
+    the short kernel name bench.py uses for roofline.traffic."""
+    import json
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    head, units = rows[0], rows[1]
+    kn = head.index("Kernel Name")
+    rd, wr = head.index("dram__bytes_read.sum"), head.index("dram__bytes_write.sum")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    out = {"_source": source}
+    for r in rows[2:]:
+        short = r[kn].split("(")[0].replace("void ", "").replace("nif::<unnamed>::", "")
+        out[short] = {"dram_bytes_read": int(float(r[rd].replace(",", "")) * scale[units[rd]]),
+                      "dram_bytes_write": int(float(r[wr].replace(",", "")) * scale[units[wr]])}
+    print(json.dumps(out, indent=1))
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -77,4 +97,4 @@ def launches(path):
 
 
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"full": full, "launches": launches, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
