@@ -1049,21 +1049,10 @@ int launch_tc2_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, i
 constexpr int kFeatTileBytes = kTileRows * kK1 * 2;  // 4096
 
 template <int N, int ND>
-__global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __restrict__ blob,
-                                                           FastLayout l,
-                                                           const int32_t* __restrict__ obj,
-                                                           const float* __restrict__ coord4,
-                                                           const float* __restrict__ rr,
-                                                           const int64_t* __restrict__ count,
-                                                           int64_t cap, uint8_t* __restrict__ feat) {
-  constexpr bool INNER = ND > 0;
-  const int64_t n = min(*count, cap);
-  const int64_t n_pad = (n + kTileRows - 1) / kTileRows * kTileRows;
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n_pad;
-       row += (int64_t)gridDim.x * blockDim.x) {
-  const __half* tpos = reinterpret_cast<const __half*>(blob + l.off_pos);
-  const __half* tdir = reinterpret_cast<const __half*>(blob + l.off_dir);
-  const __half* tdist = reinterpret_cast<const __half*>(blob + l.off_dist);
+__device__ __forceinline__ RecIn load_rec_row(const int32_t* __restrict__ obj,
+                                              const float* __restrict__ coord4,
+                                              const float* __restrict__ rr, int64_t row,
+                                              int64_t n) {
   RecIn r;
   r.valid = row < n;
   r.obj = 0;
@@ -1073,10 +1062,13 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __rest
   if (r.valid) {
     r.obj = __ldg(obj + row);
     r.c = __ldg(reinterpret_cast<const float4*>(coord4) + row);
-    if (INNER) r.r = __ldg(rr + row);
+    if (ND > 0) r.r = __ldg(rr + row);
   }
-  EncIn<N, ND> e;
-  issue_enc<N, ND>(e, r, tpos, tdir, tdist, l.R, l.Rd);
+  return r;
+}
+
+template <int N, int ND>
+__device__ __forceinline__ void store_feat(const EncIn<N, ND>& e, uint8_t* feat, int64_t row) {
   float x[16];
   finish_enc<N, ND>(e, x);
   uint4 v0, v1;
@@ -1091,6 +1083,36 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __rest
   uint4* p = reinterpret_cast<uint4*>(feat) + 2 * row;
   __stcg(p, v0);
   __stcg(p + 1, v1);
+}
+
+// Grid-stride over records, two records per thread per iteration and the
+// next iteration's record words prefetched, so each thread keeps two
+// corner-gather round trips and one record fetch in flight.
+template <int N, int ND>
+__global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __restrict__ blob,
+                                                           FastLayout l,
+                                                           const int32_t* __restrict__ obj,
+                                                           const float* __restrict__ coord4,
+                                                           const float* __restrict__ rr,
+                                                           const int64_t* __restrict__ count,
+                                                           int64_t cap, uint8_t* __restrict__ feat) {
+  const int64_t n = min(*count, cap);
+  const int64_t n_pad = (n + kTileRows - 1) / kTileRows * kTileRows;
+  const __half* tpos = reinterpret_cast<const __half*>(blob + l.off_pos);
+  const __half* tdir = reinterpret_cast<const __half*>(blob + l.off_dir);
+  const __half* tdist = reinterpret_cast<const __half*>(blob + l.off_dist);
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  RecIn ra = load_rec_row<N, ND>(obj, coord4, rr, row, n);
+  RecIn rb = load_rec_row<N, ND>(obj, coord4, rr, row + nt, n);
+  for (; row < n_pad; row += 2 * nt) {
+    EncIn<N, ND> ea, eb;
+    issue_enc<N, ND>(ea, ra, tpos, tdir, tdist, l.R, l.Rd);
+    issue_enc<N, ND>(eb, rb, tpos, tdir, tdist, l.R, l.Rd);
+    ra = load_rec_row<N, ND>(obj, coord4, rr, row + 2 * nt, n);
+    rb = load_rec_row<N, ND>(obj, coord4, rr, row + 3 * nt, n);
+    store_feat<N, ND>(ea, feat, row);
+    if (row + nt < n_pad) store_feat<N, ND>(eb, feat, row + nt);
   }
 }
 
@@ -1454,6 +1476,20 @@ int launch_ts_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, in
   }
   NIF_TS(3, 0, 64, 2, 2, 4)
   NIF_TS(5, 3, 48, 3, 3, 6)
+  // C5 sweep shapes (TMEM: W=48 -> 80 columns per tile, 64 -> 112, 128 -> 208)
+  NIF_TS(3, 0, 64, 3, 2, 4)
+  NIF_TS(3, 0, 64, 4, 2, 4)
+  NIF_TS(3, 0, 128, 2, 1, 2)
+  NIF_TS(3, 0, 128, 3, 1, 2)
+  NIF_TS(3, 0, 128, 4, 1, 2)
+  NIF_TS(5, 3, 48, 2, 3, 6)
+  NIF_TS(5, 3, 48, 4, 3, 6)
+  NIF_TS(5, 3, 64, 2, 2, 4)
+  NIF_TS(5, 3, 64, 3, 2, 4)
+  NIF_TS(5, 3, 64, 4, 2, 4)
+  NIF_TS(5, 3, 128, 2, 1, 2)
+  NIF_TS(5, 3, 128, 3, 1, 2)
+  NIF_TS(5, 3, 128, 4, 1, 2)
 #undef NIF_TS
   return 1;
 }

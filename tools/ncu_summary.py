@@ -70,7 +70,7 @@ def traffic(path, source="ncu --set full"):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     out = {"_source": source}
     for r in rows[2:]:
-        short = r[kn].split("(")[0].replace("void ", "").replace("nif::<unnamed>::", "")
+        short = r[kn].split("(")[0].replace("void ", "").split("::")[-1]
         out[short] = {"dram_bytes_read": int(float(r[rd].replace(",", "")) * scale[units[rd]]),
                       "dram_bytes_write": int(float(r[wr].replace(",", "")) * scale[units[wr]])}
     print(json.dumps(out, indent=1))
