@@ -217,6 +217,9 @@ int nif_debug_set_gather_variant(int v);
  * (6 / 4 tiles per SM); 2 runtime-shape generic kernel; 3 no corner
  * prefetch; 11 TMEM operand, one tile per CTA.                          */
 int nif_debug_set_query_variant(int v);
+/* Training fwd/bwd kernel: 0 tiled CTA-GEMM kernel where it applies
+ * (shared MLP, width a multiple of 16; default), 1 one row per thread. */
+int nif_debug_set_train_variant(int v);
 
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */
 int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray, void* stream);

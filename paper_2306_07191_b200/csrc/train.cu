@@ -379,9 +379,367 @@ __global__ void adam_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1, AdamSeg s2
   }
 }
 
+
+// Dense Adam, unit-major: blockIdx.z = segment (pos, dir, dist, w, b),
+// blockIdx.y = unit (object grid set or head), blockIdx.x = chunk of the
+// unit's elements. Untouched units exit per block (no per-element test),
+// the bias corrections c1 / c2 are computed once per block, and segments
+// whose per-unit length is a multiple of 4 move p / g / m / v as float4.
+// Per element the reference's fp64 expression (grids.py:33-45) is kept.
+__device__ __forceinline__ void adam_elem(float& p, float& gr, float& m, float& v, double lr,
+                                          double b1, double b2, double eps, double c1,
+                                          double c2) {
+  const double g = (double)gr * 1.0;
+  const double mi = b1 * ((double)m * 1.0) + (1.0 - b1) * g;
+  const double vi = b2 * ((double)v * 1.0) + (1.0 - b2) * g * g;
+  m = (float)mi;
+  v = (float)vi;
+  const double mh = mi / c1;
+  const double vh = vi / c2;
+  p = (float)((double)p - lr * mh / (sqrt(vh) + eps));
+  gr = 0.f;
+}
+
+__global__ void __launch_bounds__(256) adam_units_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1,
+                                                         AdamSeg s2, AdamSeg s3, AdamSeg s4,
+                                                         int shared, double lr, double b1,
+                                                         double b2, double eps) {
+  const AdamSeg segs[5] = {s0, s1, s2, s3, s4};
+  const AdamSeg sg = segs[blockIdx.z];
+  const int64_t unit = blockIdx.y;
+  if (unit >= sg.n_units) return;
+  int64_t step;
+  if (sg.kind == 0) {
+    if (t.counts[unit] <= 0) return;
+    step = t.grid_steps[unit];
+  } else {
+    if (!shared && t.counts[unit] <= 0) return;
+    step = t.mlp_steps[unit];
+  }
+  __shared__ double s_c[2];
+  if (threadIdx.x == 0) {
+    s_c[0] = 1.0 - int_power(b1, step);
+    s_c[1] = 1.0 - int_power(b2, step);
+  }
+  __syncthreads();
+  const double c1 = s_c[0], c2 = s_c[1];
+  const int64_t base = sg.off + unit * sg.per;
+  if ((sg.per & 3) == 0 && (base & 3) == 0) {
+    const int64_t n4 = sg.per >> 2;
+    float4* P = reinterpret_cast<float4*>(t.params + base);
+    float4* G = reinterpret_cast<float4*>(t.grad + base);
+    float4* M = reinterpret_cast<float4*>(t.m + base);
+    float4* V = reinterpret_cast<float4*>(t.v + base);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      float4 p = P[e], g = G[e], m = M[e], v = V[e];
+      adam_elem(p.x, g.x, m.x, v.x, lr, b1, b2, eps, c1, c2);
+      adam_elem(p.y, g.y, m.y, v.y, lr, b1, b2, eps, c1, c2);
+      adam_elem(p.z, g.z, m.z, v.z, lr, b1, b2, eps, c1, c2);
+      adam_elem(p.w, g.w, m.w, v.w, lr, b1, b2, eps, c1, c2);
+      P[e] = p;
+      G[e] = g;
+      M[e] = m;
+      V[e] = v;
+    }
+  } else {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < sg.per;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t q = base + e;
+      adam_elem(t.params[q], t.grad[q], t.m[q], t.v[q], lr, b1, b2, eps, c1, c2);
+    }
+  }
+}
+
 __global__ void clear_counts_kernel(int32_t* counts, int n) {
   const int i = threadIdx.x + blockIdx.x * blockDim.x;
   if (i < n) counts[i] = 0;
+}
+
+
+// ---------------------------------------------------------------------------
+// Tiled variant (shared MLP, hidden width a multiple of 16): 32 rows per CTA
+// of 128 threads, every dense layer a small CTA-wide SIMT GEMM with 4 x W/16
+// register tiles over the rows' activations in shared memory and the layer's
+// weights staged in shared memory (transposed for the forward pass). Each
+// output accumulates bias-first and k ascending with fmaf, exactly the
+// per-row kernel's order, so forward values and the per-row backward
+// quantities are bit-identical to it; only the CTA partial sums of the
+// weight gradients (32 rows instead of 128 per atomic) differ in rounding.
+// 4x more CTAs per batch and ~W/16x less serial work per thread.
+// ---------------------------------------------------------------------------
+constexpr int kRB = 32;     // rows per CTA
+constexpr int kTT = 128;    // threads per CTA
+
+template <int W>
+__global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
+  constexpr int WP = W + 1;
+  constexpr int CPT = W / 16;  // output columns per thread (16 column groups)
+  extern __shared__ float sm[];
+  const int tid = threadIdx.x;
+  const nif_family_view& f = a.f;
+  const int L = f.n_layers - 1;
+  const int IN = f.dims[0];
+  const int OUT = f.dims[f.n_layers];
+  float* zs = sm;                            // [L][kRB][WP] pre-activations
+  float* dzA = zs + (size_t)L * kRB * WP;    // [kRB][WP]
+  float* dzB = dzA + kRB * WP;               // [kRB][WP]
+  float* xs = dzB + kRB * WP;                // [kRB][kMaxIn]
+  float* dh = xs + kRB * kMaxIn;             // [kRB][kMaxOut]
+  float* sw = dh + kRB * kMaxOut;            // [max(W, IN)][W] staged weights
+  const float* Wt = f.w;
+  const float* Bt = f.b;
+  float* gW = a.t.grad + a.t.off_w;
+  float* gB = a.t.grad + a.t.off_b;
+  const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
+  const int tc = tid & 15, tr = tid >> 4;  // 16 column groups x 8 row groups of 4
+
+  // ---- encode (rows 0..31 on threads 0..31) ------------------------------
+  const int r_own = tid;  // valid only for tid < kRB
+  int64_t row = 0;
+  bool valid = false;
+  int o = 0;
+  Bil64 bp{}, bd{};
+  Axis ad{};
+  if (tid < kRB) {
+    const int64_t k_row = (int64_t)blockIdx.x * kRB + tid;
+    const int64_t g = a.row0 + k_row * a.row_step;
+    valid = g < a.n_rows;
+    row = valid ? (a.idx ? a.idx[g] : g) : 0;
+    o = valid ? (int)a.obj[row] : 0;
+    float x[kMaxIn];
+#pragma unroll
+    for (int k = 0; k < kMaxIn; ++k) x[k] = 0.f;
+    if (valid) {
+      const double* c = a.coord + row * cw;
+      const size_t g2 = (size_t)f.R * f.R * f.N;
+      const float* gp = f.pos + (size_t)o * g2;
+      const float* gd = f.dir + (size_t)o * g2;
+      bp = bil64(c[0], c[1], f.R);
+      bd = bil64(c[2], c[3], f.R);
+      for (int k = 0; k < f.N; ++k) {
+        const double sp = bp.w[0] * (double)gp[(size_t)bp.c[0] * f.N + k] +
+                          bp.w[1] * (double)gp[(size_t)bp.c[1] * f.N + k] +
+                          bp.w[2] * (double)gp[(size_t)bp.c[2] * f.N + k] +
+                          bp.w[3] * (double)gp[(size_t)bp.c[3] * f.N + k];
+        const double sd = bd.w[0] * (double)gd[(size_t)bd.c[0] * f.N + k] +
+                          bd.w[1] * (double)gd[(size_t)bd.c[1] * f.N + k] +
+                          bd.w[2] * (double)gd[(size_t)bd.c[2] * f.N + k] +
+                          bd.w[3] * (double)gd[(size_t)bd.c[3] * f.N + k];
+        x[k] = (float)sp;
+        x[f.N + k] = (float)sd;
+      }
+      if (f.family == NIF_FAMILY_INNER) {
+        ad = axis_indices(c[4], f.Rd, false);
+        const float* gr = f.dist + (size_t)o * f.Rd * f.Nd;
+        for (int k = 0; k < f.Nd; ++k) {
+          const double s = (1.0 - ad.w) * (double)gr[(size_t)ad.i0 * f.Nd + k] +
+                           ad.w * (double)gr[(size_t)ad.i1 * f.Nd + k];
+          x[2 * f.N + k] = (float)s;
+        }
+      }
+    }
+    for (int k = 0; k < kMaxIn; ++k) xs[r_own * kMaxIn + k] = x[k];
+  }
+
+  // ---- forward: Z_l = bias + act(prev) . W_l^T (k ascending) ---------------
+  size_t wo = 0, bo = 0;
+  for (int l = 0; l < L; ++l) {
+    const int K = l == 0 ? IN : W;
+    __syncthreads();  // previous layer's outputs / x visible; sw free
+    for (int e = tid; e < K * W; e += kTT) {  // sw[k][j] = W_l[j][k]
+      const int j = e / K, k = e % K;
+      sw[k * W + j] = __ldg(Wt + wo + (size_t)j * K + k);
+    }
+    __syncthreads();
+    float acc[4][CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const float bj = __ldg(Bt + bo + tc + 16 * c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][c] = bj;
+    }
+    const float* prev = l == 0 ? xs : zs + (size_t)(l - 1) * kRB * WP;
+    const int ps = l == 0 ? kMaxIn : WP;
+    for (int k = 0; k < K; ++k) {
+      float av[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float v = prev[(tr * 4 + i) * ps + k];
+        av[i] = l == 0 ? v : leaky(v);
+      }
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const float wv = sw[k * W + tc + 16 * c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][c] = fmaf(wv, av[i], acc[i][c]);
+      }
+    }
+    float* z = zs + (size_t)l * kRB * WP;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) z[(tr * 4 + i) * WP + tc + 16 * c] = acc[i][c];
+    wo += (size_t)K * W;
+    bo += W;
+  }
+  __syncthreads();
+  // ---- head + loss: one (row, q) per thread --------------------------------
+  const size_t wo_h = wo, bo_h = bo;
+  const float* zl = zs + (size_t)(L - 1) * kRB * WP;
+  {
+    const int r = tid % kRB, q = tid / kRB;
+    if (q < OUT) {
+      const int64_t k_row = (int64_t)blockIdx.x * kRB + r;
+      const int64_t g = a.row0 + k_row * a.row_step;
+      const bool v = g < a.n_rows;
+      const int64_t rw = v ? (a.idx ? a.idx[g] : g) : 0;
+      const int ob = v ? (int)a.obj[rw] : 0;
+      float acc = __ldg(Bt + bo_h + q);
+      const float* wr = Wt + wo_h + (size_t)q * W;
+      for (int k = 0; k < W; ++k) acc = fmaf(__ldg(wr + k), leaky(zl[r * WP + k]), acc);
+      const int n_o = v ? a.t.counts[ob] : 1;
+      const float scale = (float)(2.0 / ((double)n_o * OUT));
+      const float lab = v ? a.label[rw * OUT + q] : 0.f;
+      float out, dz;
+      if (f.sigmoid_head) {
+        out = acc >= 0.f ? 1.f / (1.f + expf(-acc)) : expf(acc) / (1.f + expf(acc));
+        const float diff = out - lab;
+        if (v) atomicAdd(a.sq_err, (double)diff * (double)diff);
+        dz = diff * scale * out * (1.f - out);
+      } else {
+        out = acc;
+        const float diff = out - lab;
+        if (v) atomicAdd(a.sq_err, (double)diff * (double)diff);
+        dz = diff * scale;
+      }
+      dh[r * kMaxOut + q] = v ? dz : 0.f;
+    }
+  }
+  __syncthreads();
+  // dZ_{L-1}[r][k] = mask * sum_q dh[r][q] Wh[q][k]
+  for (int e = tid; e < kRB * W; e += kTT) {
+    const int r = e / W, k = e % W;
+    float da = 0.f;
+    for (int q = 0; q < OUT; ++q) da = fmaf(dh[r * kMaxOut + q], __ldg(Wt + wo_h + q * W + k), da);
+    dzA[r * WP + k] = zl[r * WP + k] > 0.f ? da : da * kSlope;
+  }
+  // head gradients
+  for (int e = tid; e < OUT * (W + 1); e += kTT) {
+    const int q = e / (W + 1), k = e % (W + 1);
+    float s = 0.f;
+    if (k < W) {
+      for (int r = 0; r < kRB; ++r) s = fmaf(dh[r * kMaxOut + q], leaky(zl[r * WP + k]), s);
+      atomicAdd(gW + wo_h + q * W + k, s);
+    } else {
+      for (int r = 0; r < kRB; ++r) s += dh[r * kMaxOut + q];
+      atomicAdd(gB + bo_h + q, s);
+    }
+  }
+  __syncthreads();
+  float* dzc = dzA;
+  float* dzn = dzB;
+  for (int l = L - 1; l >= 1; --l) {
+    wo -= (size_t)W * W;
+    bo -= W;
+    const float* zp = zs + (size_t)(l - 1) * kRB * WP;
+    // weight grads of dense layer l
+    for (int e = tid; e < W * (W + 1); e += kTT) {
+      const int j = e / (W + 1), k = e % (W + 1);
+      float s = 0.f;
+      if (k < W) {
+        for (int r = 0; r < kRB; ++r) s = fmaf(dzc[r * WP + j], leaky(zp[r * WP + k]), s);
+        atomicAdd(gW + wo + (size_t)j * W + k, s);
+      } else {
+        for (int r = 0; r < kRB; ++r) s += dzc[r * WP + j];
+        atomicAdd(gB + bo + j, s);
+      }
+    }
+    // stage W_l natural [j][k], then dZ_{l-1} = mask . (dZ_l W_l), j ascending
+    for (int e = tid; e < W * W; e += kTT) sw[e] = __ldg(Wt + wo + e);
+    __syncthreads();
+    float acc[4][CPT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) acc[i][c] = 0.f;
+    for (int j = 0; j < W; ++j) {
+      float dv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dv[i] = dzc[(tr * 4 + i) * WP + j];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const float wv = sw[j * W + tc + 16 * c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][c] = fmaf(dv[i], wv, acc[i][c]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int r = tr * 4 + i, k = tc + 16 * c;
+        dzn[r * WP + k] = zp[r * WP + k] > 0.f ? acc[i][c] : acc[i][c] * kSlope;
+      }
+    __syncthreads();
+    float* tmp = dzc;
+    dzc = dzn;
+    dzn = tmp;
+  }
+  // layer 0 weight grads
+  for (int e = tid; e < W * (IN + 1); e += kTT) {
+    const int j = e / (IN + 1), k = e % (IN + 1);
+    float s = 0.f;
+    if (k < IN) {
+      for (int r = 0; r < kRB; ++r) s = fmaf(dzc[r * WP + j], xs[r * kMaxIn + k], s);
+      atomicAdd(gW + (size_t)j * IN + k, s);
+    } else {
+      for (int r = 0; r < kRB; ++r) s += dzc[r * WP + j];
+      atomicAdd(gB + j, s);
+    }
+  }
+  if (tid >= kRB || !valid) return;
+  // dx = dZ_0 W_0 -> grid scatter (grids.py:171-202)
+  float dx[kMaxIn];
+  for (int k = 0; k < IN; ++k) {
+    float s = 0.f;
+    const float* dc = dzc + (size_t)r_own * WP;
+    for (int j = 0; j < W; ++j) s = fmaf(dc[j], __ldg(Wt + (size_t)j * IN + k), s);
+    dx[k] = s;
+  }
+  const size_t g2 = (size_t)f.R * f.R * f.N;
+  float* gpos = a.t.grad + a.t.off_pos + (size_t)o * g2;
+  float* gdir = a.t.grad + a.t.off_dir + (size_t)o * g2;
+  for (int c = 0; c < 4; ++c)
+    for (int k = 0; k < f.N; ++k) {
+      atomicAdd(gpos + (size_t)bp.c[c] * f.N + k, (float)(bp.w[c] * (double)dx[k]));
+      atomicAdd(gdir + (size_t)bd.c[c] * f.N + k, (float)(bd.w[c] * (double)dx[f.N + k]));
+    }
+  if (f.family == NIF_FAMILY_INNER) {
+    float* gr = a.t.grad + a.t.off_dist + (size_t)o * f.Rd * f.Nd;
+    for (int k = 0; k < f.Nd; ++k) {
+      atomicAdd(gr + (size_t)ad.i0 * f.Nd + k, (float)((1.0 - ad.w) * (double)dx[2 * f.N + k]));
+      atomicAdd(gr + (size_t)ad.i1 * f.Nd + k, (float)(ad.w * (double)dx[2 * f.N + k]));
+    }
+  }
+}
+
+int g_train_variant = 0;  // 0 tiled where it applies, 1 per-row kernel (nif_debug_set_train_variant)
+
+template <int W>
+int launch_fwdbwd_tiled(const TrainArgs& a, cudaStream_t st) {
+  const int L = a.f.n_layers - 1;
+  const int K = a.f.dims[0] > W ? a.f.dims[0] : W;
+  const size_t smem = ((size_t)L * kRB * (W + 1) + 2 * (size_t)kRB * (W + 1) +
+                       (size_t)kRB * kMaxIn + (size_t)kRB * kMaxOut + (size_t)K * W) *
+                      sizeof(float);
+  auto kern = train_fwdbwd_tiled_kernel<W>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
+  if (my_rows <= 0) return NIF_OK;
+  const unsigned grid = (unsigned)((my_rows + kRB - 1) / kRB);
+  kern<<<grid, kTT, smem, st>>>(a);
+  return check_launch("nif_train_fwdbwd_dev(tiled)");
 }
 
 template <int W>
@@ -431,6 +789,17 @@ extern "C" int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_vi
   if (row_step < 1 || row0 < 0) return fail(NIF_ERR_VALUE, "bad row partition");
   TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err};
   cudaStream_t st = (cudaStream_t)stream;
+  if (g_train_variant == 0 && f->n_heads == 1) {
+    switch (f->dims[1]) {
+      case 16: return launch_fwdbwd_tiled<16>(a, st);
+      case 32: return launch_fwdbwd_tiled<32>(a, st);
+      case 48: return launch_fwdbwd_tiled<48>(a, st);
+      case 64: return launch_fwdbwd_tiled<64>(a, st);
+      case 96: return launch_fwdbwd_tiled<96>(a, st);
+      case 128: return launch_fwdbwd_tiled<128>(a, st);
+      default: break;
+    }
+  }
   switch (f->dims[1]) {
     case 8: return launch_fwdbwd<8>(a, st);
     case 16: return launch_fwdbwd<16>(a, st);
@@ -441,6 +810,11 @@ extern "C" int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_vi
     case 128: return launch_fwdbwd<128>(a, st);
     default: return fail(NIF_ERR_UNSUPPORTED, "hidden width %d not instantiated", f->dims[1]);
   }
+}
+
+extern "C" int nif_debug_set_train_variant(int v) {
+  g_train_variant = v;
+  return NIF_OK;
 }
 
 extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, double lr,
@@ -459,13 +833,28 @@ extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, d
   s[ns++] = {t->off_w, f->w_stride, n_heads, 1};
   s[ns++] = {t->off_b, f->b_stride, n_heads, 1};
   while (ns < 5) s[ns++] = {0, 1, 0, 1};
-  int64_t total = 0;
-  for (int q = 0; q < 5; ++q) total += s[q].per * s[q].n_units;
-  int64_t blocks = (total + 255) / 256;
-  const int64_t cap = (int64_t)sm_count() * 8;
-  if (blocks > cap) blocks = cap;
-  adam_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(
-      *t, s[0], s[1], s[2], s[3], s[4], 5, shared, lr, beta1, beta2, eps);
+  if (g_train_variant == 1) {
+    int64_t total = 0;
+    for (int q = 0; q < 5; ++q) total += s[q].per * s[q].n_units;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    adam_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(
+        *t, s[0], s[1], s[2], s[3], s[4], 5, shared, lr, beta1, beta2, eps);
+  } else {
+    int64_t per_max = 0, units = 0;
+    for (int q = 0; q < 5; ++q) {
+      if (s[q].per > per_max) per_max = s[q].per;
+      if (s[q].n_units > units) units = s[q].n_units;
+    }
+    // ~4 float4 per thread per block: enough blocks to fill the GPU for the
+    // touched units without a per-element segment search
+    int64_t bx = (per_max / 4 + 1023) / 1024;
+    if (bx < 1) bx = 1;
+    dim3 grid((unsigned)bx, (unsigned)(units > 0 ? units : 1), 5);
+    adam_units_kernel<<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr, beta1,
+                                            beta2, eps);
+  }
   clear_counts_kernel<<<(f->n_obj + 127) / 128, 128, 0, st>>>(t->counts, f->n_obj);
   return check_launch("nif_adam_dev");
 }

@@ -167,28 +167,35 @@ class _Step:
         self.model = model
         self.fam = model.family(which)
         self.sq = torch.zeros(1, dtype=torch.float64, device=model.device)
+        # the flat parameter buffers never move: build the C views once
+        self.fv = self.fam.view()
+        self.tv = self.fam.train_view()
 
-    def run(self, obj, coord, label, idx, n_rows, rank=0, world=1, group=None, stream=None):
-        """One optimiser step over rows idx[0:n_rows] (device tensors);
-        leaves this batch's squared-error sum added into self.sq."""
+    def run(self, obj, coord, label, idx, n_rows, rank=0, world=1, group=None, stream=None,
+            idx_ptr=None):
+        """One optimiser step over rows idx[0:n_rows] (device tensors; or a raw
+        device pointer idx_ptr into an int64 row list); leaves this batch's
+        squared-error sum added into self.sq."""
         torch = _torch()
         L = _lib.lib()
         fam, model = self.fam, self.model
         sp = _lib.stream_ptr(stream)
-        fv = fam.view()
-        tv = fam.train_view()
+        fv, tv = self.fv, self.tv
         p = _lib.ptr
-        L.nif_batch_counts_dev(p(obj), p(idx), n_rows, fam.n_obj, p(fam.counts), sp)
+        if idx_ptr is not None:
+            idx = None
+        ip = idx_ptr if idx_ptr is not None else p(idx)
+        L.nif_batch_counts_dev(p(obj), ip, n_rows, fam.n_obj, p(fam.counts), sp)
         if world > 1:
             sq_local = torch.zeros(1, dtype=torch.float64, device=model.device)
-            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), p(idx), n_rows, rank,
+            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), ip, n_rows, rank,
                                    world, p(sq_local), sp)
             import torch.distributed as dist
             dist.all_reduce(fam.grad, group=group)
             dist.all_reduce(sq_local, group=group)
             self.sq += sq_local
         else:
-            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), p(idx), n_rows, 0, 1,
+            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), ip, n_rows, 0, 1,
                                    p(self.sq), sp)
         a = model.config.adam
         L.nif_adam_dev(fv, tv, model.learning_rate, a.beta1, a.beta2, a.epsilon, sp)
@@ -259,9 +266,10 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
             perm = torch.from_numpy(rng.permutation(n)).to(model.device)
             st = steps[which]
             st.sq.zero_()
+            base = perm.data_ptr()
             for k in range(0, n, bs):
                 m = min(bs, n - k)
-                st.run(obj, coord, label, perm[k:k + m], m, rank, world, group)
+                st.run(obj, coord, label, None, m, rank, world, group, idx_ptr=base + 8 * k)
             sums[fam] = float(st.sq.item())
             counts[fam] = n
         om = sums[0] / counts[0] if counts[0] else math.nan
