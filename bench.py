@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--train-epochs", type=int, default=0,
                    help="epochs of GPU training on 1 spp before timing (0 = random init)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-chunks", type=int, default=4,
+                   help="chunks of the e2e host path (H2D of chunk k+1 overlaps chunk k)")
     p.add_argument("--profile", action="store_true", help="few steps, no clocks / cpu leg")
     return p.parse_args()
 
@@ -353,11 +355,9 @@ def main():
     hocc = torch.empty(n, dtype=torch.uint8).pin_memory()
 
     def e2e_step():
-        eng.origins[:n].copy_(ho, non_blocking=True)
-        eng.dirs[:n].copy_(hd, non_blocking=True)
-        eng.tmaxs[:n].copy_(ht, non_blocking=True)
-        graph.replay()
-        hocc.copy_(eng.occ[:n], non_blocking=True)
+        # public host API: chunked, H2D of chunk k+1 overlapped with the pass
+        # over chunk k, D2H of each chunk's answer as soon as it is final
+        eng.occluded_host(ho, hd, ht, hocc, n, chunks=args.e2e_chunks)
 
     for _ in range(args.warmup):
         e2e_step()

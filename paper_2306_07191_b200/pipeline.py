@@ -250,6 +250,72 @@ class VisibilityEngine:
                         cnt + 8, b.cap, p(self.occ), None, self.impl, sp)
         main.wait_stream(self.side)
 
+    def run_range(self, s0: int, s1: int, stream=None):
+        """The pass over rays [s0, s1) of the resident buffers (ray ids and
+        the per-ray answer offset by s0); queues are reused, so ranges on
+        one stream run back to back."""
+        L = _lib.lib()
+        torch = _torch()
+        n = s1 - s0
+        if n <= 0:
+            return
+        b = self.buf
+        sp = _lib.stream_ptr(stream)
+        out = _lib.GatherOut.from_buffer_copy(b.out)
+        out.bvh_occ = b.bvh_occ.data_ptr() + s0
+        L.nif_gather_dev(self.ds.view, _lib.ptr(self.route), self.origins.data_ptr() + 24 * s0,
+                         self.dirs.data_ptr() + 24 * s0, self.tmaxs.data_ptr() + 8 * s0, n, out,
+                         _lib.ptr(b.workspace), b.workspace.numel(), sp)
+        if self.model is None:
+            return
+        vo, vi = self._family_views()
+        p = _lib.ptr
+        cnt = b.counts.data_ptr()
+        occ = self.occ.data_ptr() + s0
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self.side.wait_stream(main)
+        L.nif_query_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None, cnt,
+                        b.cap, occ, None, self.impl, self.side.cuda_stream)
+        L.nif_query_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord), p(b.inner_r),
+                        cnt + 8, b.cap, occ, None, self.impl, sp)
+        main.wait_stream(self.side)
+
+    def occluded_host(self, ho, hd, ht, hocc, n: int, chunks: int = 4):
+        """Host -> visibility -> host with the transfers overlapped: rays in
+        pinned host tensors ho/hd (n,3) f64 and ht (n,) f64, answer into the
+        pinned uint8 tensor hocc. Chunk k+1 is copied in on a copy stream
+        while chunk k is classified and queried; the answer of chunk k is
+        copied out as soon as it is final."""
+        torch = _torch()
+        if n > self.capacity:
+            raise ValueError(f"{n} rays exceed the engine capacity {self.capacity}")
+        self._family_views()
+        if not hasattr(self, "_h2d"):
+            self._h2d = torch.cuda.Stream(device=self.ds.device)
+            self._d2h = torch.cuda.Stream(device=self.ds.device)
+        main = torch.cuda.current_stream()
+        step = -(-n // max(1, chunks))
+        bounds = [(s, min(n, s + step)) for s in range(0, n, step)]
+        self._h2d.wait_stream(main)  # previous users of the ray buffers are done
+        evs = []
+        with torch.cuda.stream(self._h2d):
+            for s0, s1 in bounds:
+                self.origins[s0:s1].copy_(ho[s0:s1], non_blocking=True)
+                self.dirs[s0:s1].copy_(hd[s0:s1], non_blocking=True)
+                self.tmaxs[s0:s1].copy_(ht[s0:s1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._h2d)
+                evs.append(ev)
+        for (s0, s1), ev in zip(bounds, evs):
+            main.wait_event(ev)
+            self.run_range(s0, s1, main)
+            done = torch.cuda.Event()
+            done.record(main)
+            self._d2h.wait_event(done)
+            with torch.cuda.stream(self._d2h):
+                hocc[s0:s1].copy_(self.occ[s0:s1], non_blocking=True)
+        main.wait_stream(self._d2h)
+
     def capture(self, n: int):
         """CUDA-graph the pass for a fixed ray count (replayed by `replay`)."""
         torch = _torch()

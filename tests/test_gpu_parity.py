@@ -140,3 +140,30 @@ def test_engine_equals_record_path(name, impl, cuda, golden, scenes):
     fused = NifBackend(m, impl=impl).occluded(s, _rays(g))
     host = NifBackend(m, impl=impl, keep_records=True).occluded(s, _rays(g))
     np.testing.assert_array_equal(fused, host)
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_occluded_host_chunked_matches_device_pass(chunks, cuda):
+    """VisibilityEngine.occluded_host (chunked, transfers overlapped) gives
+    the same per-ray answer as the device-resident pass."""
+    import torch
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import VisibilityEngine, sample_pass_dev, shadow_rays_dev
+    from paper_2306_07191_b200.synthetic import c1
+    scene = c1(200, 160, subdiv=4, plane_nif=True)
+    data = sample_pass_dev(scene, scene.camera, 0, scene.seed)
+    _, o, d, t = shadow_rays_dev(data, require_emit=False)
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0), scene)
+    eng = VisibilityEngine(scene, model, n)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    eng.run(n)
+    ref = eng.occ[:n].cpu().numpy().copy()
+    ho, hd, ht = (x.cpu().pin_memory() for x in (o, d, t))
+    hocc = torch.zeros(n, dtype=torch.uint8).pin_memory()
+    eng.occluded_host(ho, hd, ht, hocc, n, chunks=chunks)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hocc.numpy(), ref)
