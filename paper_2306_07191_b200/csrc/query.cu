@@ -67,10 +67,18 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   l.off_headf = l.off_head + (size_t)16 * l.Kp * 2;  // fp32 head row + bias (CUDA-core head)
   l.w_bytes = l.off_headf + ((size_t)(l.W + 1) * 4 + 15) / 16 * 16;
   l.off_pos = al16(l.w_bytes);
-  const size_t tab = (size_t)f.n_obj * f.R * f.R * l.NP * 2;
+  // 2-D tables with 4 latents per cell (outer) are corner-packed: one
+  // 32 B entry per (u cell, v cell + 1) holding the four bilinear corners
+  // (u wrap and v clamp applied), so a lookup is one sector and two 16 B
+  // loads. With 8 latents per cell (inner) the packed entry would be 64 B
+  // for the same four 16 B loads and a 4x larger footprint (measured
+  // slower at R <= 128), so those stay one cell per 16 B. 1-D: corner pairs.
+  const size_t tab = l.NP == 4 ? (size_t)f.n_obj * f.R * (f.R + 1) * 4 * l.NP * 2
+                               : (size_t)f.n_obj * f.R * f.R * l.NP * 2;
   l.off_dir = al16(l.off_pos + tab);
   l.off_dist = al16(l.off_dir + tab);
-  const size_t dtab = f.family == NIF_FAMILY_INNER ? (size_t)f.n_obj * f.Rd * l.NPd * 2 : 0;
+  const size_t dtab =
+      f.family == NIF_FAMILY_INNER ? (size_t)f.n_obj * (f.Rd + 1) * 2 * l.NPd * 2 : 0;
   l.total = al16(l.off_dist + dtab);
   int cols = kTpc * ((l.W + 31) / 32 * 32);  // kTpc tiles x W accumulator columns
   l.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
@@ -134,21 +142,48 @@ __global__ void pack_weights_kernel(nif_family_view f, FastLayout l, uint8_t* bl
   *reinterpret_cast<__half*>(blob + off) = __float2half_rn(val);
 }
 
-// fp32 master latents -> fp16 tables padded to NP latents per cell
+// fp32 master latents -> corner-packed fp16 tables (one thread per corner
+// of an entry). 2-D entry (iu, jq), jq in [0, R]: corners (iu, jv0),
+// (iu, jv1), (iu+1 mod R, jv0), (iu+1 mod R, jv1) with jv0 = clamp(jq-1),
+// jv1 = clamp(jq) -- exactly the four cells grids.py:125-150 combines for
+// floor(v R - 0.5) = jq - 1. 1-D entry jq in [0, Rd]: (clamp(jq-1), clamp(jq)).
 __global__ void pack_tables_kernel(nif_family_view f, FastLayout l, uint8_t* blob) {
-  const int64_t cells2 = (int64_t)l.n_obj * l.R * l.R;
-  const int64_t cells1 = f.family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * l.Rd : 0;
+  const int R = l.R, Rd = l.Rd;
+  const bool quad = l.NP == 4;
+  const int64_t ent2 = quad ? (int64_t)l.n_obj * R * (R + 1) * 4 : (int64_t)l.n_obj * R * R;
+  const int64_t ent1 = f.family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * (Rd + 1) * 2 : 0;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < 2 * cells2) {
-    const bool is_dir = idx >= cells2;
-    const int64_t c = is_dir ? idx - cells2 : idx;
+  if (idx < 2 * ent2 && !quad) {
+    const bool is_dir = idx >= ent2;
+    const int64_t c = is_dir ? idx - ent2 : idx;
     const float* src = (is_dir ? f.dir : f.pos) + c * l.N;
     __half* dst = reinterpret_cast<__half*>(blob + (is_dir ? l.off_dir : l.off_pos)) + c * l.NP;
     for (int k = 0; k < l.NP; ++k) dst[k] = __float2half_rn(k < l.N ? src[k] : 0.f);
-  } else if (idx < 2 * cells2 + cells1) {
-    const int64_t c = idx - 2 * cells2;
-    const float* src = f.dist + c * l.Nd;
-    __half* dst = reinterpret_cast<__half*>(blob + l.off_dist) + c * l.NPd;
+  } else if (idx < 2 * ent2) {
+    const bool is_dir = idx >= ent2;
+    const int64_t e = is_dir ? idx - ent2 : idx;  // ((o * R + iu) * (R+1) + jq) * 4 + c
+    const int c = (int)(e & 3);
+    const int64_t q = e >> 2;
+    const int jq = (int)(q % (R + 1));
+    const int64_t oi = q / (R + 1);
+    const int iu = (int)(oi % R);
+    const int64_t o = oi / R;
+    const int u = (c >> 1) ? (iu + 1 == R ? 0 : iu + 1) : iu;
+    int jv = (c & 1) ? jq : jq - 1;
+    jv = jv < 0 ? 0 : (jv > R - 1 ? R - 1 : jv);
+    const float* src = (is_dir ? f.dir : f.pos) + (((size_t)o * R + u) * R + jv) * l.N;
+    __half* dst = reinterpret_cast<__half*>(blob + (is_dir ? l.off_dir : l.off_pos)) + e * l.NP;
+    for (int k = 0; k < l.NP; ++k) dst[k] = __float2half_rn(k < l.N ? src[k] : 0.f);
+  } else if (idx < 2 * ent2 + ent1) {
+    const int64_t e = idx - 2 * ent2;  // ((o * (Rd+1)) + jq) * 2 + c
+    const int c = (int)(e & 1);
+    const int64_t q = e >> 1;
+    const int jq = (int)(q % (Rd + 1));
+    const int64_t o = q / (Rd + 1);
+    int j = c ? jq : jq - 1;
+    j = j < 0 ? 0 : (j > Rd - 1 ? Rd - 1 : j);
+    const float* src = f.dist + ((size_t)o * Rd + j) * l.Nd;
+    __half* dst = reinterpret_cast<__half*>(blob + l.off_dist) + e * l.NPd;
     for (int k = 0; k < l.NPd; ++k) dst[k] = __float2half_rn(k < l.Nd ? src[k] : 0.f);
   }
 }
@@ -296,39 +331,6 @@ __device__ __forceinline__ void store_chunk(uint8_t* base, int row, int chunk, i
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
-template <int NP>
-__device__ __forceinline__ void corner(const __half* t, float w, float* acc) {
-  if constexpr (NP == 4) {
-    const uint2 q = __ldg(reinterpret_cast<const uint2*>(t));
-    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&q.x));
-    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&q.y));
-    acc[0] = fmaf(w, a.x, acc[0]);
-    acc[1] = fmaf(w, a.y, acc[1]);
-    acc[2] = fmaf(w, b.x, acc[2]);
-    acc[3] = fmaf(w, b.y, acc[3]);
-  } else {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(t));
-    const uint32_t u[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u[i]));
-      acc[2 * i] = fmaf(w, a.x, acc[2 * i]);
-      acc[2 * i + 1] = fmaf(w, a.y, acc[2 * i + 1]);
-    }
-  }
-}
-
-template <int NP>
-__device__ __forceinline__ void lookup16(const __half* tab, int R, float u, float v, float* acc) {
-  const Bil b = bilinear(u, v, R);
-#pragma unroll
-  for (int i = 0; i < NP; ++i) acc[i] = 0.f;
-  corner<NP>(tab + ((size_t)b.iu0 * R + b.iv0) * NP, b.w00, acc);
-  corner<NP>(tab + ((size_t)b.iu0 * R + b.iv1) * NP, b.w01, acc);
-  corner<NP>(tab + ((size_t)b.iu1 * R + b.iv0) * NP, b.w10, acc);
-  corner<NP>(tab + ((size_t)b.iu1 * R + b.iv1) * NP, b.w11, acc);
-}
-
 // Two-stage software pipeline of the per-record inputs: while tile k runs
 // its MMA chain, the latent-table corners of tile k+1 are in flight
 // (issued right after tile k's first MMA) and the record words of tile
@@ -341,26 +343,45 @@ struct RecIn {
   bool valid;
 };
 
-template <int NP>
-struct CornerT;
-template <>
-struct CornerT<4> {
-  using V = uint2;
-};
-template <>
-struct CornerT<8> {
-  using V = uint4;
-};
-
+// Raw corner data of one record, gathered a tile ahead: NP/2 16-byte loads
+// per 2-D lookup (outer NP=4: two corners per load; inner NP=8: one) and
+// one for the 1-D distance pair.
 template <int N, int ND>
 struct EncIn {
   static constexpr int NP = N <= 4 ? 4 : 8;
-  typename CornerT<NP>::V cp[4], cd[4];
-  uint2 cr[2];
+  static constexpr int NQ = NP / 2;  // 16 B loads per 2-D lookup (2 packed / 4 cells)
+  uint4 qp[NQ], qd[NQ], qr;
   float wp[4], wd[4], wr;
   int ray;
   bool valid;
 };
+
+// bilinear entry of the corner-packed table: (u cell) x (v cell + 1)
+struct BilQ {
+  int q;
+  float w00, w01, w10, w11;
+};
+
+__device__ __forceinline__ BilQ bilinear_q(float u, float v, int R) {
+  BilQ b;
+  u = u - floorf(u);
+  const float xu = u * (float)R - 0.5f;
+  const float fu = floorf(xu);
+  const float wu = xu - fu;
+  int i0 = (int)fu;
+  if (i0 < 0) i0 += R;
+  if (i0 > R - 1) i0 = R - 1;
+  const float xv = v * (float)R - 0.5f;
+  const float fv = floorf(xv);
+  const float wv = xv - fv;
+  const int jq = (int)fminf(fmaxf(fv + 1.0f, 0.0f), (float)R);
+  b.q = i0 * (R + 1) + jq;
+  b.w00 = (1.f - wu) * (1.f - wv);
+  b.w01 = (1.f - wu) * wv;
+  b.w10 = wu * (1.f - wv);
+  b.w11 = wu * wv;
+  return b;
+}
 
 __device__ __forceinline__ RecIn load_rec(const TcArgs& a, int64_t tile, int tid, int64_t n,
                                           bool inner) {
@@ -383,32 +404,45 @@ __device__ __forceinline__ RecIn load_rec(const TcArgs& a, int64_t tile, int tid
 template <int N, int ND>
 __device__ __forceinline__ void issue_enc(EncIn<N, ND>& e, const RecIn& r, const __half* tpos,
                                           const __half* tdir, const __half* tdist, int R, int Rd) {
-  constexpr int NP = EncIn<N, ND>::NP;
-  using V = typename CornerT<NP>::V;
+  constexpr int NP = EncIn<N, ND>::NP, NQ = EncIn<N, ND>::NQ;
   e.valid = r.valid;
   e.ray = r.ray;
   if (!r.valid) return;
-  const size_t g2 = (size_t)R * R * NP;
-  const Bil bp = bilinear(r.c.x, r.c.y, R), bd = bilinear(r.c.z, r.c.w, R);
-  const V* P = reinterpret_cast<const V*>(tpos + (size_t)r.obj * g2);
-  const V* D = reinterpret_cast<const V*>(tdir + (size_t)r.obj * g2);
-  e.cp[0] = __ldg(P + (size_t)bp.iu0 * R + bp.iv0);
-  e.cp[1] = __ldg(P + (size_t)bp.iu0 * R + bp.iv1);
-  e.cp[2] = __ldg(P + (size_t)bp.iu1 * R + bp.iv0);
-  e.cp[3] = __ldg(P + (size_t)bp.iu1 * R + bp.iv1);
-  e.cd[0] = __ldg(D + (size_t)bd.iu0 * R + bd.iv0);
-  e.cd[1] = __ldg(D + (size_t)bd.iu0 * R + bd.iv1);
-  e.cd[2] = __ldg(D + (size_t)bd.iu1 * R + bd.iv0);
-  e.cd[3] = __ldg(D + (size_t)bd.iu1 * R + bd.iv1);
-  e.wp[0] = bp.w00; e.wp[1] = bp.w01; e.wp[2] = bp.w10; e.wp[3] = bp.w11;
-  e.wd[0] = bd.w00; e.wd[1] = bd.w01; e.wd[2] = bd.w10; e.wd[3] = bd.w11;
-  if constexpr (ND > 0) {
-    const Lin li = linear1(r.r, Rd);
-    const uint2* G = reinterpret_cast<const uint2*>(tdist + (size_t)r.obj * Rd * 4);
-    e.cr[0] = __ldg(G + li.i0);
-    e.cr[1] = __ldg(G + li.i1);
-    e.wr = li.w;
+  if constexpr (NP == 4) {  // corner-packed entries
+    const size_t g2 = (size_t)R * (R + 1) * NQ;  // uint4 per object table
+    const BilQ bp = bilinear_q(r.c.x, r.c.y, R), bd = bilinear_q(r.c.z, r.c.w, R);
+    const uint4* P = reinterpret_cast<const uint4*>(tpos) + (size_t)r.obj * g2 + (size_t)bp.q * NQ;
+    const uint4* D = reinterpret_cast<const uint4*>(tdir) + (size_t)r.obj * g2 + (size_t)bd.q * NQ;
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) e.qp[i] = __ldg(P + i);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) e.qd[i] = __ldg(D + i);
+    e.wp[0] = bp.w00; e.wp[1] = bp.w01; e.wp[2] = bp.w10; e.wp[3] = bp.w11;
+    e.wd[0] = bd.w00; e.wd[1] = bd.w01; e.wd[2] = bd.w10; e.wd[3] = bd.w11;
+  } else {  // one 16 B cell per corner
+    const size_t g2 = (size_t)R * R;
+    const Bil bp = bilinear(r.c.x, r.c.y, R), bd = bilinear(r.c.z, r.c.w, R);
+    const uint4* P = reinterpret_cast<const uint4*>(tpos) + (size_t)r.obj * g2;
+    const uint4* D = reinterpret_cast<const uint4*>(tdir) + (size_t)r.obj * g2;
+    e.qp[0] = __ldg(P + (size_t)bp.iu0 * R + bp.iv0);
+    e.qp[1] = __ldg(P + (size_t)bp.iu0 * R + bp.iv1);
+    e.qp[2] = __ldg(P + (size_t)bp.iu1 * R + bp.iv0);
+    e.qp[3] = __ldg(P + (size_t)bp.iu1 * R + bp.iv1);
+    e.qd[0] = __ldg(D + (size_t)bd.iu0 * R + bd.iv0);
+    e.qd[1] = __ldg(D + (size_t)bd.iu0 * R + bd.iv1);
+    e.qd[2] = __ldg(D + (size_t)bd.iu1 * R + bd.iv0);
+    e.qd[3] = __ldg(D + (size_t)bd.iu1 * R + bd.iv1);
+    e.wp[0] = bp.w00; e.wp[1] = bp.w01; e.wp[2] = bp.w10; e.wp[3] = bp.w11;
+    e.wd[0] = bd.w00; e.wd[1] = bd.w01; e.wd[2] = bd.w10; e.wd[3] = bd.w11;
   }
+  if constexpr (ND > 0) {
+    const float xc = r.r * (float)Rd - 0.5f;
+    const float f0 = floorf(xc);
+    const int jq = (int)fminf(fmaxf(f0 + 1.0f, 0.0f), (float)Rd);
+    e.qr = __ldg(reinterpret_cast<const uint4*>(tdist) + (size_t)r.obj * (Rd + 1) + jq);
+    e.wr = xc - f0;
+  }
+  (void)NP;
 }
 
 __device__ __forceinline__ void acc_h2(uint32_t u, float w, float& a0, float& a1) {
@@ -417,33 +451,40 @@ __device__ __forceinline__ void acc_h2(uint32_t u, float w, float& a0, float& a1
   a1 = fmaf(w, f.y, a1);
 }
 
-template <int NP>
-__device__ __forceinline__ void acc_corner(const typename CornerT<NP>::V& q, float w, float* acc) {
+// corner c of a packed entry: NP=4 -> words (2c, 2c+1) of the entry's 8,
+// NP=8 -> the four words of uint4 c
+template <int NP, int NQ>
+__device__ __forceinline__ void acc_entry(const uint4 (&q)[NQ], const float (&w)[4], float* acc) {
   if constexpr (NP == 4) {
-    acc_h2(q.x, w, acc[0], acc[1]);
-    acc_h2(q.y, w, acc[2], acc[3]);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      acc_h2(q[i].x, w[2 * i], acc[0], acc[1]);
+      acc_h2(q[i].y, w[2 * i], acc[2], acc[3]);
+      acc_h2(q[i].z, w[2 * i + 1], acc[0], acc[1]);
+      acc_h2(q[i].w, w[2 * i + 1], acc[2], acc[3]);
+    }
   } else {
-    acc_h2(q.x, w, acc[0], acc[1]);
-    acc_h2(q.y, w, acc[2], acc[3]);
-    acc_h2(q.z, w, acc[4], acc[5]);
-    acc_h2(q.w, w, acc[6], acc[7]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc_h2(q[c].x, w[c], acc[0], acc[1]);
+      acc_h2(q[c].y, w[c], acc[2], acc[3]);
+      acc_h2(q[c].z, w[c], acc[4], acc[5]);
+      acc_h2(q[c].w, w[c], acc[6], acc[7]);
+    }
   }
 }
 
 template <int N, int ND>
 __device__ __forceinline__ void finish_enc(const EncIn<N, ND>& e, float (&x)[16]) {
-  constexpr int NP = EncIn<N, ND>::NP;
+  constexpr int NP = EncIn<N, ND>::NP, NQ = EncIn<N, ND>::NQ;
 #pragma unroll
   for (int i = 0; i < 16; ++i) x[i] = 0.f;
   if (e.valid) {
     float ap[NP], ad[NP];
 #pragma unroll
     for (int i = 0; i < NP; ++i) ap[i] = ad[i] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      acc_corner<NP>(e.cp[c], e.wp[c], ap);
-      acc_corner<NP>(e.cd[c], e.wd[c], ad);
-    }
+    acc_entry<NP, NQ>(e.qp, e.wp, ap);
+    acc_entry<NP, NQ>(e.qd, e.wd, ad);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       x[i] = ap[i];
@@ -451,8 +492,11 @@ __device__ __forceinline__ void finish_enc(const EncIn<N, ND>& e, float (&x)[16]
     }
     if constexpr (ND > 0) {
       float ar[4] = {0.f, 0.f, 0.f, 0.f};
-      acc_corner<4>(e.cr[0], 1.f - e.wr, ar);
-      acc_corner<4>(e.cr[1], e.wr, ar);
+      const float w0 = 1.f - e.wr, w1 = e.wr;
+      acc_h2(e.qr.x, w0, ar[0], ar[1]);
+      acc_h2(e.qr.y, w0, ar[2], ar[3]);
+      acc_h2(e.qr.z, w1, ar[0], ar[1]);
+      acc_h2(e.qr.w, w1, ar[2], ar[3]);
 #pragma unroll
       for (int i = 0; i < ND; ++i) x[2 * N + i] = ar[i];
     }
@@ -1627,8 +1671,9 @@ extern "C" int nif_fast_pack_dev(const nif_family_view* f, void* blob, void* str
     const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp + l.W + 1;
     pack_weights_kernel<<<(nw + 255) / 256, 256, 0, st>>>(*f, l, (uint8_t*)blob);
   }
-  const int64_t cells = 2 * (int64_t)l.n_obj * l.R * l.R +
-                        (f->family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * l.Rd : 0);
+  const int64_t cells = 2 * (l.NP == 4 ? (int64_t)l.n_obj * l.R * (l.R + 1) * 4
+                                      : (int64_t)l.n_obj * l.R * l.R) +
+                        (f->family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * (l.Rd + 1) * 2 : 0);
   pack_tables_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, st>>>(*f, l, (uint8_t*)blob);
   return check_launch("nif_fast_pack_dev");
 }
