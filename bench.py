@@ -345,6 +345,24 @@ def main():
     timed("bvh_anyhit", lambda: L.nif_bvh_occluded_dev(
         eng.ds.view, o.data_ptr(), d.data_ptr(), t.data_ptr(), n, bvh_out.data_ptr(), sp))
 
+    # --- full frame of the renderer (sample pass -> cast -> visibility ->
+    # shading), everything resident, NIF vs BVH visibility (informational)
+    from paper_2306_07191_b200 import BvhBackend
+    from paper_2306_07191_b200.pipeline import render_dev
+    nif_be = NifBackend(model)
+    render_ms = {}
+    for name, be in (("nif", nif_be), ("bvh", BvhBackend())):
+        render_dev(scene, be, spp=1, sample_offset=rank)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            render_dev(scene, be, spp=1, sample_offset=rank)
+        e1.record(stream)
+        e1.synchronize()
+        render_ms[name] = e0.elapsed_time(e1) / 3
+    del nif_be
+
     # --- e2e through the public API with pinned host buffers ----------------
     ho = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     hd = torch.empty((n, 3), dtype=torch.float64).pin_memory()
@@ -453,6 +471,7 @@ def main():
                    "parallelism": f"{ws} independent frames (sample index = rank)"},
         "frame_ms": ms / args.steps,
         "bvh_ms_per_frame": kt["bvh_anyhit"],
+        "render_ms_per_frame_1spp": render_ms,
         "kernel_ms": kt,
         "roofline": roof,
         "rooflines": rooflines,

@@ -304,6 +304,13 @@ int nif_sample_pass_dev(const nif_scene_view* scene, const nif_camera* cam,
                         int32_t sampler, int64_t pix0, int64_t n_pix,
                         const nif_pass_out* out, void* stream);
 
+/* One progressive sample's shading (renderer.py:826-849): for the n_cast
+ * shadow-cast pixels idx[k] with visibility occ[k] (1 = shadowed), adds
+ * albedo[obj] / pi * emit * (vis * cos / pdf) to the fp64 HDR buffer
+ * buf[n_pix][3], in the reference's evaluation order.                  */
+int nif_shade_accumulate_dev(const nif_pass_out* pass, const double* albedo, const int64_t* idx,
+                             const uint8_t* occ, int64_t n_cast, double* buf, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

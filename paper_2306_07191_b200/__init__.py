@@ -18,8 +18,8 @@ from .nif import (
 )
 from .pipeline import (
     BvhBackend, HdrImage, NifBackend, OracleBackend, PredictorBackend, RenderConfig,
-    VisibilityEngine, gather_queries, label_visible, oracle_predictor, psnr, render,
-    sample_pass, sample_pass_dev, shade_pass_nif, tonemap_srgb8,
+    VisibilityEngine, gather_queries, label_visible, oracle_predictor, psnr, psnr_dev, render,
+    render_dev, sample_pass, sample_pass_dev, shade_pass_nif, tonemap_srgb8,
 )
 from .scene import (
     Aabb, AreaLight, BottomLevelBvh, Camera, InnerQuery, OuterQuery, PointLight, QueryRecords,

@@ -158,6 +158,7 @@ _SIGS = {
     "nif_sample_pass_dev": (C.c_int, [C.POINTER(SceneView), C.POINTER(Camera),
                                       C.POINTER(LightsView), I64, I64, I32, I64, I64,
                                       C.POINTER(PassOut), P]),
+    "nif_shade_accumulate_dev": (C.c_int, [C.POINTER(PassOut), P, P, P, I64, P, P]),
 }
 
 

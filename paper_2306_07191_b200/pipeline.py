@@ -13,6 +13,7 @@ ray count can be captured once in a CUDA graph and replayed.
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -143,10 +144,18 @@ class BvhBackend:
         if n == 0:
             return np.zeros(0, bool)
         o, d, t = rays_to_device(rays, ds.device)
-        out = torch.empty(n, dtype=torch.uint8, device=ds.device)
-        _lib.lib().nif_bvh_occluded_dev(ds.view, _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
-                                        _lib.ptr(out), _lib.stream_ptr())
-        return out.cpu().numpy().astype(bool)
+        return self.occluded_dev(scene, o, d, t).cpu().numpy().astype(bool)
+
+    def occluded_dev(self, scene: Scene, o, d, t):
+        """Device rays in, device uint8 answer out (no host round trip)."""
+        torch = _torch()
+        ds = scene.device()
+        n = int(t.numel())
+        out = torch.empty(max(n, 1), dtype=torch.uint8, device=ds.device)
+        if n:
+            _lib.lib().nif_bvh_occluded_dev(ds.view, _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
+                                            _lib.ptr(out), _lib.stream_ptr())
+        return out[:n]
 
 
 class PredictorBackend:
@@ -375,6 +384,19 @@ class NifBackend(PredictorBackend):
         eng.run(n)
         return eng.occ[:n].cpu().numpy().astype(bool)
 
+    def occluded_dev(self, scene: Scene, o, d, t):
+        """Device rays in, device uint8 answer out (valid until the next
+        call on this scene); the engine's buffers are filled device to
+        device."""
+        n = int(t.numel())
+        eng = self.engine(scene, max(n, 1))
+        if n:
+            eng.origins[:n].copy_(o)
+            eng.dirs[:n].copy_(d)
+            eng.tmaxs[:n].copy_(t)
+            eng.run(n)
+        return eng.occ[:n]
+
 
 def shade_pass_nif(scene: Scene, rays: ShadowRays, predictor, hybrid_threshold=None,
                    threads: int = 1) -> np.ndarray:
@@ -455,7 +477,8 @@ def sample_pass(scene: Scene, camera, sample: int, seed: int, threads: int = 1,
 def shadow_rays_dev(data, require_emit=True):
     """Cast filter of renderer.py:831-832 (cli.py:170-183 drops the emit
     test): returns (mask, origins, dirs, tmaxs) as device tensors."""
-    cos = (data["normal"] * data["ldir"]).sum(dim=1)
+    nl = data["normal"] * data["ldir"]
+    cos = (nl[:, 0] + nl[:, 2]) + nl[:, 1]  # np.einsum's pairing (renderer.py:829)
     cast = (data["hit"] != 0) & (cos > 0.0) & (data["pdf"] > 0.0)
     if require_emit:
         cast &= data["emit"].amax(dim=1) > 0.0
@@ -503,22 +526,66 @@ def render(scene: Scene, camera=None, config: RenderConfig = None, backend=None)
     dev = scene.device().device
     buf = torch.zeros((w * h, 3), dtype=torch.float64, device=dev)
     albedo = scene.device().albedo
-    inv_pi = 1.0 / math.pi
+    on_device = hasattr(backend, "occluded_dev")
+    L = _lib.lib()
+    t0 = time.perf_counter()
     for s in range(config.sample_offset, config.sample_offset + config.spp):
         data = sample_pass_dev(scene, camera, s, seed)
-        cos = (data["normal"] * data["ldir"]).sum(dim=1)
         cast, o, d, t = shadow_rays_dev(data)
-        if int(cast.sum()) == 0:
+        idx = cast.nonzero().squeeze(1)
+        n_cast = int(idx.numel())
+        if n_cast == 0:
             continue
-        rays = ShadowRays(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
-        occ = backend.occluded(scene, rays, 1)
-        vis = torch.zeros(w * h, dtype=torch.float64, device=dev)
-        vis[cast] = torch.from_numpy(~occ).to(dev).double()
-        obj = data["obj"].long().clamp(min=0)
-        scale = torch.where(cast, vis * cos / torch.where(cast, data["pdf"], 1.0), 0.0)
-        contrib = albedo[obj] * inv_pi * data["emit"] * scale[:, None]
-        buf += torch.where(cast[:, None], contrib, 0.0)
-    return HdrImage(buf.view(h, w, 3).cpu().numpy(), config.spp)
+        if on_device:  # sample pass -> visibility -> shading, all in HBM
+            occ = backend.occluded_dev(scene, o, d, t)
+        else:  # generic predictor backends answer on the host
+            rays = ShadowRays(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+            occ = torch.from_numpy(backend.occluded(scene, rays, 1).astype(np.uint8)).to(dev)
+        po = _lib.PassOut(**{k: _lib.ptr(v) for k, v in data.items()})
+        L.nif_shade_accumulate_dev(po, _lib.ptr(albedo), _lib.ptr(idx), _lib.ptr(occ), n_cast,
+                                   _lib.ptr(buf), _lib.stream_ptr())
+    img = HdrImage(buf.view(h, w, 3).cpu().numpy(), config.spp)
+    img.timings = {"total": time.perf_counter() - t0}
+    return img
+
+
+def render_dev(scene: Scene, backend, spp: int = 1, camera=None, seed=None, sample_offset=0):
+    """The renderer's per-sample loop with everything resident: returns the
+    fp64 HDR sum buffer as a device tensor (h, w, 3) -- for ms/frame
+    measurement and device-side PSNR (psnr_dev)."""
+    torch = _torch()
+    camera = camera or scene.camera
+    seed = scene.seed if seed is None else seed
+    dev = scene.device().device
+    w, h = camera.width, camera.height
+    buf = torch.zeros((w * h, 3), dtype=torch.float64, device=dev)
+    albedo = scene.device().albedo
+    L = _lib.lib()
+    for s in range(sample_offset, sample_offset + spp):
+        data = sample_pass_dev(scene, camera, s, seed)
+        cast, o, d, t = shadow_rays_dev(data)
+        idx = cast.nonzero().squeeze(1)
+        n_cast = int(idx.numel())
+        if n_cast == 0:
+            continue
+        occ = backend.occluded_dev(scene, o, d, t)
+        po = _lib.PassOut(**{k: _lib.ptr(v) for k, v in data.items()})
+        L.nif_shade_accumulate_dev(po, _lib.ptr(albedo), _lib.ptr(idx), _lib.ptr(occ), n_cast,
+                                   _lib.ptr(buf), _lib.stream_ptr())
+    return buf.view(h, w, 3)
+
+
+def psnr_dev(a_sum, b_sum, count_a: int, count_b: int) -> float:
+    """renderer.py:881-891 on device HDR sums: tonemap to 8 bits, MSE, dB."""
+    torch = _torch()
+
+    def tm(x):
+        return torch.round(torch.clamp(x, 0.0, 1.0).pow(GAMMA) * 255.0)
+    ta, tb = tm(a_sum / max(count_a, 1)), tm(b_sum / max(count_b, 1))
+    mse = float(((ta - tb) ** 2).mean())
+    if mse == 0.0:
+        return PSNR_SENTINEL
+    return 10.0 * math.log10(255.0 ** 2 / mse)
 
 
 def tonemap_srgb8(linear) -> np.ndarray:

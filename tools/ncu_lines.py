@@ -1,6 +1,6 @@
 """Per-CUDA-source-line instruction / stall totals from an ncu report.
 
-    python tools/ncu_lines.py report.ncu-rep [top]
+    python tools/ncu_lines.py report.ncu-rep [top] [function-substring]
 """
 import csv
 import io
@@ -9,15 +9,22 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+want = sys.argv[3] if len(sys.argv) > 3 else ""
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 agg = []
 fname = ""
 hdr = None
+func_ok = True
 for r in rows:
     if len(r) == 2 and r[0] == "File Path":
         fname = r[1].split("/")[-1]
+        continue
+    if len(r) == 2 and r[0] == "Function Name":
+        func_ok = want in r[1]
+        continue
+    if not func_ok:
         continue
     if r and r[0] == "Line No":
         hdr = r
