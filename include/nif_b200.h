@@ -304,6 +304,14 @@ int nif_sample_pass_dev(const nif_scene_view* scene, const nif_camera* cam,
                         int32_t sampler, int64_t pix0, int64_t n_pix,
                         const nif_pass_out* out, void* stream);
 
+/* Geometry-head labels (bvh.py:920-950 _k_label_geometry): per record,
+ * closest hit in the record's own object; labels[m][4] = (unit normal,
+ * t / diagonal) as f32, hit[m] = 1 when something was hit (keep).      */
+int nif_label_geometry_dev(const nif_scene_view* s, const int32_t* rec_obj,
+                           const int32_t* rec_ray, int64_t m, const double* origins,
+                           const double* dirs, double diagonal, float* labels, uint8_t* hit,
+                           void* stream);
+
 /* One progressive sample's shading (renderer.py:826-849): for the n_cast
  * shadow-cast pixels idx[k] with visibility occ[k] (1 = shadowed), adds
  * albedo[obj] / pi * emit * (vis * cos / pdf) to the fp64 HDR buffer

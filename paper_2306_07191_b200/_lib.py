@@ -159,6 +159,7 @@ _SIGS = {
                                       C.POINTER(LightsView), I64, I64, I32, I64, I64,
                                       C.POINTER(PassOut), P]),
     "nif_shade_accumulate_dev": (C.c_int, [C.POINTER(PassOut), P, P, P, I64, P, P]),
+    "nif_label_geometry_dev": (C.c_int, [C.POINTER(SceneView), P, P, I64, P, P, D, P, P, P]),
 }
 
 

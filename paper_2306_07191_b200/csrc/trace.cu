@@ -531,3 +531,54 @@ extern "C" int nif_shade_accumulate_dev(const nif_pass_out* pass, const double* 
       *pass, albedo, idx, occ, n_cast, buf);
   return check_launch("nif_shade_accumulate_dev");
 }
+
+// ---------------------------------------------------------------------------
+// Geometry-head labels (bvh.py:920-950 _k_label_geometry, nif.py:547-566):
+// closest hit of each record's ray against that record's object alone,
+// t in (eps, inf); label = (interpolated unit normal, t / diagonal) as fp32,
+// hit flag = keep.
+// ---------------------------------------------------------------------------
+__global__ void label_geometry_kernel(nif_scene_view s, const int32_t* __restrict__ rec_obj,
+                                      const int32_t* __restrict__ rec_ray, int64_t m,
+                                      const double* __restrict__ o, const double* __restrict__ d,
+                                      double diagonal, float* __restrict__ labels,
+                                      uint8_t* __restrict__ hit) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int64_t i = rec_ray[j];
+  double t = CUDART_INF, bu, bv;
+  const int slot = closest_in_object(s.nodes, s.tris, s.roots[rec_obj[j]], o[i * 3], o[i * 3 + 1],
+                                     o[i * 3 + 2], d[i * 3], d[i * 3 + 1], d[i * 3 + 2], s.eps, &t,
+                                     &bu, &bv);
+  if (slot < 0) {
+    hit[j] = 0;
+    for (int c = 0; c < 4; ++c) labels[j * 4 + c] = 0.f;
+    return;
+  }
+  hit[j] = 1;
+  const double b0 = 1.0 - bu - bv;
+  const double* n9 = s.normals + (size_t)slot * 9;
+  double nx = b0 * n9[0] + bu * n9[3] + bv * n9[6];
+  double ny = b0 * n9[1] + bu * n9[4] + bv * n9[7];
+  double nz = b0 * n9[2] + bu * n9[5] + bv * n9[8];
+  const double nn = sqrt(nx * nx + ny * ny + nz * nz);
+  if (nn > 0.0) {
+    nx /= nn;
+    ny /= nn;
+    nz /= nn;
+  }
+  labels[j * 4 + 0] = (float)nx;
+  labels[j * 4 + 1] = (float)ny;
+  labels[j * 4 + 2] = (float)nz;
+  labels[j * 4 + 3] = (float)(t / diagonal);
+}
+
+extern "C" int nif_label_geometry_dev(const nif_scene_view* s, const int32_t* rec_obj,
+                                      const int32_t* rec_ray, int64_t m, const double* origins,
+                                      const double* dirs, double diagonal, float* labels,
+                                      uint8_t* hit, void* stream) {
+  if (m <= 0) return NIF_OK;
+  label_geometry_kernel<<<grid_for(m, 128), 128, 0, (cudaStream_t)stream>>>(
+      *s, rec_obj, rec_ray, m, origins, dirs, diagonal, labels, hit);
+  return check_launch("nif_label_geometry_dev");
+}

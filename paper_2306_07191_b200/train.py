@@ -81,7 +81,10 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
                     threads: Optional[int] = None) -> SampleSet:
     """nif.py:569-674 on the device: per sample index, the primary pass,
     every hit pixel's shadow ray (no cosine filter), the gather in the
-    reference's record order and per-object BVH labels (1 = visible)."""
+    reference's record order and per-object BVH labels (1 = visible).
+    labeler="geometry" follows the primary rays instead (uniform sampler,
+    camera origin, infinite t_max) and labels each record with the closest
+    hit in its own object (unit normal, t / diagonal), keeping hit rows."""
     torch = _torch()
     from .pipeline import GatherBuffers, gather_dev, sample_pass_dev
     camera = camera or scene.camera
@@ -89,9 +92,10 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
         raise ValueError("no camera given and the scene has none")
     if sampler not in ("importance", "uniform"):
         raise ValueError(f"unknown sampler {sampler!r}")
-    if labeler not in (None,):
-        raise NotImplementedError("custom labelers / the geometry head are not on the device path")
-    if not scene.lights:
+    if labeler not in (None, "geometry"):
+        raise NotImplementedError("custom labeler callables are not on the device path")
+    head = "geometry" if labeler == "geometry" else "occlusion"
+    if head == "occlusion" and not scene.lights:
         raise ValueError("sample collection needs at least one light")
     seed = scene.seed if seed is None else seed
     ds = scene.device()
@@ -101,16 +105,25 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
     acc = {k: [] for k in ("oo", "oc", "ol", "or_", "io", "ic", "il", "ir")}
     n_rays = shadow_rays = degenerate = 0
     L = _lib.lib()
+    cam_pos = torch.from_numpy(np.ascontiguousarray(
+        np.broadcast_to(np.asarray(camera.position, np.float64), (n_pix, 3)))).to(dev)
+    inf_tmax = torch.full((n_pix,), math.inf, dtype=torch.float64, device=dev)
     for s in range(spp):
-        data = sample_pass_dev(scene, camera, s, seed, sampler)
-        mask = data["hit"] != 0
-        idx = mask.nonzero().squeeze(1)
-        n = int(idx.numel())
-        if n == 0:
-            continue
-        o = data["point"][idx].contiguous()
-        d = data["ldir"][idx].contiguous()
-        t = data["tmax"][idx].contiguous()
+        data = sample_pass_dev(scene, camera, s, seed,
+                               "uniform" if head == "geometry" else sampler)
+        if head == "geometry":
+            idx = torch.arange(n_pix, device=dev)
+            n = n_pix
+            o, d, t = cam_pos, data["pdir"].contiguous(), inf_tmax
+        else:
+            mask = data["hit"] != 0
+            idx = mask.nonzero().squeeze(1)
+            n = int(idx.numel())
+            if n == 0:
+                continue
+            o = data["point"][idx].contiguous()
+            d = data["ldir"][idx].contiguous()
+            t = data["tmax"][idx].contiguous()
         buf = GatherBuffers(n, int(route.sum()), dev, interleaved=True)
         gather_dev(ds, ds.route(route), o, d, t, n, buf)
         counts = buf.counts.cpu().numpy()
@@ -121,20 +134,33 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
             continue
         rec_obj = buf.rec_obj[:m]
         rec_ray = buf.rec_ray[:m]
-        vis = torch.empty(m, dtype=torch.uint8, device=dev)
-        L.nif_label_visible_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m, _lib.ptr(o),
-                                _lib.ptr(d), _lib.ptr(t), _lib.ptr(vis), _lib.stream_ptr())
+        if head == "geometry":
+            lab = torch.empty((m, 4), dtype=torch.float32, device=dev)
+            keep = torch.empty(m, dtype=torch.uint8, device=dev)
+            L.nif_label_geometry_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m,
+                                     _lib.ptr(o), _lib.ptr(d), float(scene.diagonal),
+                                     _lib.ptr(lab), _lib.ptr(keep), _lib.stream_ptr())
+            keep = keep != 0
+        else:
+            vis = torch.empty(m, dtype=torch.uint8, device=dev)
+            L.nif_label_visible_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m,
+                                    _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), _lib.ptr(vis),
+                                    _lib.stream_ptr())
+            lab, keep = vis.float(), None
         kind = buf.rec_kind[:m]
         coord = buf.rec_coord[:m * 5].view(m, 5)
         ray_ids = s * n_pix + idx
         for k, (ko, kc, kl, kr), width in ((0, ("oo", "oc", "ol", "or_"), 4),
                                            (1, ("io", "ic", "il", "ir"), 5)):
-            sel = (kind == k).nonzero().squeeze(1)
+            selm = kind == k
+            if keep is not None:
+                selm &= keep
+            sel = selm.nonzero().squeeze(1)
             if sel.numel() == 0:
                 continue
             acc[ko].append(rec_obj[sel].long())
             acc[kc].append(coord[sel, :width].contiguous())
-            acc[kl].append(vis[sel].float())
+            acc[kl].append(lab[sel])
             acc[kr].append(ray_ids[rec_ray[sel].long()])
         n_rays += n
 
@@ -143,10 +169,11 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
             return torch.cat(acc[key]).contiguous()
         return torch.zeros((0,) + tail, dtype=dt, device=dev)
 
-    out = SampleSet("occlusion", cat("oo", (), torch.int64), cat("oc", (4,), torch.float64),
-                    cat("ol", (), torch.float32), cat("or_", (), torch.int64),
+    lt = () if head == "occlusion" else (4,)
+    out = SampleSet(head, cat("oo", (), torch.int64), cat("oc", (4,), torch.float64),
+                    cat("ol", lt, torch.float32), cat("or_", (), torch.int64),
                     cat("io", (), torch.int64), cat("ic", (5,), torch.float64),
-                    cat("il", (), torch.float32), cat("ir", (), torch.int64), n_rays=n_rays)
+                    cat("il", lt, torch.float32), cat("ir", (), torch.int64), n_rays=n_rays)
     out.stats = {"pixel_samples": spp * n_pix, "shadow_rays": shadow_rays,
                  "degenerate_queries": degenerate,
                  "outer_per_object": np.bincount(out.outer_obj.cpu().numpy(),
@@ -270,7 +297,9 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
             for k in range(0, n, bs):
                 m = min(bs, n - k)
                 st.run(obj, coord, label, None, m, rank, world, group, idx_ptr=base + 8 * k)
-            sums[fam] = float(st.sq.item())
+            # the reference's per-batch loss is the mean over rows x outputs
+            width = int(label.shape[1]) if label.dim() > 1 else 1
+            sums[fam] = float(st.sq.item()) / width
             counts[fam] = n
         om = sums[0] / counts[0] if counts[0] else math.nan
         im = sums[1] / counts[1] if counts[1] else math.nan

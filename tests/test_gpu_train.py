@@ -127,3 +127,33 @@ def test_train_curve_close_to_reference(name, cuda, golden, scenes):
     assert np.all(np.isnan(curve) == np.isnan(ref))
     ok = ~np.isnan(ref)
     np.testing.assert_allclose(curve[ok], ref[ok], rtol=0.05)
+
+
+def test_geometry_head_samples_and_training(cuda, golden):
+    """labeler="geometry" (nif.py:547-566 / bvh.py:920-950): primary rays,
+    per-object closest-hit labels (unit normal, t / diagonal) and the kept
+    rows equal the reference's bit for bit (golden made by running the
+    reference's own kernel, tests/golden/make_geometry.py); a geometry-head
+    model (4-wide identity output) trains with the reference's loss curve."""
+    from scenes import RECIPES, build_scene
+    from paper_2306_07191_b200.nif import NifConfig, NifModel
+    from paper_2306_07191_b200.train import collect_samples, train
+    g = golden("geometry")
+    recipe = dict(RECIPES["overlap"])
+    recipe["camera"] = {**recipe["camera"], "width": 48, "height": 40}
+    s = build_scene(recipe)
+    smp = collect_samples(s, spp=2, labeler="geometry", seed=s.seed)
+    assert smp.head == "geometry"
+    h = smp.host()
+    for k in ("outer_obj", "outer_label", "outer_ray", "inner_obj", "inner_label", "inner_ray"):
+        np.testing.assert_array_equal(h[k], g[k], err_msg=k)
+    np.testing.assert_allclose(h["outer_coord"], g["outer_coord"], rtol=0, atol=1e-14)
+    cfg = NifConfig(seed=4, head="geometry")
+    cfg.outer.grid_resolution = 32
+    cfg.inner.grid_resolution = 16
+    m = NifModel(cfg, s.n_objects, s.diagonal)
+    curve = train(m, smp, epochs=2)
+    ref = g["curve"]
+    assert np.all(np.isnan(curve) == np.isnan(ref))
+    ok = ~np.isnan(ref)
+    np.testing.assert_allclose(curve[ok], ref[ok], rtol=0.02)
