@@ -212,6 +212,10 @@ int nif_debug_set_prof_gather(void* buf);
  * with look-back (reference order), 2 persistent TMA-pipelined look-back
  * (reference order). All produce the same records.                     */
 int nif_debug_set_gather_variant(int v);
+/* Culling statistics of the hot-path gather since the last call (rays,
+ * bundle survivors, prefilter survivors, classified hits); only in a
+ * library built with -DNIF_GATHER_STATS (tools/gather_stats.py).       */
+int nif_debug_gather_stats(unsigned long long* out4);
 /* Query-kernel variant (benchmarks / equivalence tests): 0 fused with the
  * A operand in TMEM (default); 1 / 9 shared-memory-operand specialisations
  * (6 / 4 tiles per SM); 2 runtime-shape generic kernel; 3 no corner

@@ -934,6 +934,10 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
 #ifndef NIF_GATHER_MINB_U
 #define NIF_GATHER_MINB_U 3
 #endif
+#ifdef NIF_GATHER_STATS
+// diagnostics build only: rays, bundle survivors, prefilter survivors, hits
+__device__ unsigned long long g_gstats[4];
+#endif
 
 __global__ void __launch_bounds__(kThreads, NIF_GATHER_MINB_U)
 gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
@@ -1029,12 +1033,20 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       } else {
         pmask = all_obj;
       }
+#ifdef NIF_GATHER_STATS
+      atomicAdd(&g_gstats[0], 1ull);
+      atomicAdd(&g_gstats[1], (unsigned long long)__popc(wmask));
+      atomicAdd(&g_gstats[2], (unsigned long long)__popc(pmask));
+#endif
       while (pmask) {
         const int k = __ffs(pmask) - 1;
         pmask &= pmask - 1;
         double t0;
         const int kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
         if (kind == 0) continue;
+#ifdef NIF_GATHER_STATS
+        atomicAdd(&g_gstats[3], 1ull);
+#endif
         if (objs[k].route == 1) {
           mask |= (uint64_t)kind << (2 * k);
           if (kind == 1) ++n_out;
@@ -1210,6 +1222,18 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
 extern "C" int nif_debug_set_prof_gather(void* buf) {
   g_gprof = (long long*)buf;
   return NIF_OK;
+}
+
+extern "C" int nif_debug_gather_stats(unsigned long long* out) {
+#ifdef NIF_GATHER_STATS
+  cudaMemcpyFromSymbol(out, g_gstats, sizeof(unsigned long long) * 4);
+  unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_gstats, z, sizeof(z));
+  return NIF_OK;
+#else
+  (void)out;
+  return fail(NIF_ERR_UNSUPPORTED, "built without NIF_GATHER_STATS");
+#endif
 }
 
 extern "C" int nif_debug_set_gather_variant(int v) {
