@@ -100,6 +100,11 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
   float* dzB = dzA + (size_t)RB * WP;      // [RB][WP]
   float* xs = dzB + (size_t)RB * WP;       // [RB][kMaxIn]
   float* dh = xs + (size_t)RB * kMaxIn;    // [RB][kMaxOut]
+  // per_object sharing: the weight gradients of a CTA are reduced per head
+  // over that head's rows only (rows of a batch belong to several objects)
+  int* s_rhead = reinterpret_cast<int*>(dh + (size_t)RB * kMaxOut);  // [RB]
+  int* s_uniq = s_rhead + RB;                                         // [RB]
+  __shared__ int s_nuniq;
 
   const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
   const int64_t g = a.row0 + k_row * a.row_step;
@@ -107,10 +112,25 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
   const int64_t row = valid ? (a.idx ? a.idx[g] : g) : 0;
   const int o = valid ? (int)a.obj[row] : 0;
   const int head = f.n_heads > 1 ? o : 0;
+  s_rhead[tid] = valid ? head : -1;
+  __syncthreads();
+  if (tid == 0) {
+    int nu = 0;
+    for (int r = 0; r < RB; ++r) {
+      const int h = s_rhead[r];
+      if (h < 0) continue;
+      bool seen = false;
+      for (int q = 0; q < nu; ++q) seen = seen || s_uniq[q] == h;
+      if (!seen) s_uniq[nu++] = h;
+    }
+    s_nuniq = nu;
+  }
+  __syncthreads();
+  const int n_uniq = s_nuniq;
   const float* Wt = f.w + (size_t)head * f.w_stride;
   const float* Bt = f.b + (size_t)head * f.b_stride;
-  float* gW = a.t.grad + a.t.off_w + (size_t)head * f.w_stride;
-  float* gB = a.t.grad + a.t.off_b + (size_t)head * f.b_stride;
+  float* gW0 = a.t.grad + a.t.off_w;
+  float* gB0 = a.t.grad + a.t.off_b;
   const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
 
   // ---- encode (grids.py:141-191: fp64 weights, fp64 sum, fp32 result) ----
@@ -214,16 +234,23 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
   }
   __syncthreads();
   // head gradients: gW[q][k] = sum_r dh[r][q] * a_{L-1}[r][k]
-  for (int e = tid; e < OUT * (W + 1); e += RB) {
-    const int q = e / (W + 1), k = e % (W + 1);
-    float s = 0.f;
-    if (k < W) {
-      for (int r = 0; r < RB; ++r)
-        s = fmaf(dh[r * kMaxOut + q], leaky(zs[((size_t)(L - 1) * RB + r) * WP + k]), s);
-      atomicAdd(gW + wo_h + q * W + k, s);
-    } else {
-      for (int r = 0; r < RB; ++r) s += dh[r * kMaxOut + q];
-      atomicAdd(gB + bo_h + q, s);
+  for (int hi = 0; hi < n_uniq; ++hi) {
+    const int hh = s_uniq[hi];
+    float* gW = gW0 + (size_t)hh * f.w_stride;
+    float* gB = gB0 + (size_t)hh * f.b_stride;
+    for (int e = tid; e < OUT * (W + 1); e += RB) {
+      const int q = e / (W + 1), k = e % (W + 1);
+      float s = 0.f;
+      if (k < W) {
+        for (int r = 0; r < RB; ++r)
+          if (s_rhead[r] == hh)
+            s = fmaf(dh[r * kMaxOut + q], leaky(zs[((size_t)(L - 1) * RB + r) * WP + k]), s);
+        atomicAdd(gW + wo_h + q * W + k, s);
+      } else {
+        for (int r = 0; r < RB; ++r)
+          if (s_rhead[r] == hh) s += dh[r * kMaxOut + q];
+        atomicAdd(gB + bo_h + q, s);
+      }
     }
   }
   // hidden layers L-1 .. 1
@@ -233,16 +260,24 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
     wo -= (size_t)W * W;
     bo -= W;
     // weight grads of dense layer l: sum_r dz_l[r][j] * a_{l-1}[r][k]
-    for (int e = tid; e < W * (W + 1); e += RB) {
-      const int j = e / (W + 1), k = e % (W + 1);
-      float s = 0.f;
-      if (k < W) {
-        for (int r = 0; r < RB; ++r)
-          s = fmaf(dzc[(size_t)r * WP + j], leaky(zs[((size_t)(l - 1) * RB + r) * WP + k]), s);
-        atomicAdd(gW + wo + (size_t)j * W + k, s);
-      } else {
-        for (int r = 0; r < RB; ++r) s += dzc[(size_t)r * WP + j];
-        atomicAdd(gB + bo + j, s);
+    for (int hi = 0; hi < n_uniq; ++hi) {
+      const int hh = s_uniq[hi];
+      float* gW = gW0 + (size_t)hh * f.w_stride;
+      float* gB = gB0 + (size_t)hh * f.b_stride;
+      for (int e = tid; e < W * (W + 1); e += RB) {
+        const int j = e / (W + 1), k = e % (W + 1);
+        float s = 0.f;
+        if (k < W) {
+          for (int r = 0; r < RB; ++r)
+            if (s_rhead[r] == hh)
+              s = fmaf(dzc[(size_t)r * WP + j], leaky(zs[((size_t)(l - 1) * RB + r) * WP + k]),
+                       s);
+          atomicAdd(gW + wo + (size_t)j * W + k, s);
+        } else {
+          for (int r = 0; r < RB; ++r)
+            if (s_rhead[r] == hh) s += dzc[(size_t)r * WP + j];
+          atomicAdd(gB + bo + j, s);
+        }
       }
     }
     // dz_{l-1} = mask(z_{l-1}) * (dz_l W_l)
@@ -262,15 +297,22 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
     dzn = tmp;
   }
   // layer 0 weight grads: sum_r dz_0[r][j] * x[r][k]
-  for (int e = tid; e < W * (IN + 1); e += RB) {
-    const int j = e / (IN + 1), k = e % (IN + 1);
-    float s = 0.f;
-    if (k < IN) {
-      for (int r = 0; r < RB; ++r) s = fmaf(dzc[(size_t)r * WP + j], xs[r * kMaxIn + k], s);
-      atomicAdd(gW + (size_t)j * IN + k, s);
-    } else {
-      for (int r = 0; r < RB; ++r) s += dzc[(size_t)r * WP + j];
-      atomicAdd(gB + j, s);
+  for (int hi = 0; hi < n_uniq; ++hi) {
+    const int hh = s_uniq[hi];
+    float* gW = gW0 + (size_t)hh * f.w_stride;
+    float* gB = gB0 + (size_t)hh * f.b_stride;
+    for (int e = tid; e < W * (IN + 1); e += RB) {
+      const int j = e / (IN + 1), k = e % (IN + 1);
+      float s = 0.f;
+      if (k < IN) {
+        for (int r = 0; r < RB; ++r)
+          if (s_rhead[r] == hh) s = fmaf(dzc[(size_t)r * WP + j], xs[r * kMaxIn + k], s);
+        atomicAdd(gW + (size_t)j * IN + k, s);
+      } else {
+        for (int r = 0; r < RB; ++r)
+          if (s_rhead[r] == hh) s += dzc[(size_t)r * WP + j];
+        atomicAdd(gB + j, s);
+      }
     }
   }
   if (!valid) return;
@@ -748,7 +790,7 @@ int launch_fwdbwd(const TrainArgs& a, cudaStream_t st) {
   int rb = 128;
   auto smem_for = [&](int r) {
     return ((size_t)L * r * (W + 1) + 2 * (size_t)r * (W + 1) + (size_t)r * kMaxIn +
-            (size_t)r * kMaxOut) * sizeof(float);
+            (size_t)r * kMaxOut) * sizeof(float) + 2 * (size_t)r * sizeof(int);
   };
   while (rb > 32 && smem_for(rb) > 200 * 1024) rb /= 2;
   const size_t smem = smem_for(rb);
