@@ -352,15 +352,16 @@ def main():
     nif_be = NifBackend(model)
     render_ms = {}
     for name, be in (("nif", nif_be), ("bvh", BvhBackend())):
-        render_dev(scene, be, spp=1, sample_offset=rank)
+        for _ in range(2):
+            render_dev(scene, be, spp=1, sample_offset=rank)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(3):
+        for _ in range(5):
             render_dev(scene, be, spp=1, sample_offset=rank)
         e1.record(stream)
         e1.synchronize()
-        render_ms[name] = e0.elapsed_time(e1) / 3
+        render_ms[name] = e0.elapsed_time(e1) / 5
     del nif_be
 
     # --- e2e through the public API with pinned host buffers ----------------
