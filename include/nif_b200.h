@@ -218,8 +218,8 @@ int nif_debug_set_gather_variant(int v);
 int nif_debug_gather_stats(unsigned long long* out4);
 /* Query-kernel variant (benchmarks / equivalence tests): 0 fused with the
  * A operand in TMEM (default); 1 / 9 shared-memory-operand specialisations
- * (6 / 4 tiles per SM); 2 runtime-shape generic kernel; 3 no corner
- * prefetch; 11 TMEM operand, one tile per CTA.                          */
+ * (6 / 4 tiles per SM); 2 runtime-shape generic kernel; 11 TMEM operand,
+ * one tile per CTA.                                                     */
 int nif_debug_set_query_variant(int v);
 /* Training fwd/bwd kernel: 0 tiled CTA-GEMM kernel where it applies
  * (shared MLP, width a multiple of 16; default), 1 one row per thread. */

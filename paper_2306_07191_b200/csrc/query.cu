@@ -800,7 +800,7 @@ __device__ __forceinline__ float head_simt(uint32_t taddr, const float* __restri
   return s.x + s.y;
 }
 
-template <int N, int ND, int W, int L, int G, int TPS, bool PF, bool HS, int DBG>
+template <int N, int ND, int W, int L, int G, int TPS>
 __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
   using C = Tc2<N, ND, W, L, G>;
   constexpr bool INNER = ND > 0;
@@ -826,28 +826,11 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
   const int64_t stride = (int64_t)gridDim.x * G;
   const int64_t first = (int64_t)blockIdx.x * G + wg;
 
-  // PF: corner gathers of tile k+1 in flight under tile k's head MMA;
-  // otherwise only the record words are prefetched one tile ahead.
-  // DBG (bench-only ablations): 1 = no latent-table gathers, 2 = no MLP
-  auto issue = [&](EncIn<N, ND>& e, const RecIn& r, const __half* p0, const __half* p1,
-                   const __half* p2, int R, int Rd) {
-    if constexpr (DBG == 1) {
-      e = EncIn<N, ND>{};
-      e.valid = r.valid;
-      e.ray = r.ray;
-      e.wp[0] = r.c.x;
-    } else {
-      issue_enc<N, ND>(e, r, p0, p1, p2, R, Rd);
-    }
-  };
+  // corner gathers of tile k+1 in flight under tile k's head MMA, record
+  // words of tile k+2 one stage earlier
   EncIn<N, ND> ea;
-  RecIn rb;
-  if constexpr (PF) {
-    issue(ea, load_rec(a, first, trow, n, INNER), tpos, tdir, tdist, l.R, l.Rd);
-    rb = load_rec(a, first + stride, trow, n, INNER);
-  } else {
-    rb = load_rec(a, first, trow, n, INNER);
-  }
+  issue_enc<N, ND>(ea, load_rec(a, first, trow, n, INNER), tpos, tdir, tdist, l.R, l.Rd);
+  RecIn rb = load_rec(a, first + stride, trow, n, INNER);
 
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.blob);
@@ -883,10 +866,6 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
   uint32_t phase = 0;
   for (int64_t t = first; t < n_tiles; t += stride) {
     const int64_t row = t * kTileRows + trow;
-    if constexpr (!PF) {
-      issue(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
-      rb = load_rec(a, t + stride, trow, n, INNER);
-    }
     const bool valid = ea.valid;
     const int my_ray = ea.ray;
     {
@@ -904,15 +883,6 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
       store_chunk(sA, trow, 0, Kp, v0);
       store_chunk(sA, trow, 1, Kp, v1);
     }
-    if constexpr (DBG == 2) {
-      if constexpr (PF) {
-        issue(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
-        rb = load_rec(a, t + 2 * stride, trow, n, INNER);
-      }
-      if (valid && a.occ && __half2float(reinterpret_cast<__half*>(sA + trow * 16)[0]) < -100.f)
-        a.occ[my_ray] = 1;
-      continue;
-    }
     tc::fence_async_smem();
     tc::fence_before_sync();
     tc::named_sync(bar_id, 128);
@@ -928,7 +898,6 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
 
 #pragma unroll
     for (int layer = 1; layer <= L; ++layer) {
-      if (HS && layer == L) break;  // last layer + head on the CUDA cores below
       epilogue_act<W>(lane_acc, sA, trow, Kp, slope2);
       tc::fence_async_smem();
       tc::fence_before_sync();
@@ -947,21 +916,16 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
                       tc::smem_desc(wb + s * 256, 128, Kp * 16), hid ? idW : id16, s > 0);
         tc::mma_commit(bar);
       }
-      if (PF && layer == (HS ? L - 1 : L)) {
-        // next tile's inputs go in flight under the last MMA of this tile
-        issue(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+      if (layer == L) {
+        // next tile's inputs go in flight under the head MMA of this tile
+        issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
         rb = load_rec(a, t + 2 * stride, trow, n, INNER);
       }
       tc::mbar_wait_sleep(bar, phase);
       phase ^= 1;
       tc::fence_after_sync();
     }
-    float logit;
-    if constexpr (HS) {
-      logit = head_simt<W>(lane_acc, reinterpret_cast<const float*>(sW + C::OFF_HEADF));
-    } else {
-      logit = tc::tmem_ld1(lane_acc);
-    }
+    const float logit = tc::tmem_ld1(lane_acc);
     if (valid) {
       if (a.logits) a.logits[row] = logit;
       if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
@@ -974,11 +938,10 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
 
 // TPS = tiles in flight per SM the register budget is sized for
 // (8: 64 registers/thread; 6: 80).
-template <int N, int ND, int W, int L, int G, int TPS = 8, bool PF = true, bool HS = false,
-          int DBG = 0>
+template <int N, int ND, int W, int L, int G, int TPS>
 int launch_tc2(const TcArgs& a, cudaStream_t st) {
   using C = Tc2<N, ND, W, L, G>;
-  auto kern = query_tc2_kernel<N, ND, W, L, G, TPS, PF, HS, DBG>;
+  auto kern = query_tc2_kernel<N, ND, W, L, G, TPS>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
       cudaSuccess)
     return check_launch("query_tc2: smem attribute");
@@ -996,82 +959,20 @@ int launch_tc2(const TcArgs& a, cudaStream_t st) {
   return check_launch("nif_query_dev(tcgen05 specialised)");
 }
 
-// Dispatch to a compile-time specialisation; returns 1 when none matches.
+// Shared-memory-operand specialisations of the default shapes, kept as
+// measured alternatives (nif_debug_set_query_variant 1 / 9) and checked
+// against the oracle by tests/test_gpu_query_variants.py.
 int launch_tc2_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
   const int W = a.l.W, L = a.l.L;
-#define NIF_TC2H(NN, NDD, WW, LL, GG, TT, PP, HH)                                     \
-  if (f.N == NN && (NDD == 0 ? f.family == NIF_FAMILY_OUTER                 \
-                             : (f.family == NIF_FAMILY_INNER && f.Nd == NDD)) && \
-      W == WW && L == LL) {                                                 \
-    *rc = launch_tc2<NN, NDD, WW, LL, GG, TT, PP, HH>(a, st);                         \
-    return 0;                                                               \
+  const int tps = g_query_variant == 9 ? 4 : 6;
+  if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
+    *rc = tps == 4 ? launch_tc2<3, 0, 64, 2, 2, 4>(a, st) : launch_tc2<3, 0, 64, 2, 2, 6>(a, st);
+    return 0;
   }
-#define NIF_TC2(NN, NDD, WW, LL, GG, TT, PP) NIF_TC2H(NN, NDD, WW, LL, GG, TT, PP, false)
-  // defaults (nif.py:59-156): outer 2 x 64, inner 3 x 48
-  if (g_query_variant == 1) {
-    NIF_TC2(3, 0, 64, 2, 2, 6, true)
-    NIF_TC2(5, 3, 48, 3, 2, 6, true)
+  if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
+    *rc = tps == 4 ? launch_tc2<5, 3, 48, 3, 2, 4>(a, st) : launch_tc2<5, 3, 48, 3, 2, 6>(a, st);
+    return 0;
   }
-  if (g_query_variant == 4) {
-    NIF_TC2H(3, 0, 64, 2, 2, 8, true, true)
-    NIF_TC2H(5, 3, 48, 3, 2, 8, true, true)
-  }
-  if (g_query_variant == 5) {
-    NIF_TC2H(3, 0, 64, 2, 2, 6, true, true)
-    NIF_TC2H(5, 3, 48, 3, 2, 6, true, true)
-  }
-  if (g_query_variant == 6) {
-    if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
-      *rc = launch_tc2<3, 0, 64, 2, 2, 6, true, false, 1>(a, st);
-      return 0;
-    }
-    if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
-      *rc = launch_tc2<5, 3, 48, 3, 2, 6, true, false, 1>(a, st);
-      return 0;
-    }
-  }
-  if (g_query_variant == 7) {
-    if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
-      *rc = launch_tc2<3, 0, 64, 2, 2, 6, true, false, 2>(a, st);
-      return 0;
-    }
-    if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
-      *rc = launch_tc2<5, 3, 48, 3, 2, 6, true, false, 2>(a, st);
-      return 0;
-    }
-  }
-  if (g_query_variant == 8) {
-    NIF_TC2(3, 0, 64, 2, 1, 5, true)
-    NIF_TC2(5, 3, 48, 3, 1, 5, true)
-  }
-  if (g_query_variant == 9) {
-    NIF_TC2(3, 0, 64, 2, 2, 4, true)
-    NIF_TC2(5, 3, 48, 3, 2, 4, true)
-  }
-  if (g_query_variant == 10) {
-    NIF_TC2(3, 0, 64, 2, 1, 4, true)
-    NIF_TC2(5, 3, 48, 3, 1, 4, true)
-  }
-  if (g_query_variant == 3) {
-    NIF_TC2(3, 0, 64, 2, 2, 8, false)
-    NIF_TC2(5, 3, 48, 3, 2, 8, false)
-  }
-  NIF_TC2(3, 0, 64, 2, 2, 8, true)
-  NIF_TC2(5, 3, 48, 3, 2, 8, true)
-  // C5 sweep: widths 64 / 128, 2-4 hidden layers
-  NIF_TC2(3, 0, 64, 3, 2, 8, true)
-  NIF_TC2(3, 0, 64, 4, 2, 8, true)
-  NIF_TC2(3, 0, 128, 2, 1, 2, true)
-  NIF_TC2(3, 0, 128, 3, 1, 2, true)
-  NIF_TC2(3, 0, 128, 4, 1, 2, true)
-  NIF_TC2(5, 3, 64, 2, 2, 8, true)
-  NIF_TC2(5, 3, 64, 3, 2, 8, true)
-  NIF_TC2(5, 3, 64, 4, 2, 8, true)
-  NIF_TC2(5, 3, 128, 2, 1, 2, true)
-  NIF_TC2(5, 3, 128, 3, 1, 2, true)
-  NIF_TC2(5, 3, 128, 4, 1, 2, true)
-#undef NIF_TC2
-#undef NIF_TC2H
   return 1;
 }
 
@@ -1697,9 +1598,11 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
              logits, g_prof};
     if (impl != NIF_IMPL_TCGEN05_GENERIC && g_prof == nullptr && g_query_variant != 2) {
       int rc = NIF_OK;
-      if ((g_query_variant == 0 || g_query_variant == 11) && launch_ts_any(a, *f, st, &rc) == 0)
+      if (g_query_variant == 1 || g_query_variant == 9) {
+        if (launch_tc2_any(a, *f, st, &rc) == 0) return rc;
+      } else if (launch_ts_any(a, *f, st, &rc) == 0) {
         return rc;
-      if (launch_tc2_any(a, *f, st, &rc) == 0) return rc;
+      }
     }
     if (f->family == NIF_FAMILY_OUTER && f->N == 3) return launch_tc<3, 0>(a, st);
     if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 3) return launch_tc<5, 3>(a, st);

@@ -2,9 +2,10 @@
 
     python tools/bench_query.py [--train-epochs 0]
 
-Variants (nif_debug_set_query_variant): 0 specialised, 8 tiles/SM, corner
-prefetch; 1 specialised, 6 tiles/SM (80 regs); 3 specialised, no corner
-prefetch; 2 runtime-shape generic kernel. Logits of every variant are
+Variants (nif_debug_set_query_variant): 0 production (A operand in TMEM);
+1 / 9 shared-memory-operand specialisations (6 / 4 tiles per SM); 2
+runtime-shape generic kernel; 11 TMEM operand, one tile per CTA; "S0" the
+split path (encoding kernel + MLP kernel). Logits of every variant are
 compared with the generic kernel on the same records.
 """
 import ctypes as C
