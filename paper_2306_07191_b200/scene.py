@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -155,6 +156,19 @@ def build_bottom(arrays) -> BottomLevelBvh:
     if bvh.depth() > MAX_DEPTH - 8:
         raise ValueError("tree depth exceeds the traversal stack budget")
     return bvh
+
+
+def build_bottoms(arrays_list, workers: Optional[int] = None):
+    """build_bottom over many objects on host threads (the native builder
+    and numpy release the GIL); trees are identical to sequential builds."""
+    from concurrent.futures import ThreadPoolExecutor
+    arrays_list = list(arrays_list)
+    if workers is None:
+        workers = min(len(arrays_list), os.cpu_count() or 1)
+    if workers <= 1 or len(arrays_list) <= 1:
+        return [build_bottom(a) for a in arrays_list]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(build_bottom, arrays_list))
 
 
 def build_top(boxes: Sequence[Aabb]) -> TopLevelBvh:

@@ -14,7 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import meshgen
-from .scene import Camera, PointLight, Scene, SceneObject, build_bottom
+from .scene import Camera, PointLight, Scene, SceneObject, build_bottom, build_bottoms
 
 LIGHT = PointLight(np.array([2.2, -1.6, 2.8]), np.array([28.0, 28.0, 28.0]))
 
@@ -36,16 +36,19 @@ def c1(width=256, height=256, subdiv=5, plane_nif=False) -> Scene:
 def lattice(n_spheres: int, subdiv: int, radius: float, width=1920, height=1080,
             cols: int = 4) -> Scene:
     base = meshgen.mesh_arrays(*meshgen.icosphere(subdiv, radius))
-    objs = []
     rows = (n_spheres + cols - 1) // cols
     pitch = 1.2 if n_spheres <= 12 else 3.6 / max(cols - 1, 1)
+    arrays = []
     for k in range(n_spheres):
         x = -1.8 + pitch * (k % cols)
         y = -0.6 + 1.2 * (k // cols) - (0.6 * (rows - 3) if rows > 3 else 0.0)
-        arrays = meshgen.transformed(base, 1.0, (x, y, radius))
-        objs.append(_obj(f"sphere{k}", arrays, (0.75, 0.33, 0.27)))
-    objs.append(_obj("plane", meshgen.mesh_arrays(*meshgen.ground_plane(4.0)),
-                     (0.62, 0.62, 0.6), True))
+        arrays.append(meshgen.transformed(base, 1.0, (x, y, radius)))
+    arrays.append(meshgen.mesh_arrays(*meshgen.ground_plane(4.0)))
+    # the per-object trees are independent: build them on all host cores
+    trees = build_bottoms(arrays)
+    objs = [SceneObject(f"sphere{k}", trees[k], np.asarray((0.75, 0.33, 0.27), np.float64), True)
+            for k in range(n_spheres)]
+    objs.append(SceneObject("plane", trees[-1], np.asarray((0.62, 0.62, 0.6), np.float64), True))
     cam = Camera(np.array([0.0, -4.4, 2.2]), np.array([0.0, 0.0, 0.3]),
                  np.array([0.0, 0.0, 1.0]), 45.0, width, height)
     return Scene(objs, [LIGHT], cam, 11)
