@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--train-epochs", type=int, default=0,
                    help="epochs of GPU training on 1 spp before timing (0 = random init)")
+    p.add_argument("--sharing", default="shared", choices=["shared", "per_object"],
+                   help="NifConfig.sharing (per_object: one MLP per object, bucketed query)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-chunks", type=int, default=4,
                    help="chunks of the e2e host path (H2D of chunk k+1 overlaps chunk k)")
@@ -267,7 +269,7 @@ def main():
     data = sample_pass_dev(scene, scene.camera, rank, scene.seed)
     _, o, d, t = shadow_rays_dev(data, require_emit=False)
     n = int(t.numel())
-    model = build_model(NifConfig(seed=0), scene)
+    model = build_model(NifConfig(seed=0, sharing=args.sharing), scene)
     if args.train_epochs > 0:
         from paper_2306_07191_b200 import train as tr
         samples = tr.collect_samples_dev(scene, spp=1, seed=scene.seed)
@@ -467,7 +469,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "rays_per_frame_per_gpu": n,
                    "outer_records": n_outer,
-                   "inner_records": n_inner, "model": "NifConfig() defaults (R 256/128)",
+                   "inner_records": n_inner, "model": f"NifConfig() defaults (R 256/128), sharing={args.sharing}",
                    "trained_epochs": args.train_epochs, "l2": "flushed (256 MiB write) per step",
                    "parallelism": f"{ws} independent frames (sample index = rank)"},
         "frame_ms": ms / args.steps,

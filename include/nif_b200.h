@@ -196,6 +196,17 @@ int nif_query_split_dev(const nif_family_view* f, const int32_t* obj, const int3
                         const float* coord4, const float* r, const int64_t* count_dev,
                         int64_t capacity, uint8_t* occ_ray, float* logits, void* feat,
                         int32_t flags, void* stream);
+/* per_object sharing (one MLP per object, nif.py:91-92, 380-397) on the
+ * tensor cores: the queue is counting-sorted by object into 128-row tiles
+ * (padding rows inert) inside scratch (nif_bucket_scratch_bytes), then the
+ * TMEM-operand kernel runs each tile with its object's weights. Same
+ * outputs as nif_query_dev; without bucketing per-object MLPs run on the
+ * SIMT kernel.                                                         */
+size_t nif_bucket_scratch_bytes(int64_t capacity, int32_t n_obj);
+int nif_query_bucketed_dev(const nif_family_view* f, const int32_t* obj, const int32_t* ray,
+                           const float* coord4, const float* r, const int64_t* count_dev,
+                           int64_t capacity, uint8_t* occ_ray, float* logits, void* scratch,
+                           void* stream);
 #define NIF_IMPL_AUTO 0
 #define NIF_IMPL_SIMT 1    /* fp32 CUDA-core reference kernel */
 #define NIF_IMPL_TCGEN05 2 /* fused tcgen05/TMEM fp16 kernel (shape-specialised

@@ -145,6 +145,8 @@ _SIGS = {
     "nif_query_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, I32, P]),
     "nif_occ_init_dev": (C.c_int, [P, I64, P, P]),
     "nif_feat_scratch_bytes": (C.c_size_t, [I64]),
+    "nif_bucket_scratch_bytes": (C.c_size_t, [I64, I32]),
+    "nif_query_bucketed_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, P, P]),
     "nif_query_split_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, P, I32, P]),
     "nif_debug_set_prof": (C.c_int, [P]),
     "nif_debug_set_prof_gather": (C.c_int, [P]),

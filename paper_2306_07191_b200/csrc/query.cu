@@ -41,6 +41,8 @@ constexpr int kTpc = 1;
 struct FastLayout {
   int W, L, in_dim, Kp, NP, NPd, R, Rd, N, Nd, n_obj;
   size_t off_w1, off_hidden, off_head, off_headf, w_bytes;
+  size_t w_stride_blob;  // bytes between the weight blocks of two heads
+  int n_heads;
   size_t off_pos, off_dir, off_dist, total;
   int tmem_cols;
   bool tc_ok;
@@ -66,7 +68,10 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   l.off_head = l.off_hidden + (size_t)(l.L > 0 ? l.L - 1 : 0) * l.W * l.Kp * 2;
   l.off_headf = l.off_head + (size_t)16 * l.Kp * 2;  // fp32 head row + bias (CUDA-core head)
   l.w_bytes = l.off_headf + ((size_t)(l.W + 1) * 4 + 15) / 16 * 16;
-  l.off_pos = al16(l.w_bytes);
+  // one weight block per head (per_object sharing: one MLP per object)
+  l.n_heads = f.n_heads;
+  l.w_stride_blob = al16(l.w_bytes);
+  l.off_pos = l.w_stride_blob * (size_t)(f.n_heads > 0 ? f.n_heads : 1);
   // 2-D tables with 4 latents per cell (outer) are corner-packed: one
   // 32 B entry per (u cell, v cell + 1) holding the four bilinear corners
   // (u wrap and v clamp applied), so a lookup is one sector and two 16 B
@@ -87,7 +92,7 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   const bool inst = (f.family == NIF_FAMILY_OUTER && (f.N == 2 || f.N == 3 || f.N == 4)) ||
                     (f.family == NIF_FAMILY_INNER &&
                      ((f.N == 5 && (f.Nd == 3 || f.Nd == 4)) || (f.N == 4 && f.Nd == 3)));
-  l.tc_ok = inst && f.n_heads == 1 && f.sigmoid_head == 1 && f.dims[f.n_layers] == 1 &&
+  l.tc_ok = inst && f.n_heads >= 1 && f.sigmoid_head == 1 && f.dims[f.n_layers] == 1 &&
             l.L >= 1 && hidden_same && l.W % 16 == 0 && l.W >= 16 && l.W <= 240 &&
             l.in_dim + 1 <= kK1;
   return l;
@@ -101,6 +106,10 @@ __host__ __device__ inline size_t canon_off(int r, int k, int kp) {
 
 // weights -> fp16 canonical tiles with the bias folded into column `in`
 __global__ void pack_weights_kernel(nif_family_view f, FastLayout l, uint8_t* blob) {
+  // blockIdx.y = head: per_object sharing packs one weight block per object
+  blob += (size_t)blockIdx.y * l.w_stride_blob;
+  f.w += (size_t)blockIdx.y * f.w_stride;
+  f.b += (size_t)blockIdx.y * f.b_stride;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int n1 = l.W * kK1;
   const int nh = (l.L - 1) * l.W * l.Kp;
@@ -318,6 +327,10 @@ struct TcArgs {
   uint8_t* occ;
   float* logits;
   long long* prof;  // diagnostic phase timestamps (nif_debug_set_prof), or NULL
+  // per_object sharing: records bucketed by object into 128-row tiles
+  const int32_t* perm;      // [tile * 128 + row] -> record index, -1 = padding
+  const int32_t* tile_obj;  // [tile] -> object (= head)
+  const int64_t* n_tiles;   // device count of bucketed tiles
 };
 
 long long* g_prof = nullptr;
@@ -337,7 +350,7 @@ __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<ui
 // k+2 are being fetched, so the dependent gathers (record -> indices ->
 // corners) never sit on the critical path of a tile.
 struct RecIn {
-  int obj, ray;
+  int obj, ray, rec;  // rec: record index (differs from the row for bucketed tiles)
   float4 c;
   float r;
   bool valid;
@@ -352,7 +365,7 @@ struct EncIn {
   static constexpr int NQ = NP / 2;  // 16 B loads per 2-D lookup (2 packed / 4 cells)
   uint4 qp[NQ], qd[NQ], qr;
   float wp[4], wd[4], wr;
-  int ray;
+  int ray, rec;
   bool valid;
 };
 
@@ -390,6 +403,7 @@ __device__ __forceinline__ RecIn load_rec(const TcArgs& a, int64_t tile, int tid
   r.valid = row < n;
   r.obj = 0;
   r.ray = 0;
+  r.rec = (int)row;
   r.c = make_float4(0.f, 0.f, 0.f, 0.f);
   r.r = 0.f;
   if (r.valid) {
@@ -401,12 +415,38 @@ __device__ __forceinline__ RecIn load_rec(const TcArgs& a, int64_t tile, int tid
   return r;
 }
 
+// record of a bucketed tile (per_object sharing): row -> record index via
+// perm, -1 = padding
+__device__ __forceinline__ RecIn load_rec_perm(const TcArgs& a, int64_t tile, int tid,
+                                               int64_t t_end, bool inner) {
+  RecIn r;
+  r.valid = false;
+  r.obj = 0;
+  r.ray = 0;
+  r.rec = -1;
+  r.c = make_float4(0.f, 0.f, 0.f, 0.f);
+  r.r = 0.f;
+  if (tile < t_end) {
+    const int idx = __ldg(a.perm + tile * kTileRows + tid);
+    if (idx >= 0) {
+      r.valid = true;
+      r.rec = idx;
+      r.obj = __ldg(a.obj + idx);
+      r.ray = __ldg(a.ray + idx);
+      r.c = __ldg(reinterpret_cast<const float4*>(a.coord4) + idx);
+      if (inner) r.r = __ldg(a.rr + idx);
+    }
+  }
+  return r;
+}
+
 template <int N, int ND>
 __device__ __forceinline__ void issue_enc(EncIn<N, ND>& e, const RecIn& r, const __half* tpos,
                                           const __half* tdir, const __half* tdist, int R, int Rd) {
   constexpr int NP = EncIn<N, ND>::NP, NQ = EncIn<N, ND>::NQ;
   e.valid = r.valid;
   e.ray = r.ray;
+  e.rec = r.rec;
   if (!r.valid) return;
   if constexpr (NP == 4) {  // corner-packed entries
     const size_t g2 = (size_t)R * (R + 1) * NQ;  // uint4 per object table
@@ -1002,6 +1042,7 @@ __device__ __forceinline__ RecIn load_rec_row(const int32_t* __restrict__ obj,
   r.valid = row < n;
   r.obj = 0;
   r.ray = 0;
+  r.rec = (int)row;
   r.c = make_float4(0.f, 0.f, 0.f, 0.f);
   r.r = 0.f;
   if (r.valid) {
@@ -1272,7 +1313,11 @@ __global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) 
 // last layer and the N=1 head run on the CUDA cores from the fp32
 // accumulator. 6 (W=48) / 4 (W=64) tiles in flight per SM, bounded by TMEM.
 // ---------------------------------------------------------------------------
-template <int N, int ND, int W, int L, int G, int TPS>
+// PO (per_object sharing): records arrive bucketed by object into 128-row
+// tiles (nif_query_bucketed_dev); each warpgroup walks a contiguous range of
+// tiles and keeps its own copy of the current object's weights, reloading
+// it only when the object changes.
+template <int N, int ND, int W, int L, int G, int TPS, bool PO = false>
 __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   using C = MlpCfg<W, L, G>;
   constexpr bool INNER = ND > 0;
@@ -1284,8 +1329,8 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   const int trow = tid & (kTileRows - 1);
   const int quad = (tid >> 5) & 3;
   const bool leader = trow == 0;
-  uint8_t* sW = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::W_AL);
+  uint8_t* sW = smem + (PO ? (size_t)wg * C::W_AL : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (PO ? G : 1) * C::W_AL);
   uint64_t* bar = bars + wg;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + G);
 
@@ -1293,18 +1338,32 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
   const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
   const int64_t n = min(*a.count, a.cap);
-  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
-  const int64_t stride = (int64_t)gridDim.x * G;
-  const int64_t first = (int64_t)blockIdx.x * G + wg;
+  int64_t n_tiles, stride, first;
+  if constexpr (PO) {  // contiguous tile range per warpgroup (objects change rarely)
+    const int64_t nt = *a.n_tiles;
+    const int64_t gw = (int64_t)gridDim.x * G;
+    const int64_t per = (nt + gw - 1) / gw;
+    first = ((int64_t)blockIdx.x * G + wg) * per;
+    n_tiles = min(first + per, nt);
+    stride = 1;
+  } else {
+    n_tiles = (n + kTileRows - 1) / kTileRows;
+    stride = (int64_t)gridDim.x * G;
+    first = (int64_t)blockIdx.x * G + wg;
+  }
+  auto fetch = [&](int64_t t) {
+    if constexpr (PO) return load_rec_perm(a, t, trow, n_tiles, INNER);
+    else return load_rec(a, t, trow, n, INNER);
+  };
 
   if (tid == 0) {
     for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
     tc::fence_barrier_init();
   }
   EncIn<N, ND> ea;
-  issue_enc<N, ND>(ea, load_rec(a, first, trow, n, INNER), tpos, tdir, tdist, l.R, l.Rd);
-  RecIn rb = load_rec(a, first + stride, trow, n, INNER);
-  {
+  issue_enc<N, ND>(ea, fetch(first), tpos, tdir, tdist, l.R, l.Rd);
+  RecIn rb = fetch(first + stride);
+  if constexpr (!PO) {
     const uint4* src = reinterpret_cast<const uint4*>(a.blob);
     uint4* dst = reinterpret_cast<uint4*>(sW);
     for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
@@ -1331,10 +1390,22 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   const float* headw = reinterpret_cast<const float*>(sW + C::OFF_HEADF);
 
   uint32_t phase = 0;
+  int cur_obj = -1;
   for (int64_t t = first; t < n_tiles; t += stride) {
-    const int64_t row = t * kTileRows + trow;
+    const int64_t row = ea.rec;
     const bool valid = ea.valid;
     const int my_ray = ea.ray;
+    if constexpr (PO) {  // this tile's object MLP -> the warpgroup's weight buffer
+      const int ot = __ldg(a.tile_obj + t);
+      if (ot != cur_obj) {
+        tc::named_sync(bar_id, 128);  // every thread is done with the previous head weights
+        const uint4* src = reinterpret_cast<const uint4*>(a.blob + (size_t)ot * l.w_stride_blob);
+        uint4* dst = reinterpret_cast<uint4*>(sW);
+        for (int i = trow; i < (int)(C::W_BYTES / 16); i += kTileRows) dst[i] = __ldg(src + i);
+        tc::fence_async_smem();
+        cur_obj = ot;
+      }
+    }
     {
       float x[16];
       finish_enc<N, ND>(ea, x);
@@ -1369,7 +1440,7 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
       }
       if (layer == L - 1) {  // next tile's gathers in flight under the last MMA + head
         issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
-        rb = load_rec(a, t + 2 * stride, trow, n, INNER);
+        rb = fetch(t + 2 * stride);
       }
       tc::mbar_wait_sleep(bar, phase);
       phase ^= 1;
@@ -1386,11 +1457,12 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
 }
 
-template <int N, int ND, int W, int L, int G, int TPS>
+template <int N, int ND, int W, int L, int G, int TPS, bool PO = false>
 int launch_ts(const TcArgs& a, cudaStream_t st) {
   using C = MlpCfg<W, L, G>;
-  auto kern = query_ts_kernel<N, ND, W, L, G, TPS>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+  auto kern = query_ts_kernel<N, ND, W, L, G, TPS, PO>;
+  const size_t smem = C::SMEM + (PO ? (size_t)(G - 1) * C::W_AL : 0);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return check_launch("query_ts: smem attribute");
   const int per_sm_tmem = 512 / C::COLS;
@@ -1401,8 +1473,22 @@ int launch_ts(const TcArgs& a, cudaStream_t st) {
   const int64_t need = (max_tiles + G - 1) / G;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, 128 * G, C::SMEM, st>>>(a);
+  kern<<<(unsigned)grid, 128 * G, smem, st>>>(a);
   return check_launch("nif_query_dev(tcgen05 TS)");
+}
+
+// per_object sharing (bucketed tiles): default shapes; 0 = launched
+int launch_ts_po(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
+  const int W = a.l.W, L = a.l.L;
+  if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
+    *rc = launch_ts<3, 0, 64, 2, 2, 4, true>(a, st);
+    return 0;
+  }
+  if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
+    *rc = launch_ts<5, 3, 48, 3, 3, 6, true>(a, st);
+    return 0;
+  }
+  return 1;
 }
 
 // 0 = launched, 1 = no specialisation
@@ -1555,6 +1641,104 @@ int launch_tc(const TcArgs& a, cudaStream_t st) {
   return check_launch("nif_query_dev(tcgen05)");
 }
 
+
+// ---------------------------------------------------------------------------
+// Bucketing by object (per_object sharing): counting sort of a record queue
+// into per-object segments padded to whole 128-row tiles, so every tile of
+// the tensor-core kernel runs one object's MLP. Order inside a segment is
+// arbitrary (the pass only ORs per ray).
+//   scratch: hist i32[n_obj] | cursor i32[n_obj] | tile_off i64[n_obj + 1] |
+//            n_tiles i64 | tile_obj i32[max_tiles] | perm i32[max_tiles*128]
+// ---------------------------------------------------------------------------
+struct BucketWs {
+  int32_t* hist;
+  int32_t* cursor;
+  int64_t* tile_off;
+  int64_t* n_tiles;
+  int32_t* tile_obj;
+  int32_t* perm;
+  int64_t max_tiles;
+};
+
+__host__ __device__ inline int64_t bucket_max_tiles(int64_t capacity, int n_obj) {
+  return (capacity + kTileRows - 1) / kTileRows + n_obj;
+}
+
+inline BucketWs bucket_ws(void* scratch, int64_t capacity, int n_obj) {
+  BucketWs w;
+  uint8_t* p = (uint8_t*)scratch;
+  const size_t o4 = ((size_t)n_obj * 4 + 255) / 256 * 256;
+  w.hist = (int32_t*)p;
+  w.cursor = (int32_t*)(p + o4);
+  w.tile_off = (int64_t*)(p + 2 * o4);
+  const size_t o8 = ((size_t)(n_obj + 1) * 8 + 255) / 256 * 256;
+  w.n_tiles = (int64_t*)(p + 2 * o4 + o8);
+  w.max_tiles = bucket_max_tiles(capacity, n_obj);
+  w.tile_obj = (int32_t*)(p + 2 * o4 + o8 + 256);
+  const size_t ot = ((size_t)w.max_tiles * 4 + 255) / 256 * 256;
+  w.perm = (int32_t*)(p + 2 * o4 + o8 + 256 + ot);
+  return w;
+}
+
+__global__ void bucket_hist_kernel(const int32_t* __restrict__ obj,
+                                   const int64_t* __restrict__ count, int64_t cap, int n_obj,
+                                   int32_t* __restrict__ hist) {
+  extern __shared__ int32_t sh[];
+  for (int o = threadIdx.x; o < n_obj; o += blockDim.x) sh[o] = 0;
+  __syncthreads();
+  const int64_t n = min(*count, cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(sh + __ldg(obj + i), 1);
+  __syncthreads();
+  for (int o = threadIdx.x; o < n_obj; o += blockDim.x)
+    if (sh[o]) atomicAdd(hist + o, sh[o]);
+}
+
+// one block: tile offsets (exclusive scan of padded counts), tile -> object
+__global__ void bucket_scan_kernel(BucketWs w, int n_obj) {
+  __shared__ int64_t s_total;
+  if (threadIdx.x == 0) {
+    int64_t off = 0;
+    for (int o = 0; o < n_obj; ++o) {
+      w.tile_off[o] = off;
+      off += (w.hist[o] + kTileRows - 1) / kTileRows;
+      w.cursor[o] = 0;
+    }
+    w.tile_off[n_obj] = off;
+    *w.n_tiles = off;
+    s_total = off;
+  }
+  __syncthreads();
+  for (int o = 0; o < n_obj; ++o)
+    for (int64_t t = w.tile_off[o] + threadIdx.x; t < w.tile_off[o + 1]; t += blockDim.x)
+      w.tile_obj[t] = o;
+  (void)s_total;
+}
+
+__global__ void bucket_scatter_kernel(const int32_t* __restrict__ obj,
+                                      const int64_t* __restrict__ count, int64_t cap,
+                                      BucketWs w) {
+  const int64_t n = min(*count, cap);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool v = i < n;
+    const int o = v ? __ldg(obj + i) : -1;
+    // warp-aggregated reservation: one atomic per distinct object per warp
+    const unsigned peers = __match_any_sync(0xffffffffu, o);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (v && lane == leader) base = atomicAdd(w.cursor + o, __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (v) {
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      w.perm[w.tile_off[o] * kTileRows + base + rank] = (int32_t)i;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace nif
 
@@ -1570,7 +1754,8 @@ extern "C" int nif_fast_pack_dev(const nif_family_view* f, void* blob, void* str
   cudaMemsetAsync(blob, 0, l.total, st);
   if (l.tc_ok) {
     const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp + l.W + 1;
-    pack_weights_kernel<<<(nw + 255) / 256, 256, 0, st>>>(*f, l, (uint8_t*)blob);
+    pack_weights_kernel<<<dim3((nw + 255) / 256, f->n_heads), 256, 0, st>>>(*f, l,
+                                                                            (uint8_t*)blob);
   }
   const int64_t cells = 2 * (l.NP == 4 ? (int64_t)l.n_obj * l.R * (l.R + 1) * 4
                                       : (int64_t)l.n_obj * l.R * l.R) +
@@ -1588,8 +1773,13 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
     return fail(NIF_ERR_VALUE, "inner queries need the radial coordinate");
   cudaStream_t st = (cudaStream_t)stream;
   const FastLayout l = make_layout(*f);
+  // one MLP per object needs the bucketed records of nif_query_bucketed_dev
+  // to run on the tensor cores; unbucketed it runs on the SIMT kernel
+  const bool shared_mlp = f->n_heads == 1;
+  if (!shared_mlp && (impl == NIF_IMPL_TCGEN05 || impl == NIF_IMPL_TCGEN05_GENERIC))
+    return fail(NIF_ERR_UNSUPPORTED, "per-object MLPs on tensor cores need nif_query_bucketed_dev");
   const bool want_tc = impl == NIF_IMPL_TCGEN05 || impl == NIF_IMPL_TCGEN05_GENERIC ||
-                       (impl == NIF_IMPL_AUTO && l.tc_ok && f->fast);
+                       (impl == NIF_IMPL_AUTO && l.tc_ok && shared_mlp && f->fast);
   if (want_tc) {
     if (!l.tc_ok)
       return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernel");
@@ -1621,6 +1811,49 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
   query_simt_kernel<<<(unsigned)blocks, 128, 0, st>>>(*f, obj, ray, coord4, r, count_dev,
                                                       capacity, occ_ray, logits);
   return check_launch("nif_query_dev(simt)");
+}
+
+
+extern "C" size_t nif_bucket_scratch_bytes(int64_t capacity, int32_t n_obj) {
+  const int64_t mt = bucket_max_tiles(capacity, n_obj);
+  const size_t o4 = ((size_t)n_obj * 4 + 255) / 256 * 256;
+  const size_t o8 = ((size_t)(n_obj + 1) * 8 + 255) / 256 * 256;
+  const size_t ot = ((size_t)mt * 4 + 255) / 256 * 256;
+  return 2 * o4 + o8 + 256 + ot + (size_t)mt * kTileRows * 4;
+}
+
+extern "C" int nif_query_bucketed_dev(const nif_family_view* f, const int32_t* obj,
+                                      const int32_t* ray, const float* coord4, const float* r,
+                                      const int64_t* count_dev, int64_t capacity,
+                                      uint8_t* occ_ray, float* logits, void* scratch,
+                                      void* stream) {
+  if (capacity <= 0) return NIF_OK;
+  if (f->family == NIF_FAMILY_INNER && r == nullptr)
+    return fail(NIF_ERR_VALUE, "inner queries need the radial coordinate");
+  if (scratch == nullptr) return fail(NIF_ERR_VALUE, "bucketed query needs a scratch buffer");
+  const FastLayout l = make_layout(*f);
+  if (!l.tc_ok) return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernels");
+  if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
+  cudaStream_t st = (cudaStream_t)stream;
+  const BucketWs w = bucket_ws(scratch, capacity, f->n_obj);
+  cudaMemsetAsync(w.hist, 0, (size_t)f->n_obj * 4, st);
+  cudaMemsetAsync(w.perm, 0xff, (size_t)w.max_tiles * kTileRows * 4, st);
+  int64_t blocks = (capacity + 255) / 256;
+  const int64_t cap_blocks = (int64_t)sm_count() * 8;
+  if (blocks > cap_blocks) blocks = cap_blocks;
+  bucket_hist_kernel<<<(unsigned)blocks, 256, (size_t)f->n_obj * 4, st>>>(obj, count_dev, capacity,
+                                                                          f->n_obj, w.hist);
+  bucket_scan_kernel<<<1, 256, 0, st>>>(w, f->n_obj);
+  bucket_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(obj, count_dev, capacity, w);
+  TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
+           logits, nullptr, w.perm, w.tile_obj, w.n_tiles};
+  // the tile range is bounded by max_tiles (read from the device count in-kernel)
+  a.cap = w.max_tiles * kTileRows;
+  int rc = NIF_OK;
+  if (launch_ts_po(a, *f, st, &rc) != 0)
+    return fail(NIF_ERR_UNSUPPORTED, "no per-object tensor-core specialisation for W=%d L=%d",
+                l.W, l.L);
+  return rc;
 }
 
 extern "C" size_t nif_feat_scratch_bytes(int64_t capacity) {

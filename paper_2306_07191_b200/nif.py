@@ -506,7 +506,15 @@ def query_family(model: NifModel, which: str, obj, coord, impl: int = _lib.IMPL_
     d_r = _to_dev(coord[:, 4], np.float32, dev) if which == "inner" else None
     d_cnt = torch.tensor([m], dtype=torch.int64, device=dev)
     d_log = torch.empty(m * fam.dims[-1], dtype=torch.float32, device=dev)
-    if split:
+    if fam.n_heads > 1 and impl in (_lib.IMPL_AUTO, _lib.IMPL_TCGEN05) and not split:
+        # per_object sharing: bucket by object, then the tensor-core kernel
+        L = _lib.lib()
+        scratch = torch.empty(int(L.nif_bucket_scratch_bytes(m, fam.n_obj)), dtype=torch.uint8,
+                              device=dev)
+        L.nif_query_bucketed_dev(fam.view(with_fast=True), _lib.ptr(d_obj), _lib.ptr(d_ray),
+                                 _lib.ptr(d_c4), _lib.ptr(d_r), _lib.ptr(d_cnt), m, None,
+                                 _lib.ptr(d_log), _lib.ptr(scratch), _lib.stream_ptr())
+    elif split:
         L = _lib.lib()
         feat = torch.empty(int(L.nif_feat_scratch_bytes(m)), dtype=torch.uint8, device=dev)
         L.nif_query_split_dev(fam.view(with_fast=True), _lib.ptr(d_obj), _lib.ptr(d_ray),

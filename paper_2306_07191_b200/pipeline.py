@@ -218,6 +218,13 @@ class VisibilityEngine:
         self.side = torch.cuda.Stream(device=dev)
         self._views = None
         self.graphs = {}
+        # per_object sharing: per-family scratch for the bucketed tensor-core query
+        self.bucket = None
+        if model is not None and model.outer.n_heads > 1:
+            L = _lib.lib()
+            nb = int(L.nif_bucket_scratch_bytes(self.buf.cap, model.outer.n_obj))
+            self.bucket = (torch.empty(nb, dtype=torch.uint8, device=dev),
+                           torch.empty(nb, dtype=torch.uint8, device=dev))
 
     def _family_views(self):
         if self._views is None or self.model.outer.dirty or self.model.inner.dirty:
@@ -248,16 +255,31 @@ class VisibilityEngine:
             return
         vo, vi = self._family_views()
         p = _lib.ptr
-        cnt = b.counts.data_ptr()
         # the two families are independent: outer on a side stream, inner on
         # the main one, joined before returning (fork/join is graph-capturable)
         main = stream if stream is not None else torch.cuda.current_stream()
         self.side.wait_stream(main)
-        L.nif_query_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None, cnt,
-                        b.cap, p(self.occ), None, self.impl, self.side.cuda_stream)
-        L.nif_query_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord), p(b.inner_r),
-                        cnt + 8, b.cap, p(self.occ), None, self.impl, sp)
+        self._query(vo, vi, p(self.occ), self.side.cuda_stream, sp)
         main.wait_stream(self.side)
+
+    def _query(self, vo, vi, occ, side_sp, main_sp):
+        """Outer family on the side stream, inner on the main one; per_object
+        models go through the bucketed tensor-core query."""
+        L = _lib.lib()
+        b = self.buf
+        p = _lib.ptr
+        cnt = b.counts.data_ptr()
+        if self.bucket is not None and self.impl in (_lib.IMPL_AUTO, _lib.IMPL_TCGEN05):
+            L.nif_query_bucketed_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None,
+                                     cnt, b.cap, occ, None, p(self.bucket[0]), side_sp)
+            L.nif_query_bucketed_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord),
+                                     p(b.inner_r), cnt + 8, b.cap, occ, None, p(self.bucket[1]),
+                                     main_sp)
+            return
+        L.nif_query_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None, cnt, b.cap,
+                        occ, None, self.impl, side_sp)
+        L.nif_query_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord), p(b.inner_r),
+                        cnt + 8, b.cap, occ, None, self.impl, main_sp)
 
     def run_range(self, s0: int, s1: int, stream=None):
         """The pass over rays [s0, s1) of the resident buffers (ray ids and
@@ -278,15 +300,10 @@ class VisibilityEngine:
         if self.model is None:
             return
         vo, vi = self._family_views()
-        p = _lib.ptr
-        cnt = b.counts.data_ptr()
         occ = self.occ.data_ptr() + s0
         main = stream if stream is not None else torch.cuda.current_stream()
         self.side.wait_stream(main)
-        L.nif_query_dev(vo, p(b.outer_obj), p(b.outer_ray), p(b.outer_coord), None, cnt,
-                        b.cap, occ, None, self.impl, self.side.cuda_stream)
-        L.nif_query_dev(vi, p(b.inner_obj), p(b.inner_ray), p(b.inner_coord), p(b.inner_r),
-                        cnt + 8, b.cap, occ, None, self.impl, sp)
+        self._query(vo, vi, occ, self.side.cuda_stream, sp)
         main.wait_stream(self.side)
 
     def occluded_host(self, ho, hd, ht, hocc, n: int, chunks: int = 4):

@@ -5,7 +5,7 @@
 Variants (nif_debug_set_query_variant): 0 production (A operand in TMEM);
 1 / 9 shared-memory-operand specialisations (6 / 4 tiles per SM); 2
 runtime-shape generic kernel; 11 TMEM operand, one tile per CTA; "S0" the
-split path (encoding kernel + MLP kernel). Logits of every variant are
+split path (encoding kernel + MLP kernel); "P" the fp32 SIMT kernel. Logits of every variant are
 compared with the generic kernel on the same records.
 """
 import ctypes as C
@@ -44,7 +44,7 @@ fams = (("outer", vo, b.outer_obj, b.outer_ray, b.outer_coord, None, b.counts.da
         ("inner", vi, b.inner_obj, b.inner_ray, b.inner_coord, b.inner_r, b.counts.data_ptr() + 8,
          counts[1]))
 ref = {}
-VARIANTS = [(v if v.startswith('S') else int(v)) for v in sys.argv[1].split(',')] if len(sys.argv) > 1 else [2, 0, 1]
+VARIANTS = [(v if v[0] in "SP" else int(v)) for v in sys.argv[1].split(',')] if len(sys.argv) > 1 else [2, 0, 1]
 if 2 not in VARIANTS:
     VARIANTS = [2] + VARIANTS
 REPS = int(sys.argv[2]) if len(sys.argv) > 2 else 30
@@ -56,7 +56,11 @@ for variant in VARIANTS:
         logits = torch.zeros(b.cap, dtype=torch.float32, device="cuda")
 
         def run(lg=None):
-            if isinstance(variant, str):
+            if variant == "P":  # the fp32 SIMT kernel (per_object / geometry path)
+                rc = L.nif_query_dev(v, obj.data_ptr(), ray.data_ptr(), c4.data_ptr(),
+                                     r.data_ptr() if r is not None else None, cnt, b.cap,
+                                     eng.occ.data_ptr(), lg, _lib.IMPL_SIMT, st.cuda_stream)
+            elif isinstance(variant, str):
                 rc = L.nif_query_split_dev(v, obj.data_ptr(), ray.data_ptr(), c4.data_ptr(),
                                            r.data_ptr() if r is not None else None, cnt, b.cap,
                                            eng.occ.data_ptr(), lg, feat.data_ptr(),
