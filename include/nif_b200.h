@@ -327,6 +327,25 @@ int nif_label_geometry_dev(const nif_scene_view* s, const int32_t* rec_obj,
                            const double* dirs, double diagonal, float* labels, uint8_t* hit,
                            void* stream);
 
+/* ---- native engine: the whole pass behind one handle ------------------
+ * (SURVEY.md §8b "nif_occluded"; replaces PredictorBackend.occluded,
+ * renderer.py:675-683, for FFI callers with rays in host memory). The
+ * engine owns the ray buffers, record queues, gather workspace and, for
+ * per_object models, the bucketing scratch, for up to `capacity` rays;
+ * scene / route / families are views of caller-owned device memory (call
+ * nif_fast_pack_dev after optimiser steps, then nif_engine_update_model).
+ * nif_engine_occluded_host: host rays in, one byte per ray out (1 =
+ * shadowed), synchronous; chunk k+1's upload overlaps chunk k's pass.   */
+typedef struct nif_engine nif_engine;
+int nif_engine_create(const nif_scene_view* scene, const uint8_t* route_dev, int32_t n_net_obj,
+                      const nif_family_view* outer, const nif_family_view* inner,
+                      int64_t capacity, nif_engine** out_engine);
+int nif_engine_update_model(nif_engine* e, const nif_family_view* outer,
+                            const nif_family_view* inner);
+int nif_engine_occluded_host(nif_engine* e, const double* origins, const double* dirs,
+                             const double* tmaxs, int64_t n, uint8_t* occ_out, int32_t chunks);
+int nif_engine_destroy(nif_engine* e);
+
 /* One progressive sample's shading (renderer.py:826-849): for the n_cast
  * shadow-cast pixels idx[k] with visibility occ[k] (1 = shadowed), adds
  * albedo[obj] / pi * emit * (vis * cos / pdf) to the fp64 HDR buffer

@@ -17,7 +17,7 @@ from .nif import (
     infer_occlusion, infer_records, logits_arrays,
 )
 from .pipeline import (
-    BvhBackend, HdrImage, NifBackend, OracleBackend, PredictorBackend, RenderConfig,
+    BvhBackend, HdrImage, NativeEngine, NifBackend, OracleBackend, PredictorBackend, RenderConfig,
     VisibilityEngine, gather_queries, label_visible, oracle_predictor, psnr, psnr_dev, render,
     render_dev, sample_pass, sample_pass_dev, shade_pass_nif, tonemap_srgb8,
 )

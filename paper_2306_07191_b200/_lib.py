@@ -146,6 +146,11 @@ _SIGS = {
     "nif_occ_init_dev": (C.c_int, [P, I64, P, P]),
     "nif_feat_scratch_bytes": (C.c_size_t, [I64]),
     "nif_bucket_scratch_bytes": (C.c_size_t, [I64, I32]),
+    "nif_engine_create": (C.c_int, [C.POINTER(SceneView), P, I32, C.POINTER(FamilyView),
+                                    C.POINTER(FamilyView), I64, C.POINTER(C.c_void_p)]),
+    "nif_engine_update_model": (C.c_int, [P, C.POINTER(FamilyView), C.POINTER(FamilyView)]),
+    "nif_engine_occluded_host": (C.c_int, [P, P, P, P, I64, P, I32]),
+    "nif_engine_destroy": (C.c_int, [P]),
     "nif_query_bucketed_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, P, P]),
     "nif_query_split_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, P, I32, P]),
     "nif_debug_set_prof": (C.c_int, [P]),

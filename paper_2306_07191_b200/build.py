@@ -22,7 +22,7 @@ BUILD = ROOT / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXACT_UNITS = ["trace.cu", "exact.cu", "gather.cu", "train.cu"]
 FAST_UNITS = ["query.cu"]
-HOST_UNITS = ["sah_builder.cpp", "api.cpp"]
+HOST_UNITS = ["sah_builder.cpp", "api.cpp", "engine.cpp"]
 
 
 def _nvcc():

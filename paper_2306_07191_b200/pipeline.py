@@ -12,6 +12,7 @@ ray count can be captured once in a CUDA graph and replayed.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import time
 from dataclasses import dataclass, field
@@ -359,6 +360,52 @@ class VisibilityEngine:
 
     def counts(self):
         return self.buf.counts.cpu().numpy()
+
+
+class NativeEngine:
+    """The whole pass behind the native engine object (nif_engine_*): host
+    rays in, per-ray answer out, one C-ABI call -- what a ctypes stub inside
+    the reference binds for PredictorBackend.occluded."""
+
+    def __init__(self, scene: Scene, model, capacity: int, hybrid_threshold=None):
+        self.scene, self.model, self.capacity = scene, model, capacity
+        self.ds = scene.device()
+        route = scene.nif_route_mask(hybrid_threshold)
+        self.route = self.ds.route(route)
+        L = _lib.lib()
+        vo = model.outer.view(with_fast=True)
+        vi = model.inner.view(with_fast=True)
+        h = C.c_void_p()
+        L.nif_engine_create(self.ds.view, _lib.ptr(self.route), int(route.sum()), vo, vi,
+                            int(capacity), C.byref(h))
+        self.handle = h
+
+    def update_model(self):
+        """After optimiser steps: repack and point the engine at the blobs."""
+        _lib.lib().nif_engine_update_model(self.handle, self.model.outer.view(with_fast=True),
+                                           self.model.inner.view(with_fast=True))
+
+    def occluded(self, rays: ShadowRays, chunks: int = 4) -> np.ndarray:
+        n = len(rays)
+        out = np.zeros(n, np.uint8)
+        if n:
+            o = np.ascontiguousarray(rays.origins, np.float64)
+            d = np.ascontiguousarray(rays.dirs, np.float64)
+            t = np.ascontiguousarray(rays.tmaxs, np.float64)
+            _lib.lib().nif_engine_occluded_host(self.handle, o.ctypes.data, d.ctypes.data,
+                                                t.ctypes.data, n, out.ctypes.data, chunks)
+        return out.astype(bool)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.lib().nif_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class NifBackend(PredictorBackend):

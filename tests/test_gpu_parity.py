@@ -203,3 +203,24 @@ def test_device_shading_matches_reference_formula(cuda):
     np.testing.assert_array_equal(img2.sum, img.sum)
     dev = render_dev(scene, BvhBackend(), spp=2).cpu().numpy()
     np.testing.assert_array_equal(dev, img.sum)
+
+
+@pytest.mark.parametrize("sharing", ["shared", "per_object"])
+def test_native_engine_matches_backend(sharing, cuda):
+    """nif_engine_* (the whole pass behind one C-ABI handle, host rays in)
+    answers exactly like NifBackend.occluded on the same model."""
+    from paper_2306_07191_b200 import NativeEngine, NifBackend, build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import sample_pass
+    from paper_2306_07191_b200.scene import ShadowRays
+    from paper_2306_07191_b200.synthetic import c2
+    scene = c2(256, 144)
+    data = sample_pass(scene, scene.camera, 0, scene.seed)
+    cast = data["hit"]
+    rays = ShadowRays(data["point"][cast], data["ldir"][cast], data["tmax"][cast])
+    model = build_model(NifConfig(seed=0, sharing=sharing), scene)
+    ref = NifBackend(model).occluded(scene, rays)
+    eng = NativeEngine(scene, model, len(rays) + 100)
+    for chunks in (1, 3):
+        np.testing.assert_array_equal(eng.occluded(rays, chunks=chunks), ref)
+    eng.close()
