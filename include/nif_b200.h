@@ -233,7 +233,8 @@ int nif_debug_gather_stats(unsigned long long* out4);
  * one tile per CTA.                                                     */
 int nif_debug_set_query_variant(int v);
 /* Training fwd/bwd kernel: 0 tiled CTA-GEMM kernel where it applies
- * (shared MLP, width a multiple of 16; default), 1 one row per thread. */
+ * (shared MLP, width a multiple of 16; 16 rows x 256 threads; default),
+ * 1 one row per thread, 2 tiled 32 x 128, 3 tiled 32 x 256.            */
 int nif_debug_set_train_variant(int v);
 
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */

@@ -510,11 +510,12 @@ __global__ void clear_counts_kernel(int32_t* counts, int n) {
 // weight gradients (32 rows instead of 128 per atomic) differ in rounding.
 // 4x more CTAs per batch and ~W/16x less serial work per thread.
 // ---------------------------------------------------------------------------
-constexpr int kRB = 32;     // rows per CTA
-constexpr int kTT = 128;    // threads per CTA
-
-template <int W>
-__global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
+// RB rows per CTA, TT threads: 16 column groups x (TT/16) row groups of
+// RPT = 16 RB / TT rows each
+template <int W, int RB, int TT>
+__global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
+  constexpr int RPT = RB * 16 / TT;
+  static_assert(RPT >= 1 && RB * 16 == RPT * TT && TT >= RB * kMaxOut, "tiling");
   constexpr int WP = W + 1;
   constexpr int CPT = W / 16;  // output columns per thread (16 column groups)
   extern __shared__ float sm[];
@@ -523,28 +524,28 @@ __global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   const int L = f.n_layers - 1;
   const int IN = f.dims[0];
   const int OUT = f.dims[f.n_layers];
-  float* zs = sm;                            // [L][kRB][WP] pre-activations
-  float* dzA = zs + (size_t)L * kRB * WP;    // [kRB][WP]
-  float* dzB = dzA + kRB * WP;               // [kRB][WP]
-  float* xs = dzB + kRB * WP;                // [kRB][kMaxIn]
-  float* dh = xs + kRB * kMaxIn;             // [kRB][kMaxOut]
-  float* sw = dh + kRB * kMaxOut;            // [max(W, IN)][W] staged weights
+  float* zs = sm;                            // [L][RB][WP] pre-activations
+  float* dzA = zs + (size_t)L * RB * WP;    // [RB][WP]
+  float* dzB = dzA + RB * WP;               // [RB][WP]
+  float* xs = dzB + RB * WP;                // [RB][kMaxIn]
+  float* dh = xs + RB * kMaxIn;             // [RB][kMaxOut]
+  float* sw = dh + RB * kMaxOut;            // [max(W, IN)][W] staged weights
   const float* Wt = f.w;
   const float* Bt = f.b;
   float* gW = a.t.grad + a.t.off_w;
   float* gB = a.t.grad + a.t.off_b;
   const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
-  const int tc = tid & 15, tr = tid >> 4;  // 16 column groups x 8 row groups of 4
+  const int tc = tid & 15, tr = tid >> 4;  // 16 column groups x TT/16 row groups of RPT
 
   // ---- encode (rows 0..31 on threads 0..31) ------------------------------
-  const int r_own = tid;  // valid only for tid < kRB
+  const int r_own = tid;  // valid only for tid < RB
   int64_t row = 0;
   bool valid = false;
   int o = 0;
   Bil64 bp{}, bd{};
   Axis ad{};
-  if (tid < kRB) {
-    const int64_t k_row = (int64_t)blockIdx.x * kRB + tid;
+  if (tid < RB) {
+    const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
     const int64_t g = a.row0 + k_row * a.row_step;
     valid = g < a.n_rows;
     row = valid ? (a.idx ? a.idx[g] : g) : 0;
@@ -589,50 +590,50 @@ __global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   for (int l = 0; l < L; ++l) {
     const int K = l == 0 ? IN : W;
     __syncthreads();  // previous layer's outputs / x visible; sw free
-    for (int e = tid; e < K * W; e += kTT) {  // sw[k][j] = W_l[j][k]
+    for (int e = tid; e < K * W; e += TT) {  // sw[k][j] = W_l[j][k]
       const int j = e / K, k = e % K;
       sw[k * W + j] = __ldg(Wt + wo + (size_t)j * K + k);
     }
     __syncthreads();
-    float acc[4][CPT];
+    float acc[RPT][CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const float bj = __ldg(Bt + bo + tc + 16 * c);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i][c] = bj;
+      for (int i = 0; i < RPT; ++i) acc[i][c] = bj;
     }
-    const float* prev = l == 0 ? xs : zs + (size_t)(l - 1) * kRB * WP;
+    const float* prev = l == 0 ? xs : zs + (size_t)(l - 1) * RB * WP;
     const int ps = l == 0 ? kMaxIn : WP;
     for (int k = 0; k < K; ++k) {
-      float av[4];
+      float av[RPT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float v = prev[(tr * 4 + i) * ps + k];
+      for (int i = 0; i < RPT; ++i) {
+        const float v = prev[(tr * RPT + i) * ps + k];
         av[i] = l == 0 ? v : leaky(v);
       }
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const float wv = sw[k * W + tc + 16 * c];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i][c] = fmaf(wv, av[i], acc[i][c]);
+        for (int i = 0; i < RPT; ++i) acc[i][c] = fmaf(wv, av[i], acc[i][c]);
       }
     }
-    float* z = zs + (size_t)l * kRB * WP;
+    float* z = zs + (size_t)l * RB * WP;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RPT; ++i)
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) z[(tr * 4 + i) * WP + tc + 16 * c] = acc[i][c];
+      for (int c = 0; c < CPT; ++c) z[(tr * RPT + i) * WP + tc + 16 * c] = acc[i][c];
     wo += (size_t)K * W;
     bo += W;
   }
   __syncthreads();
   // ---- head + loss: one (row, q) per thread --------------------------------
   const size_t wo_h = wo, bo_h = bo;
-  const float* zl = zs + (size_t)(L - 1) * kRB * WP;
+  const float* zl = zs + (size_t)(L - 1) * RB * WP;
   {
-    const int r = tid % kRB, q = tid / kRB;
+    const int r = tid % RB, q = tid / RB;
     if (q < OUT) {
-      const int64_t k_row = (int64_t)blockIdx.x * kRB + r;
+      const int64_t k_row = (int64_t)blockIdx.x * RB + r;
       const int64_t g = a.row0 + k_row * a.row_step;
       const bool v = g < a.n_rows;
       const int64_t rw = v ? (a.idx ? a.idx[g] : g) : 0;
@@ -660,21 +661,21 @@ __global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   }
   __syncthreads();
   // dZ_{L-1}[r][k] = mask * sum_q dh[r][q] Wh[q][k]
-  for (int e = tid; e < kRB * W; e += kTT) {
+  for (int e = tid; e < RB * W; e += TT) {
     const int r = e / W, k = e % W;
     float da = 0.f;
     for (int q = 0; q < OUT; ++q) da = fmaf(dh[r * kMaxOut + q], __ldg(Wt + wo_h + q * W + k), da);
     dzA[r * WP + k] = zl[r * WP + k] > 0.f ? da : da * kSlope;
   }
   // head gradients
-  for (int e = tid; e < OUT * (W + 1); e += kTT) {
+  for (int e = tid; e < OUT * (W + 1); e += TT) {
     const int q = e / (W + 1), k = e % (W + 1);
     float s = 0.f;
     if (k < W) {
-      for (int r = 0; r < kRB; ++r) s = fmaf(dh[r * kMaxOut + q], leaky(zl[r * WP + k]), s);
+      for (int r = 0; r < RB; ++r) s = fmaf(dh[r * kMaxOut + q], leaky(zl[r * WP + k]), s);
       atomicAdd(gW + wo_h + q * W + k, s);
     } else {
-      for (int r = 0; r < kRB; ++r) s += dh[r * kMaxOut + q];
+      for (int r = 0; r < RB; ++r) s += dh[r * kMaxOut + q];
       atomicAdd(gB + bo_h + q, s);
     }
   }
@@ -684,43 +685,43 @@ __global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   for (int l = L - 1; l >= 1; --l) {
     wo -= (size_t)W * W;
     bo -= W;
-    const float* zp = zs + (size_t)(l - 1) * kRB * WP;
+    const float* zp = zs + (size_t)(l - 1) * RB * WP;
     // weight grads of dense layer l
-    for (int e = tid; e < W * (W + 1); e += kTT) {
+    for (int e = tid; e < W * (W + 1); e += TT) {
       const int j = e / (W + 1), k = e % (W + 1);
       float s = 0.f;
       if (k < W) {
-        for (int r = 0; r < kRB; ++r) s = fmaf(dzc[r * WP + j], leaky(zp[r * WP + k]), s);
+        for (int r = 0; r < RB; ++r) s = fmaf(dzc[r * WP + j], leaky(zp[r * WP + k]), s);
         atomicAdd(gW + wo + (size_t)j * W + k, s);
       } else {
-        for (int r = 0; r < kRB; ++r) s += dzc[r * WP + j];
+        for (int r = 0; r < RB; ++r) s += dzc[r * WP + j];
         atomicAdd(gB + bo + j, s);
       }
     }
     // stage W_l natural [j][k], then dZ_{l-1} = mask . (dZ_l W_l), j ascending
-    for (int e = tid; e < W * W; e += kTT) sw[e] = __ldg(Wt + wo + e);
+    for (int e = tid; e < W * W; e += TT) sw[e] = __ldg(Wt + wo + e);
     __syncthreads();
-    float acc[4][CPT];
+    float acc[RPT][CPT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RPT; ++i)
 #pragma unroll
       for (int c = 0; c < CPT; ++c) acc[i][c] = 0.f;
     for (int j = 0; j < W; ++j) {
-      float dv[4];
+      float dv[RPT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dv[i] = dzc[(tr * 4 + i) * WP + j];
+      for (int i = 0; i < RPT; ++i) dv[i] = dzc[(tr * RPT + i) * WP + j];
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const float wv = sw[j * W + tc + 16 * c];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i][c] = fmaf(dv[i], wv, acc[i][c]);
+        for (int i = 0; i < RPT; ++i) acc[i][c] = fmaf(dv[i], wv, acc[i][c]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RPT; ++i)
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        const int r = tr * 4 + i, k = tc + 16 * c;
+        const int r = tr * RPT + i, k = tc + 16 * c;
         dzn[r * WP + k] = zp[r * WP + k] > 0.f ? acc[i][c] : acc[i][c] * kSlope;
       }
     __syncthreads();
@@ -729,18 +730,18 @@ __global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     dzn = tmp;
   }
   // layer 0 weight grads
-  for (int e = tid; e < W * (IN + 1); e += kTT) {
+  for (int e = tid; e < W * (IN + 1); e += TT) {
     const int j = e / (IN + 1), k = e % (IN + 1);
     float s = 0.f;
     if (k < IN) {
-      for (int r = 0; r < kRB; ++r) s = fmaf(dzc[r * WP + j], xs[r * kMaxIn + k], s);
+      for (int r = 0; r < RB; ++r) s = fmaf(dzc[r * WP + j], xs[r * kMaxIn + k], s);
       atomicAdd(gW + (size_t)j * IN + k, s);
     } else {
-      for (int r = 0; r < kRB; ++r) s += dzc[r * WP + j];
+      for (int r = 0; r < RB; ++r) s += dzc[r * WP + j];
       atomicAdd(gB + j, s);
     }
   }
-  if (tid >= kRB || !valid) return;
+  if (tid >= RB || !valid) return;
   // dx = dZ_0 W_0 -> grid scatter (grids.py:171-202)
   float dx[kMaxIn];
   for (int k = 0; k < IN; ++k) {
@@ -768,20 +769,30 @@ __global__ void __launch_bounds__(kTT) train_fwdbwd_tiled_kernel(TrainArgs a) {
 
 int g_train_variant = 0;  // 0 tiled where it applies, 1 per-row kernel (nif_debug_set_train_variant)
 
-template <int W>
-int launch_fwdbwd_tiled(const TrainArgs& a, cudaStream_t st) {
+template <int W, int RB, int TT>
+int launch_fwdbwd_tiled_rb(const TrainArgs& a, cudaStream_t st) {
   const int L = a.f.n_layers - 1;
   const int K = a.f.dims[0] > W ? a.f.dims[0] : W;
-  const size_t smem = ((size_t)L * kRB * (W + 1) + 2 * (size_t)kRB * (W + 1) +
-                       (size_t)kRB * kMaxIn + (size_t)kRB * kMaxOut + (size_t)K * W) *
+  const size_t smem = ((size_t)L * RB * (W + 1) + 2 * (size_t)RB * (W + 1) +
+                       (size_t)RB * kMaxIn + (size_t)RB * kMaxOut + (size_t)K * W) *
                       sizeof(float);
-  auto kern = train_fwdbwd_tiled_kernel<W>;
+  auto kern = train_fwdbwd_tiled_kernel<W, RB, TT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
   if (my_rows <= 0) return NIF_OK;
-  const unsigned grid = (unsigned)((my_rows + kRB - 1) / kRB);
-  kern<<<grid, kTT, smem, st>>>(a);
+  const unsigned grid = (unsigned)((my_rows + RB - 1) / RB);
+  kern<<<grid, TT, smem, st>>>(a);
   return check_launch("nif_train_fwdbwd_dev(tiled)");
+}
+
+// 16 rows x 256 threads (one row per thread-row): twice the CTAs and eight
+// warps each, against the latency of the small per-layer GEMMs
+// (nif_debug_set_train_variant 2 selects the 32-row / 128-thread tiling)
+template <int W>
+int launch_fwdbwd_tiled(const TrainArgs& a, cudaStream_t st) {
+  if (g_train_variant == 2) return launch_fwdbwd_tiled_rb<W, 32, 128>(a, st);
+  if (g_train_variant == 3) return launch_fwdbwd_tiled_rb<W, 32, 256>(a, st);
+  return launch_fwdbwd_tiled_rb<W, 16, 256>(a, st);
 }
 
 template <int W>
@@ -831,7 +842,7 @@ extern "C" int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_vi
   if (row_step < 1 || row0 < 0) return fail(NIF_ERR_VALUE, "bad row partition");
   TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err};
   cudaStream_t st = (cudaStream_t)stream;
-  if (g_train_variant == 0 && f->n_heads == 1) {
+  if (g_train_variant != 1 && f->n_heads == 1) {
     switch (f->dims[1]) {
       case 16: return launch_fwdbwd_tiled<16>(a, st);
       case 32: return launch_fwdbwd_tiled<32>(a, st);
