@@ -1,0 +1,47 @@
+"""Small end-to-end exercise of every device path for compute-sanitizer
+(tools/gpu_sanitize.sh): ordered + unordered gather, labels, sample
+collection, one training epoch (tiled fwd/bwd, per-head per-row kernel,
+unit-major Adam), fused / split / bucketed (per_object) queries, the native
+engine and device shading."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2306_07191_b200 import (BvhBackend, NativeEngine, NifBackend, RenderConfig,  # noqa: E402
+                                   build_model, render)
+from paper_2306_07191_b200.nif import NifConfig, query_family  # noqa: E402
+from paper_2306_07191_b200.pipeline import sample_pass  # noqa: E402
+from paper_2306_07191_b200.scene import ShadowRays  # noqa: E402
+from paper_2306_07191_b200.synthetic import c1, lattice  # noqa: E402
+from paper_2306_07191_b200.train import collect_samples, train  # noqa: E402
+
+torch.cuda.set_device(0)
+scene = lattice(3, 2, 0.35, 48, 32)
+for sharing in ("shared", "per_object"):
+    cfg = NifConfig(seed=0, sharing=sharing)
+    cfg.outer.grid_resolution = 32
+    cfg.inner.grid_resolution = 16
+    model = build_model(cfg, scene)
+    smp = collect_samples(scene, spp=1, seed=scene.seed)
+    train(model, smp, epochs=1)
+    data = sample_pass(scene, scene.camera, 0, scene.seed)
+    rays = ShadowRays(data["point"][data["hit"]], data["ldir"][data["hit"]],
+                      data["tmax"][data["hit"]])
+    occ = NifBackend(model).occluded(scene, rays)
+    eng = NativeEngine(scene, model, len(rays))
+    assert np.array_equal(eng.occluded(rays, chunks=2), occ)
+    eng.close()
+    rng = np.random.default_rng(0)
+    o = rng.integers(0, scene.n_objects, 300)
+    c = rng.random((300, 5))
+    for fam, w in (("outer", 4), ("inner", 5)):
+        query_family(model, fam, o, c[:, :w])
+        if sharing == "shared":
+            query_family(model, fam, o, c[:, :w], split=True)
+render(c1(32, 24, subdiv=2), config=RenderConfig(spp=1), backend=BvhBackend())
+torch.cuda.synchronize()
+print("sanitize paths ok")
