@@ -369,6 +369,14 @@ struct EncIn {
   bool valid;
 };
 
+// 32-byte read-only load (LDG.256 on sm_100) of an aligned entry
+__device__ __forceinline__ void ldg256(const uint4* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                 "=r"(b.w)
+               : "l"(p));
+}
+
 // bilinear entry of the corner-packed table: (u cell) x (v cell + 1)
 struct BilQ {
   int q;
@@ -448,15 +456,13 @@ __device__ __forceinline__ void issue_enc(EncIn<N, ND>& e, const RecIn& r, const
   e.ray = r.ray;
   e.rec = r.rec;
   if (!r.valid) return;
-  if constexpr (NP == 4) {  // corner-packed entries
+  if constexpr (NP == 4) {  // corner-packed 32 B entries: one 256-bit load each
     const size_t g2 = (size_t)R * (R + 1) * NQ;  // uint4 per object table
     const BilQ bp = bilinear_q(r.c.x, r.c.y, R), bd = bilinear_q(r.c.z, r.c.w, R);
     const uint4* P = reinterpret_cast<const uint4*>(tpos) + (size_t)r.obj * g2 + (size_t)bp.q * NQ;
     const uint4* D = reinterpret_cast<const uint4*>(tdir) + (size_t)r.obj * g2 + (size_t)bd.q * NQ;
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) e.qp[i] = __ldg(P + i);
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) e.qd[i] = __ldg(D + i);
+    ldg256(P, e.qp[0], e.qp[1]);
+    ldg256(D, e.qd[0], e.qd[1]);
     e.wp[0] = bp.w00; e.wp[1] = bp.w01; e.wp[2] = bp.w10; e.wp[3] = bp.w11;
     e.wd[0] = bd.w00; e.wd[1] = bd.w01; e.wd[2] = bd.w10; e.wd[3] = bd.w11;
   } else {  // one 16 B cell per corner
