@@ -273,6 +273,17 @@ int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_view* t, cons
                          int64_t n_rows, int64_t row0, int64_t row_step, double* sq_err,
                          void* stream);
 
+/* Graph-replayable variants: the batch's rows start at idx + *cursor
+ * (cursor: device int64), advanced on the device by nif_cursor_advance_dev,
+ * so one captured optimiser step is replayed for every full batch.      */
+int nif_batch_counts_cur_dev(const int64_t* obj, const int64_t* idx, const int64_t* cursor,
+                             int64_t n_rows, int32_t n_obj, int32_t* counts, void* stream);
+int nif_train_fwdbwd_cur_dev(const nif_family_view* f, const nif_train_view* t,
+                             const int64_t* obj, const double* coord, const float* label,
+                             const int64_t* idx, const int64_t* cursor, int64_t n_rows,
+                             int64_t row0, int64_t row_step, double* sq_err, void* stream);
+int nif_cursor_advance_dev(int64_t* cursor, int64_t delta, void* stream);
+
 /* Adam (grids.py:31-45) on every touched object's grids (dense, all
  * cells) and on each touched MLP head; fp64 moments over fp32 storage,
  * numba's integer power for the bias correction; clears the gradients of

@@ -159,6 +159,10 @@ _SIGS = {
     "nif_debug_set_query_variant": (C.c_int, [C.c_int]),
     "nif_debug_set_train_variant": (C.c_int, [C.c_int]),
     "nif_batch_counts_dev": (C.c_int, [P, P, I64, I32, P, P]),
+    "nif_batch_counts_cur_dev": (C.c_int, [P, P, P, I64, I32, P, P]),
+    "nif_train_fwdbwd_cur_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P,
+                                           P, P, I64, I64, I64, P, P]),
+    "nif_cursor_advance_dev": (C.c_int, [P, I64, P]),
     "nif_train_fwdbwd_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
                                        I64, I64, I64, P, P]),
     "nif_adam_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), D, D, D, D, P]),

@@ -83,7 +83,14 @@ struct TrainArgs {
   const int64_t* idx;
   int64_t n_rows, row0, row_step;
   double* sq_err;
+  const int64_t* cursor;  // device row offset added to idx (graph-replayed steps), or NULL
 };
+
+// idx + *cursor: a CUDA graph of one optimiser step is replayed per batch
+// while the batch start lives on the device
+__device__ __forceinline__ const int64_t* batch_idx(const int64_t* idx, const int64_t* cursor) {
+  return (idx != nullptr && cursor != nullptr) ? idx + *cursor : idx;
+}
 
 template <int W>
 __global__ void train_fwdbwd_kernel(TrainArgs a) {
@@ -109,7 +116,8 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
   const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
   const int64_t g = a.row0 + k_row * a.row_step;
   const bool valid = k_row * a.row_step + a.row0 < a.n_rows && g < a.n_rows;
-  const int64_t row = valid ? (a.idx ? a.idx[g] : g) : 0;
+  const int64_t* bidx = batch_idx(a.idx, a.cursor);
+  const int64_t row = valid ? (bidx ? bidx[g] : g) : 0;
   const int o = valid ? (int)a.obj[row] : 0;
   const int head = f.n_heads > 1 ? o : 0;
   s_rhead[tid] = valid ? head : -1;
@@ -342,9 +350,11 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
 }
 
 __global__ void batch_counts_kernel(const int64_t* __restrict__ obj, const int64_t* __restrict__ idx,
-                                    int64_t n, int n_obj, int32_t* __restrict__ counts) {
+                                    int64_t n, int n_obj, int32_t* __restrict__ counts,
+                                    const int64_t* __restrict__ cursor) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
+  idx = batch_idx(idx, cursor);
   const int64_t o = obj[idx ? idx[r] : r];
   if (o >= 0 && o < n_obj) atomicAdd(counts + o, 1);
 }
@@ -548,7 +558,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
     const int64_t g = a.row0 + k_row * a.row_step;
     valid = g < a.n_rows;
-    row = valid ? (a.idx ? a.idx[g] : g) : 0;
+    const int64_t* bidx = batch_idx(a.idx, a.cursor);
+    row = valid ? (bidx ? bidx[g] : g) : 0;
     o = valid ? (int)a.obj[row] : 0;
     float x[kMaxIn];
 #pragma unroll
@@ -636,7 +647,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       const int64_t k_row = (int64_t)blockIdx.x * RB + r;
       const int64_t g = a.row0 + k_row * a.row_step;
       const bool v = g < a.n_rows;
-      const int64_t rw = v ? (a.idx ? a.idx[g] : g) : 0;
+      const int64_t* bidx = batch_idx(a.idx, a.cursor);
+      const int64_t rw = v ? (bidx ? bidx[g] : g) : 0;
       const int ob = v ? (int)a.obj[rw] : 0;
       float acc = __ldg(Bt + bo_h + q);
       const float* wr = Wt + wo_h + (size_t)q * W;
@@ -820,19 +832,47 @@ int launch_fwdbwd(const TrainArgs& a, cudaStream_t st) {
 
 using namespace nif;
 
-extern "C" int nif_batch_counts_dev(const int64_t* obj, const int64_t* idx, int64_t n_rows,
-                                    int32_t n_obj, int32_t* counts, void* stream) {
+__global__ void cursor_advance_kernel(int64_t* cursor, int64_t delta) { *cursor += delta; }
+
+extern "C" int nif_batch_counts_cur_dev(const int64_t* obj, const int64_t* idx,
+                                        const int64_t* cursor, int64_t n_rows, int32_t n_obj,
+                                        int32_t* counts, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_rows <= 0) return NIF_OK;
   batch_counts_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(obj, idx, n_rows, n_obj,
-                                                                        counts);
+                                                                        counts, cursor);
   return check_launch("nif_batch_counts_dev");
 }
+
+extern "C" int nif_batch_counts_dev(const int64_t* obj, const int64_t* idx, int64_t n_rows,
+                                    int32_t n_obj, int32_t* counts, void* stream) {
+  return nif_batch_counts_cur_dev(obj, idx, nullptr, n_rows, n_obj, counts, stream);
+}
+
+extern "C" int nif_cursor_advance_dev(int64_t* cursor, int64_t delta, void* stream) {
+  cursor_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(cursor, delta);
+  return check_launch("nif_cursor_advance_dev");
+}
+
+extern "C" int nif_train_fwdbwd_cur_dev(const nif_family_view* f, const nif_train_view* t,
+                                        const int64_t* obj, const double* coord,
+                                        const float* label, const int64_t* idx,
+                                        const int64_t* cursor, int64_t n_rows, int64_t row0,
+                                        int64_t row_step, double* sq_err, void* stream);
 
 extern "C" int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_view* t,
                                     const int64_t* obj, const double* coord, const float* label,
                                     const int64_t* idx, int64_t n_rows, int64_t row0,
                                     int64_t row_step, double* sq_err, void* stream) {
+  return nif_train_fwdbwd_cur_dev(f, t, obj, coord, label, idx, nullptr, n_rows, row0, row_step,
+                                  sq_err, stream);
+}
+
+extern "C" int nif_train_fwdbwd_cur_dev(const nif_family_view* f, const nif_train_view* t,
+                                        const int64_t* obj, const double* coord,
+                                        const float* label, const int64_t* idx,
+                                        const int64_t* cursor, int64_t n_rows, int64_t row0,
+                                        int64_t row_step, double* sq_err, void* stream) {
   if (n_rows <= 0) return NIF_OK;
   if (f->n_layers < 2) return fail(NIF_ERR_UNSUPPORTED, "training needs at least one hidden layer");
   if (f->dims[0] > kMaxIn) return fail(NIF_ERR_UNSUPPORTED, "input width above %d", kMaxIn);
@@ -840,7 +880,7 @@ extern "C" int nif_train_fwdbwd_dev(const nif_family_view* f, const nif_train_vi
   for (int i = 2; i < f->n_layers; ++i)
     if (f->dims[i] != f->dims[1]) return fail(NIF_ERR_UNSUPPORTED, "hidden widths must match");
   if (row_step < 1 || row0 < 0) return fail(NIF_ERR_VALUE, "bad row partition");
-  TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err};
+  TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err, cursor};
   cudaStream_t st = (cudaStream_t)stream;
   if (g_train_variant != 1 && f->n_heads == 1) {
     switch (f->dims[1]) {

@@ -229,6 +229,61 @@ class _Step:
         fam.dirty = True
 
 
+class _GraphStep:
+    """One family's optimiser step captured as a CUDA graph and replayed
+    for every full batch of an epoch: the batch start lives on the device
+    (a cursor into a persistent permutation buffer, advanced by the graph
+    itself), so an epoch is one H2D copy of the permutation plus one graph
+    launch per batch -- no per-step host work."""
+
+    def __init__(self, step: "_Step", obj, coord, label, n: int, bs: int):
+        torch = _torch()
+        self.step, self.bs = step, bs
+        dev = step.model.device
+        self.perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        self.cursor = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.obj, self.coord, self.label = obj, coord, label
+        self.graph = None
+
+    def _enqueue(self, n_rows: int, advance: bool):
+        L = _lib.lib()
+        st, fam, model = self.step, self.step.fam, self.step.model
+        p = _lib.ptr
+        sp = _lib.stream_ptr()
+        L.nif_batch_counts_cur_dev(p(self.obj), p(self.perm), p(self.cursor), n_rows, fam.n_obj,
+                                   p(fam.counts), sp)
+        L.nif_train_fwdbwd_cur_dev(st.fv, st.tv, p(self.obj), p(self.coord), p(self.label),
+                                   p(self.perm), p(self.cursor), n_rows, 0, 1, p(st.sq), sp)
+        a = model.config.adam
+        L.nif_adam_dev(st.fv, st.tv, model.learning_rate, a.beta1, a.beta2, a.epsilon, sp)
+        if advance:
+            L.nif_cursor_advance_dev(p(self.cursor), n_rows, sp)
+
+    def epoch(self, perm_host: np.ndarray):
+        torch = _torch()
+        n = len(perm_host)
+        self.perm[:n].copy_(torch.from_numpy(perm_host))
+        self.cursor.zero_()
+        n_full = n // self.bs
+        if n_full and self.graph is None:
+            s = torch.cuda.Stream(device=self.perm.device)
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            # capture_begin/end directly: the torch.cuda.graph context manager
+            # runs gc.collect() + empty_cache() first (~100 ms per capture)
+            with torch.cuda.stream(s):
+                g.capture_begin()
+                self._enqueue(self.bs, True)
+                g.capture_end()
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = g
+        for _ in range(n_full):
+            self.graph.replay()
+        if n - n_full * self.bs:
+            self._enqueue(n - n_full * self.bs, False)
+        self.step.fam.dirty = True
+
+
 def train_batch(model: NifModel, which: str, obj, coord, label) -> float:
     """nif.py:682-749 _train_batch with host arrays; returns the batch mean
     loss (sum of squared errors / rows)."""
@@ -280,6 +335,9 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     bo = model.config.outer.batch_size
     bi = model.config.inner.batch_size
     steps = {"outer": _Step(model, "outer"), "inner": _Step(model, "inner")}
+    # single GPU: every full batch is a replay of one captured step
+    use_graph = world == 1 and model.device.type == "cuda"
+    gsteps = {}
     fams = ((0, bo, "outer", samples.outer_obj, samples.outer_coord, samples.outer_label),
             (1, bi, "inner", samples.inner_obj, samples.inner_coord, samples.inner_label))
     for e in range(epochs):
@@ -290,13 +348,19 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
             n = int(obj.shape[0])
             if n == 0:
                 continue
-            perm = torch.from_numpy(rng.permutation(n)).to(model.device)
+            perm_np = rng.permutation(n)
             st = steps[which]
             st.sq.zero_()
-            base = perm.data_ptr()
-            for k in range(0, n, bs):
-                m = min(bs, n - k)
-                st.run(obj, coord, label, None, m, rank, world, group, idx_ptr=base + 8 * k)
+            if use_graph:
+                if which not in gsteps:
+                    gsteps[which] = _GraphStep(st, obj, coord, label, n, bs)
+                gsteps[which].epoch(perm_np)
+            else:
+                perm = torch.from_numpy(perm_np).to(model.device)
+                base = perm.data_ptr()
+                for k in range(0, n, bs):
+                    m = min(bs, n - k)
+                    st.run(obj, coord, label, None, m, rank, world, group, idx_ptr=base + 8 * k)
             # the reference's per-batch loss is the mean over rows x outputs
             width = int(label.shape[1]) if label.dim() > 1 else 1
             sums[fam] = float(st.sq.item()) / width

@@ -34,3 +34,8 @@ torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 print(f"variant {variant}  samples {samples.n_outer}+{samples.n_inner}  steps {steps}  {dt:.3f} s  "
       f"{steps / dt:.0f} steps/s  {dt / steps * 1e6:.1f} us/step  loss {curve[-1]}")
+t0 = time.perf_counter()
+curve = train(model, samples, epochs=5)
+torch.cuda.synchronize()
+dt = time.perf_counter() - t0
+print(f"5 epochs: {5 * steps / dt:.0f} steps/s  {dt / (5 * steps) * 1e6:.1f} us/step")
