@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-EXACT_UNITS = ["trace.cu", "exact.cu", "gather.cu", "train.cu"]
+EXACT_UNITS = ["trace.cu", "exact.cu", "gather.cu", "train.cu", "sah_gpu.cu"]
 FAST_UNITS = ["query.cu"]
 HOST_UNITS = ["sah_builder.cpp", "api.cpp", "engine.cpp"]
 

@@ -96,6 +96,34 @@ def _build_sah(lo, hi, ce, max_leaf):
             node_b[:k].copy(), node_leaf[:k].copy(), order)
 
 
+def build_sah_dev(lo, hi, ce, max_leaf=MAX_LEAF, stream=None):
+    """_build_sah on the GPU (nif_build_sah_dev): lo/hi/ce are [n, 3] float64
+    CUDA tensors; returns (node_lo, node_hi, node_a, node_b, node_leaf, order)
+    as CUDA tensors, identical to the host build."""
+    import torch
+    n = lo.shape[0]
+    if n == 0:
+        raise ValueError("cannot build a tree over zero primitives")
+    dev = lo.device
+    lo, hi, ce = (t.to(torch.float64).contiguous() for t in (lo, hi, ce))
+    cap = 2 * n
+    node_lo = torch.empty((cap, 3), dtype=torch.float64, device=dev)
+    node_hi = torch.empty((cap, 3), dtype=torch.float64, device=dev)
+    node_a = torch.zeros(cap, dtype=torch.int64, device=dev)
+    node_b = torch.zeros(cap, dtype=torch.int64, device=dev)
+    node_leaf = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    order = torch.empty(n, dtype=torch.int64, device=dev)
+    n_nodes = C.c_int64(0)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _lib.lib().nif_build_sah_dev(
+        lo.data_ptr(), hi.data_ptr(), ce.data_ptr(), n, max_leaf, N_BINS,
+        COST_TRAVERSAL, COST_INTERSECT, node_lo.data_ptr(), node_hi.data_ptr(),
+        node_a.data_ptr(), node_b.data_ptr(), node_leaf.data_ptr(), order.data_ptr(),
+        C.byref(n_nodes), C.c_void_p(st.cuda_stream))
+    k = n_nodes.value
+    return node_lo[:k], node_hi[:k], node_a[:k], node_b[:k], node_leaf[:k], order
+
+
 class _FlatBvh:
     def __init__(self, node_lo, node_hi, node_a, node_b, node_leaf, order):
         self.node_lo = node_lo
