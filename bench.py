@@ -135,13 +135,15 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def build_workload(args, rank):
+def build_workload(args, rank, build_device=None):
     from paper_2306_07191_b200 import synthetic
     if args.config == "c1":
         return synthetic.c1(min(args.width, 256), min(args.height, 256))
+    # scene setup (untimed); build_device: per-object SAH builds on the GPU
+    # (identical trees) -- the reference arm keeps the host builder
     if args.config == "c3":
-        return synthetic.c3(args.width, args.height)
-    return synthetic.c2(args.width, args.height)
+        return synthetic.c3(args.width, args.height, build_device=build_device)
+    return synthetic.c2(args.width, args.height, build_device=build_device)
 
 
 def cpu_path_step(scene, model, rays_np, n):
@@ -265,7 +267,7 @@ def main():
     from paper_2306_07191_b200.pipeline import (VisibilityEngine, sample_pass_dev,
                                                 shadow_rays_dev)
     dev = torch.device("cuda", torch.cuda.current_device())
-    scene = build_workload(args, rank)
+    scene = build_workload(args, rank, build_device=dev)
     data = sample_pass_dev(scene, scene.camera, rank, scene.seed)
     _, o, d, t = shadow_rays_dev(data, require_emit=False)
     n = int(t.numel())

@@ -77,17 +77,20 @@ int nif_build_sah(const double* lo, const double* hi, const double* ce, int64_t 
                   double* node_lo, double* node_hi, int64_t* node_a, int64_t* node_b,
                   uint8_t* node_leaf, int64_t* order, int64_t* n_nodes_out);
 
-/* The same build on the GPU (level-synchronous, one CTA per node of a tree
- * level), node-for-node identical to nif_build_sah / bvh.py:34-303:
- * lo/hi/ce and every output are DEVICE arrays (outputs sized for 2n nodes),
- * n_nodes_out is host memory. Synchronises `stream` (one host round trip per
+/* The same build on the GPU (level-synchronous; a warp, a CTA or a chunked
+ * multi-CTA pass per node by segment size), node-for-node identical to
+ * nif_build_sah / bvh.py:34-303: lo/hi/ce and every output are DEVICE
+ * arrays (outputs sized for 2n nodes), n_nodes_out is host memory.
+ * workspace: nif_build_sah_workspace_bytes(n) bytes of device memory, or
+ * NULL to allocate per call. Synchronises `stream` (one host round trip per
  * tree level). Serves build_bottom / build_top (bvh.py:400-437) when the
  * primitive bounds are already resident. */
+size_t nif_build_sah_workspace_bytes(int64_t n);
 int nif_build_sah_dev(const double* lo, const double* hi, const double* ce, int64_t n,
                       int64_t max_leaf, int64_t n_bins, double c_trav, double c_isect,
                       double* node_lo, double* node_hi, int64_t* node_a, int64_t* node_b,
                       uint8_t* node_leaf, int64_t* order, int64_t* n_nodes_out,
-                      void* stream);
+                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- phase 1: gather (bvh.py:772-901 _k_gather_queries,
  *                       renderer.py:613-644 gather_queries) --------------

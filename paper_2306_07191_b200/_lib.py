@@ -133,7 +133,9 @@ _SIGS = {
     "nif_abi_version": (C.c_int, []),
     "nif_device_check": (C.c_int, [C.c_int]),
     "nif_build_sah": (C.c_int, [P, P, P, I64, I64, I64, D, D, P, P, P, P, P, P, P]),
-    "nif_build_sah_dev": (C.c_int, [P, P, P, I64, I64, I64, D, D, P, P, P, P, P, P, P, P]),
+    "nif_build_sah_workspace_bytes": (C.c_size_t, [I64]),
+    "nif_build_sah_dev": (C.c_int, [P, P, P, I64, I64, I64, D, D, P, P, P, P, P, P, P, P,
+                                    C.c_size_t, P]),
     "nif_gather_workspace_bytes": (C.c_size_t, [I64]),
     "nif_gather_dev": (C.c_int, [C.POINTER(SceneView), P, P, P, P, I64,
                                  C.POINTER(GatherOut), P, C.c_size_t, P]),

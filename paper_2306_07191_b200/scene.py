@@ -115,11 +115,13 @@ def build_sah_dev(lo, hi, ce, max_leaf=MAX_LEAF, stream=None):
     order = torch.empty(n, dtype=torch.int64, device=dev)
     n_nodes = C.c_int64(0)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
+    ws_bytes = _lib.lib().nif_build_sah_workspace_bytes(n)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     _lib.lib().nif_build_sah_dev(
         lo.data_ptr(), hi.data_ptr(), ce.data_ptr(), n, max_leaf, N_BINS,
         COST_TRAVERSAL, COST_INTERSECT, node_lo.data_ptr(), node_hi.data_ptr(),
         node_a.data_ptr(), node_b.data_ptr(), node_leaf.data_ptr(), order.data_ptr(),
-        C.byref(n_nodes), C.c_void_p(st.cuda_stream))
+        C.byref(n_nodes), ws.data_ptr(), ws_bytes, C.c_void_p(st.cuda_stream))
     k = n_nodes.value
     return node_lo[:k], node_hi[:k], node_a[:k], node_b[:k], node_leaf[:k], order
 
@@ -138,15 +140,14 @@ class _FlatBvh:
         return len(self.node_a)
 
     def depth(self) -> int:
-        best = 0
-        stack = [(0, 1)]
-        while stack:
-            i, d = stack.pop()
-            best = max(best, d)
-            if not self.node_leaf[i]:
-                stack.append((int(self.node_a[i]), d + 1))
-                stack.append((int(self.node_b[i]), d + 1))
-        return best
+        """bvh.py:337-346 depth, computed one frontier per level."""
+        frontier = np.zeros(1, np.int64)
+        d = 0
+        while frontier.size:
+            d += 1
+            inner = frontier[self.node_leaf[frontier] == 0]
+            frontier = np.concatenate((self.node_a[inner], self.node_b[inner]))
+        return d
 
 
 class BottomLevelBvh(_FlatBvh):
@@ -168,16 +169,22 @@ class TopLevelBvh(_FlatBvh):
     pass
 
 
-def build_bottom(arrays) -> BottomLevelBvh:
+def build_bottom(arrays, device=None) -> BottomLevelBvh:
     """bvh.py:402-428: tree over one object's triangles from
-    (v0, v1, v2, n0, n1, n2) arrays."""
+    (v0, v1, v2, n0, n1, n2) arrays. With a CUDA ``device`` the SAH build
+    runs there (nif_build_sah_dev, the identical tree)."""
     v0, v1, v2, n0, n1, n2 = (np.ascontiguousarray(a, np.float64) for a in arrays)
     if len(v0) == 0:
         raise ValueError("cannot build a tree over zero triangles")
     lo = np.minimum(np.minimum(v0, v1), v2)
     hi = np.maximum(np.maximum(v0, v1), v2)
     ce = (lo + hi) * 0.5
-    *nodes, order = _build_sah(lo, hi, ce, MAX_LEAF)
+    if device is None:
+        *nodes, order = _build_sah(lo, hi, ce, MAX_LEAF)
+    else:
+        import torch
+        t = [torch.from_numpy(x).to(device) for x in (lo, hi, ce)]
+        *nodes, order = (x.cpu().numpy() for x in build_sah_dev(*t, max_leaf=MAX_LEAF))
     bvh = BottomLevelBvh(tuple(nodes), order, v0[order].copy(), v1[order].copy(),
                          v2[order].copy(), n0[order].copy(), n1[order].copy(),
                          n2[order].copy(), order.copy())
@@ -186,11 +193,14 @@ def build_bottom(arrays) -> BottomLevelBvh:
     return bvh
 
 
-def build_bottoms(arrays_list, workers: Optional[int] = None):
-    """build_bottom over many objects on host threads (the native builder
-    and numpy release the GIL); trees are identical to sequential builds."""
+def build_bottoms(arrays_list, workers: Optional[int] = None, device=None):
+    """build_bottom over many objects: on host threads (the native builder
+    and numpy release the GIL), or one after another on a CUDA ``device``;
+    trees are identical to sequential host builds."""
     from concurrent.futures import ThreadPoolExecutor
     arrays_list = list(arrays_list)
+    if device is not None:
+        return [build_bottom(a, device) for a in arrays_list]
     if workers is None:
         workers = min(len(arrays_list), os.cpu_count() or 1)
     if workers <= 1 or len(arrays_list) <= 1:

@@ -34,7 +34,7 @@ def c1(width=256, height=256, subdiv=5, plane_nif=False) -> Scene:
 
 
 def lattice(n_spheres: int, subdiv: int, radius: float, width=1920, height=1080,
-            cols: int = 4) -> Scene:
+            cols: int = 4, build_device=None) -> Scene:
     base = meshgen.mesh_arrays(*meshgen.icosphere(subdiv, radius))
     rows = (n_spheres + cols - 1) // cols
     pitch = 1.2 if n_spheres <= 12 else 3.6 / max(cols - 1, 1)
@@ -44,8 +44,9 @@ def lattice(n_spheres: int, subdiv: int, radius: float, width=1920, height=1080,
         y = -0.6 + 1.2 * (k // cols) - (0.6 * (rows - 3) if rows > 3 else 0.0)
         arrays.append(meshgen.transformed(base, 1.0, (x, y, radius)))
     arrays.append(meshgen.mesh_arrays(*meshgen.ground_plane(4.0)))
-    # the per-object trees are independent: build them on all host cores
-    trees = build_bottoms(arrays)
+    # the per-object trees are independent: build them on all host cores, or
+    # on the GPU (identical trees)
+    trees = build_bottoms(arrays, device=build_device)
     objs = [SceneObject(f"sphere{k}", trees[k], np.asarray((0.75, 0.33, 0.27), np.float64), True)
             for k in range(n_spheres)]
     objs.append(SceneObject("plane", trees[-1], np.asarray((0.62, 0.62, 0.6), np.float64), True))
@@ -54,12 +55,12 @@ def lattice(n_spheres: int, subdiv: int, radius: float, width=1920, height=1080,
     return Scene(objs, [LIGHT], cam, 11)
 
 
-def c2(width=1920, height=1080) -> Scene:
-    return lattice(12, 6, 0.35, width, height)
+def c2(width=1920, height=1080, build_device=None) -> Scene:
+    return lattice(12, 6, 0.35, width, height, build_device=build_device)
 
 
-def c3(width=1920, height=1080, subdiv=8) -> Scene:
-    return lattice(24, subdiv, 0.3, width, height, cols=6)
+def c3(width=1920, height=1080, subdiv=8, build_device=None) -> Scene:
+    return lattice(24, subdiv, 0.3, width, height, cols=6, build_device=build_device)
 
 
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3}

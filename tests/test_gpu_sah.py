@@ -88,3 +88,17 @@ def test_sah_dev_signed_zero_ties(cuda):
     hi = lo + g.integers(0, 3, (n, 3))
     hi[(hi == 0) & (g.random((n, 3)) < 0.5)] = -0.0
     _compare(lo, hi, (lo + hi) * 0.5, 4, cuda)
+
+
+def test_build_bottoms_on_device(cuda):
+    """Scene-level use: per-object trees built on the GPU equal host builds."""
+    from paper_2306_07191_b200 import meshgen
+    from paper_2306_07191_b200.scene import build_bottoms
+    base = meshgen.mesh_arrays(*meshgen.icosphere(5, 0.35))
+    arrays = [meshgen.transformed(base, 1.0, (0.3 * k, -0.2 * k, 0.35)) for k in range(3)]
+    arrays.append(meshgen.mesh_arrays(*meshgen.torus()))
+    host = build_bottoms(arrays, workers=1)
+    dev = build_bottoms(arrays, device=cuda)
+    for h, d in zip(host, dev):
+        for nm in ("node_lo", "node_hi", "node_a", "node_b", "node_leaf", "order", "v0", "n2"):
+            assert getattr(h, nm).tobytes() == getattr(d, nm).tobytes(), nm

@@ -54,7 +54,7 @@ def main():
     res = {"config": "C3: 24 x icosphere(8) + NIF plane, 1920x1080, point light",
            "spp_train": a.spp, "epochs": a.epochs}
     t0 = time.perf_counter()
-    scene = c3(a.width, a.height)
+    scene = c3(a.width, a.height, build_device=torch.device("cuda", 0))
     ds = scene.device()
     res["triangles"] = int(sum(o.n_triangles for o in scene.objects))
     res["build_s"] = time.perf_counter() - t0
