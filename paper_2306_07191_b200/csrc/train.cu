@@ -438,6 +438,18 @@ __global__ void adam_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1, AdamSeg s2
 // the bias corrections c1 / c2 are computed once per block, and segments
 // whose per-unit length is a multiple of 4 move p / g / m / v as float4.
 // Per element the reference's fp64 expression (grids.py:33-45) is kept.
+// x, or 1.0 where x is +-0 -- as PTX, so the compiler cannot fold it back
+// into the division it guards
+__device__ __forceinline__ double nonzero(double x) {
+  double r;
+  asm("{\n .reg .pred z;\n setp.eq.f64 z, %1, 0d0000000000000000;\n"
+      " selp.f64 %0, 0d3FF0000000000000, %1, z;\n}"
+      : "=d"(r)
+      : "d"(x));
+  return r;
+}
+
+template <int V>
 __device__ __forceinline__ void adam_elem(float& p, float& gr, float& m, float& v, double lr,
                                           double b1, double b2, double eps, double c1,
                                           double c2) {
@@ -446,18 +458,33 @@ __device__ __forceinline__ void adam_elem(float& p, float& gr, float& m, float& 
   const double vi = b2 * ((double)v * 1.0) + (1.0 - b2) * g * g;
   m = (float)mi;
   v = (float)vi;
-  const double mh = mi / c1;
-  const double vh = vi / c2;
-  p = (float)((double)p - lr * mh / (sqrt(vh) + eps));
+  if constexpr (V == 1) {  // the plain expression (variant for measurement)
+    const double mh = mi / c1;
+    const double vh = vi / c2;
+    p = (float)((double)p - lr * mh / (sqrt(vh) + eps));
+  } else {
+    // Zero operands are resolved by selects: x / c for x = +-0 and c > 0 is
+    // x itself, and vi == 0 is +0 (so sqrt(vi / c2) + eps == eps); the
+    // divisions and the square root only ever see non-zero operands (1.0
+    // stands in), which keeps them on their fast path -- most cells of a
+    // sparsely touched grid hold zero moments, and a zero operand sends a
+    // division into its slow special-operand subroutine. Bit-identical.
+    const double mh = mi == 0.0 ? mi : nonzero(mi) / c1;
+    const double num = lr * mh;
+    const double den = vi == 0.0 ? eps : sqrt(nonzero(vi) / c2) + eps;
+    const double q = num == 0.0 ? num : nonzero(num) / den;
+    p = (float)((double)p - q);
+  }
   gr = 0.f;
 }
 
-__global__ void __launch_bounds__(256) adam_units_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1,
+template <int AV>
+__global__ void __launch_bounds__(256, 4) adam_units_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1,
                                                          AdamSeg s2, AdamSeg s3, AdamSeg s4,
                                                          int shared, double lr, double b1,
                                                          double b2, double eps) {
-  const AdamSeg segs[5] = {s0, s1, s2, s3, s4};
-  const AdamSeg sg = segs[blockIdx.z];
+  const unsigned z = blockIdx.z;  // uniform selects (no local-memory array)
+  const AdamSeg sg = z == 0 ? s0 : z == 1 ? s1 : z == 2 ? s2 : z == 3 ? s3 : s4;
   const int64_t unit = blockIdx.y;
   if (unit >= sg.n_units) return;
   int64_t step;
@@ -485,10 +512,10 @@ __global__ void __launch_bounds__(256) adam_units_kernel(nif_train_view t, AdamS
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
          e += (int64_t)gridDim.x * blockDim.x) {
       float4 p = P[e], g = G[e], m = M[e], v = V[e];
-      adam_elem(p.x, g.x, m.x, v.x, lr, b1, b2, eps, c1, c2);
-      adam_elem(p.y, g.y, m.y, v.y, lr, b1, b2, eps, c1, c2);
-      adam_elem(p.z, g.z, m.z, v.z, lr, b1, b2, eps, c1, c2);
-      adam_elem(p.w, g.w, m.w, v.w, lr, b1, b2, eps, c1, c2);
+      adam_elem<AV>(p.x, g.x, m.x, v.x, lr, b1, b2, eps, c1, c2);
+      adam_elem<AV>(p.y, g.y, m.y, v.y, lr, b1, b2, eps, c1, c2);
+      adam_elem<AV>(p.z, g.z, m.z, v.z, lr, b1, b2, eps, c1, c2);
+      adam_elem<AV>(p.w, g.w, m.w, v.w, lr, b1, b2, eps, c1, c2);
       P[e] = p;
       G[e] = g;
       M[e] = m;
@@ -498,7 +525,7 @@ __global__ void __launch_bounds__(256) adam_units_kernel(nif_train_view t, AdamS
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < sg.per;
          e += (int64_t)gridDim.x * blockDim.x) {
       const int64_t q = base + e;
-      adam_elem(t.params[q], t.grad[q], t.m[q], t.v[q], lr, b1, b2, eps, c1, c2);
+      adam_elem<AV>(t.params[q], t.grad[q], t.m[q], t.v[q], lr, b1, b2, eps, c1, c2);
     }
   }
 }
@@ -602,7 +629,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     const int K = l == 0 ? IN : W;
     __syncthreads();  // previous layer's outputs / x visible; sw free
     for (int e = tid; e < K * W; e += TT) {  // sw[k][j] = W_l[j][k]
-      const int j = e / K, k = e % K;
+      const int j = l == 0 ? e / K : e / W, k = l == 0 ? e % K : e % W;
       sw[k * W + j] = __ldg(Wt + wo + (size_t)j * K + k);
     }
     __syncthreads();
@@ -638,6 +665,13 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     bo += W;
   }
   __syncthreads();
+  // from here on the hidden layers hold activations leaky(z) (same sign as z,
+  // so the backward masks `z > 0` read them unchanged)
+  for (int e = tid; e < L * RB * W; e += TT) {
+    const int lr = e / W, k = e % W;
+    zs[lr * WP + k] = leaky(zs[lr * WP + k]);
+  }
+  __syncthreads();
   // ---- head + loss: one (row, q) per thread --------------------------------
   const size_t wo_h = wo, bo_h = bo;
   const float* zl = zs + (size_t)(L - 1) * RB * WP;
@@ -652,7 +686,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       const int ob = v ? (int)a.obj[rw] : 0;
       float acc = __ldg(Bt + bo_h + q);
       const float* wr = Wt + wo_h + (size_t)q * W;
-      for (int k = 0; k < W; ++k) acc = fmaf(__ldg(wr + k), leaky(zl[r * WP + k]), acc);
+      for (int k = 0; k < W; ++k) acc = fmaf(__ldg(wr + k), zl[r * WP + k], acc);
       const int n_o = v ? a.t.counts[ob] : 1;
       const float scale = (float)(2.0 / ((double)n_o * OUT));
       const float lab = v ? a.label[rw * OUT + q] : 0.f;
@@ -684,7 +718,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     const int q = e / (W + 1), k = e % (W + 1);
     float s = 0.f;
     if (k < W) {
-      for (int r = 0; r < RB; ++r) s = fmaf(dh[r * kMaxOut + q], leaky(zl[r * WP + k]), s);
+      for (int r = 0; r < RB; ++r) s = fmaf(dh[r * kMaxOut + q], zl[r * WP + k], s);
       atomicAdd(gW + wo_h + q * W + k, s);
     } else {
       for (int r = 0; r < RB; ++r) s += dh[r * kMaxOut + q];
@@ -698,16 +732,49 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     wo -= (size_t)W * W;
     bo -= W;
     const float* zp = zs + (size_t)(l - 1) * RB * WP;
-    // weight grads of dense layer l
-    for (int e = tid; e < W * (W + 1); e += TT) {
-      const int j = e / (W + 1), k = e % (W + 1);
-      float s = 0.f;
-      if (k < W) {
-        for (int r = 0; r < RB; ++r) s = fmaf(dzc[r * WP + j], leaky(zp[r * WP + k]), s);
-        atomicAdd(gW + wo + (size_t)j * W + k, s);
-      } else {
-        for (int r = 0; r < RB; ++r) s += dzc[r * WP + j];
-        atomicAdd(gB + bo + j, s);
+    // weight grads of dense layer l: gW[j][k] += sum_r dz[r][j] a[r][k]
+    if constexpr (TT == 256) {
+      // 16 x 16 threads, each a CPT x CPT register tile (j = tj + 16 cj,
+      // k = tk + 16 ck), rows ascending as in the per-element loop
+      const int tj = tid >> 4, tk = tid & 15;
+      float g[CPT][CPT];
+#pragma unroll
+      for (int cj = 0; cj < CPT; ++cj)
+#pragma unroll
+        for (int ck = 0; ck < CPT; ++ck) g[cj][ck] = 0.f;
+      for (int r = 0; r < RB; ++r) {
+        float dj[CPT], ak[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          dj[c] = dzc[r * WP + tj + 16 * c];
+          ak[c] = zp[r * WP + tk + 16 * c];
+        }
+#pragma unroll
+        for (int cj = 0; cj < CPT; ++cj)
+#pragma unroll
+          for (int ck = 0; ck < CPT; ++ck) g[cj][ck] = fmaf(dj[cj], ak[ck], g[cj][ck]);
+      }
+#pragma unroll
+      for (int cj = 0; cj < CPT; ++cj)
+#pragma unroll
+        for (int ck = 0; ck < CPT; ++ck)
+          atomicAdd(gW + wo + (size_t)(tj + 16 * cj) * W + tk + 16 * ck, g[cj][ck]);
+      if (tid < W) {
+        float sb = 0.f;
+        for (int r = 0; r < RB; ++r) sb += dzc[r * WP + tid];
+        atomicAdd(gB + bo + tid, sb);
+      }
+    } else {
+      for (int e = tid; e < W * (W + 1); e += TT) {
+        const int j = e / (W + 1), k = e % (W + 1);
+        float s = 0.f;
+        if (k < W) {
+          for (int r = 0; r < RB; ++r) s = fmaf(dzc[r * WP + j], zp[r * WP + k], s);
+          atomicAdd(gW + wo + (size_t)j * W + k, s);
+        } else {
+          for (int r = 0; r < RB; ++r) s += dzc[r * WP + j];
+          atomicAdd(gB + bo + j, s);
+        }
       }
     }
     // stage W_l natural [j][k], then dZ_{l-1} = mask . (dZ_l W_l), j ascending
@@ -779,7 +846,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   }
 }
 
-int g_train_variant = 0;  // 0 tiled where it applies, 1 per-row kernel (nif_debug_set_train_variant)
+int g_train_variant = 0;  // 0 tiled where it applies, 1 per-row kernel, 2/3 other tilings,
+                          // 4 plain Adam expression (nif_debug_set_train_variant)
 
 template <int W, int RB, int TT>
 int launch_fwdbwd_tiled_rb(const TrainArgs& a, cudaStream_t st) {
@@ -945,8 +1013,12 @@ extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, d
     int64_t bx = (per_max / 4 + 1023) / 1024;
     if (bx < 1) bx = 1;
     dim3 grid((unsigned)bx, (unsigned)(units > 0 ? units : 1), 5);
-    adam_units_kernel<<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr, beta1,
-                                            beta2, eps);
+    if (g_train_variant == 4)
+      adam_units_kernel<1><<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr,
+                                                 beta1, beta2, eps);
+    else
+      adam_units_kernel<0><<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr,
+                                                 beta1, beta2, eps);
   }
   clear_counts_kernel<<<(f->n_obj + 127) / 128, 128, 0, st>>>(t->counts, f->n_obj);
   return check_launch("nif_adam_dev");
