@@ -549,6 +549,30 @@ __global__ void clear_counts_kernel(int32_t* counts, int n) {
 // ---------------------------------------------------------------------------
 // RB rows per CTA, TT threads: 16 column groups x (TT/16) row groups of
 // RPT = 16 RB / TT rows each
+// shared-memory carve of the tiled kernel (floats unless noted)
+struct TiledSmem {
+  int zs, dzA, dzB, xs, dh, sw, sb, rwd, rwi, total_bytes;
+  int o_h1, o_head;  // offsets of the hidden / head weights inside sw
+};
+__host__ __device__ inline TiledSmem tiled_smem(int W, int RB, int L, int IN, int OUT) {
+  TiledSmem t;
+  const int WP = W + 1;
+  t.zs = 0;
+  t.dzA = t.zs + L * RB * WP;
+  t.dzB = t.dzA + RB * WP;
+  t.xs = t.dzB + RB * WP;
+  t.dh = t.xs + RB * kMaxIn;
+  t.sw = t.dh + RB * kMaxOut;
+  t.o_h1 = W * (IN + 1);
+  t.o_head = t.o_h1 + (L - 1) * W * WP;
+  t.sb = t.sw + t.o_head + OUT * WP;
+  const int end_f = t.sb + L * W + kMaxOut;
+  t.rwd = (end_f + 1) / 2;  // in doubles: [RB][9] corner weights of each row
+  t.rwi = (t.rwd + RB * 9) * 2;  // in ints: [RB][11] corner cells, object (-1: no row)
+  t.total_bytes = (t.rwi + RB * 11) * 4;
+  return t;
+}
+
 template <int W, int RB, int TT>
 __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   constexpr int RPT = RB * 16 / TT;
@@ -560,37 +584,57 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   const nif_family_view& f = a.f;
   const int L = f.n_layers - 1;
   const int IN = f.dims[0];
+  const int INP = IN + 1;
   const int OUT = f.dims[f.n_layers];
-  float* zs = sm;                            // [L][RB][WP] pre-activations
-  float* dzA = zs + (size_t)L * RB * WP;    // [RB][WP]
-  float* dzB = dzA + RB * WP;               // [RB][WP]
-  float* xs = dzB + RB * WP;                // [RB][kMaxIn]
-  float* dh = xs + RB * kMaxIn;             // [RB][kMaxOut]
-  float* sw = dh + RB * kMaxOut;            // [max(W, IN)][W] staged weights
-  const float* Wt = f.w;
-  const float* Bt = f.b;
+  const TiledSmem T = tiled_smem(W, RB, L, IN, OUT);
+  float* zs = sm + T.zs;    // [L][RB][WP] pre-activations, then activations
+  float* dzA = sm + T.dzA;  // [RB][WP]
+  float* dzB = sm + T.dzB;  // [RB][WP]
+  float* xs = sm + T.xs;    // [RB][kMaxIn]
+  float* dh = sm + T.dh;    // [RB][kMaxOut]
+  float* sw = sm + T.sw;    // every layer's weights, natural [j][k], rows padded to K + 1
+  float* sb = sm + T.sb;    // every layer's biases
+  double* rwd = reinterpret_cast<double*>(sm) + T.rwd;
+  int* rwi = reinterpret_cast<int*>(sm) + T.rwi;
   float* gW = a.t.grad + a.t.off_w;
   float* gB = a.t.grad + a.t.off_b;
   const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
   const int tc = tid & 15, tr = tid >> 4;  // 16 column groups x TT/16 row groups of RPT
 
-  // ---- encode (rows 0..31 on threads 0..31) ------------------------------
-  const int r_own = tid;  // valid only for tid < RB
-  int64_t row = 0;
-  bool valid = false;
-  int o = 0;
-  Bil64 bp{}, bd{};
-  Axis ad{};
+  // ---- stage the whole MLP once (its loads overlap the encode's) -----------
+  {
+    const int n0 = W * IN, nh = (L - 1) * W * W, total = n0 + nh + OUT * W;
+    for (int e = tid; e < total; e += TT) {
+      const float v = __ldg(f.w + e);
+      int d;
+      if (e < n0) {
+        const int j = e / IN;
+        d = j * INP + (e - j * IN);
+      } else if (e < n0 + nh) {
+        const int e2 = e - n0, l = e2 / (W * W), r2 = e2 - l * W * W;
+        d = T.o_h1 + l * W * WP + (r2 / W) * WP + r2 % W;
+      } else {
+        const int e2 = e - n0 - nh;
+        d = T.o_head + (e2 / W) * WP + e2 % W;
+      }
+      sw[d] = v;
+    }
+    for (int e = tid; e < L * W + OUT; e += TT) sb[e] = __ldg(f.b + e);
+  }
+
+  // ---- encode (rows 0..RB-1 on threads 0..RB-1) ------------------------------
   if (tid < RB) {
     const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
     const int64_t g = a.row0 + k_row * a.row_step;
-    valid = g < a.n_rows;
+    const bool valid = g < a.n_rows;
     const int64_t* bidx = batch_idx(a.idx, a.cursor);
-    row = valid ? (bidx ? bidx[g] : g) : 0;
-    o = valid ? (int)a.obj[row] : 0;
+    const int64_t row = valid ? (bidx ? bidx[g] : g) : 0;
+    const int o = valid ? (int)a.obj[row] : 0;
     float x[kMaxIn];
 #pragma unroll
     for (int k = 0; k < kMaxIn; ++k) x[k] = 0.f;
+    Bil64 bp{}, bd{};
+    Axis ad{};
     if (valid) {
       const double* c = a.coord + row * cw;
       const size_t g2 = (size_t)f.R * f.R * f.N;
@@ -620,23 +664,30 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
         }
       }
     }
-    for (int k = 0; k < kMaxIn; ++k) xs[r_own * kMaxIn + k] = x[k];
+    for (int k = 0; k < kMaxIn; ++k) xs[tid * kMaxIn + k] = x[k];
+    // the row's scatter targets, for the backward pass's (row, input) threads
+    for (int c = 0; c < 4; ++c) {
+      rwd[tid * 9 + c] = bp.w[c];
+      rwd[tid * 9 + 4 + c] = bd.w[c];
+      rwi[tid * 11 + c] = bp.c[c];
+      rwi[tid * 11 + 4 + c] = bd.c[c];
+    }
+    rwd[tid * 9 + 8] = ad.w;
+    rwi[tid * 11 + 8] = ad.i0;
+    rwi[tid * 11 + 9] = ad.i1;
+    rwi[tid * 11 + 10] = valid ? o : -1;
   }
 
   // ---- forward: Z_l = bias + act(prev) . W_l^T (k ascending) ---------------
-  size_t wo = 0, bo = 0;
   for (int l = 0; l < L; ++l) {
     const int K = l == 0 ? IN : W;
-    __syncthreads();  // previous layer's outputs / x visible; sw free
-    for (int e = tid; e < K * W; e += TT) {  // sw[k][j] = W_l[j][k]
-      const int j = l == 0 ? e / K : e / W, k = l == 0 ? e % K : e % W;
-      sw[k * W + j] = __ldg(Wt + wo + (size_t)j * K + k);
-    }
-    __syncthreads();
+    const int KP = K + 1;
+    const float* wl = l == 0 ? sw : sw + T.o_h1 + (l - 1) * W * WP;
+    __syncthreads();  // weights, x / the previous layer's outputs visible
     float acc[RPT][CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-      const float bj = __ldg(Bt + bo + tc + 16 * c);
+      const float bj = sb[l * W + tc + 16 * c];
 #pragma unroll
       for (int i = 0; i < RPT; ++i) acc[i][c] = bj;
     }
@@ -651,7 +702,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       }
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        const float wv = sw[k * W + tc + 16 * c];
+        const float wv = wl[(tc + 16 * c) * KP + k];
 #pragma unroll
         for (int i = 0; i < RPT; ++i) acc[i][c] = fmaf(wv, av[i], acc[i][c]);
       }
@@ -661,8 +712,6 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     for (int i = 0; i < RPT; ++i)
 #pragma unroll
       for (int c = 0; c < CPT; ++c) z[(tr * RPT + i) * WP + tc + 16 * c] = acc[i][c];
-    wo += (size_t)K * W;
-    bo += W;
   }
   __syncthreads();
   // from here on the hidden layers hold activations leaky(z) (same sign as z,
@@ -673,7 +722,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   }
   __syncthreads();
   // ---- head + loss: one (row, q) per thread --------------------------------
-  const size_t wo_h = wo, bo_h = bo;
+  const size_t wo_h = (size_t)W * IN + (size_t)(L - 1) * W * W, bo_h = (size_t)L * W;
+  const float* swh = sw + T.o_head;
   const float* zl = zs + (size_t)(L - 1) * RB * WP;
   {
     const int r = tid % RB, q = tid / RB;
@@ -684,9 +734,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       const int64_t* bidx = batch_idx(a.idx, a.cursor);
       const int64_t rw = v ? (bidx ? bidx[g] : g) : 0;
       const int ob = v ? (int)a.obj[rw] : 0;
-      float acc = __ldg(Bt + bo_h + q);
-      const float* wr = Wt + wo_h + (size_t)q * W;
-      for (int k = 0; k < W; ++k) acc = fmaf(__ldg(wr + k), zl[r * WP + k], acc);
+      float acc = sb[bo_h + q];
+      for (int k = 0; k < W; ++k) acc = fmaf(swh[q * WP + k], zl[r * WP + k], acc);
       const int n_o = v ? a.t.counts[ob] : 1;
       const float scale = (float)(2.0 / ((double)n_o * OUT));
       const float lab = v ? a.label[rw * OUT + q] : 0.f;
@@ -710,7 +759,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   for (int e = tid; e < RB * W; e += TT) {
     const int r = e / W, k = e % W;
     float da = 0.f;
-    for (int q = 0; q < OUT; ++q) da = fmaf(dh[r * kMaxOut + q], __ldg(Wt + wo_h + q * W + k), da);
+    for (int q = 0; q < OUT; ++q) da = fmaf(dh[r * kMaxOut + q], swh[q * WP + k], da);
     dzA[r * WP + k] = zl[r * WP + k] > 0.f ? da : da * kSlope;
   }
   // head gradients
@@ -729,8 +778,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   float* dzc = dzA;
   float* dzn = dzB;
   for (int l = L - 1; l >= 1; --l) {
-    wo -= (size_t)W * W;
-    bo -= W;
+    const size_t wo = (size_t)W * IN + (size_t)(l - 1) * W * W, bo = (size_t)l * W;
+    const float* wl = sw + T.o_h1 + (l - 1) * W * WP;
     const float* zp = zs + (size_t)(l - 1) * RB * WP;
     // weight grads of dense layer l: gW[j][k] += sum_r dz[r][j] a[r][k]
     if constexpr (TT == 256) {
@@ -760,9 +809,9 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
         for (int ck = 0; ck < CPT; ++ck)
           atomicAdd(gW + wo + (size_t)(tj + 16 * cj) * W + tk + 16 * ck, g[cj][ck]);
       if (tid < W) {
-        float sb = 0.f;
-        for (int r = 0; r < RB; ++r) sb += dzc[r * WP + tid];
-        atomicAdd(gB + bo + tid, sb);
+        float sbias = 0.f;
+        for (int r = 0; r < RB; ++r) sbias += dzc[r * WP + tid];
+        atomicAdd(gB + bo + tid, sbias);
       }
     } else {
       for (int e = tid; e < W * (W + 1); e += TT) {
@@ -777,9 +826,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
         }
       }
     }
-    // stage W_l natural [j][k], then dZ_{l-1} = mask . (dZ_l W_l), j ascending
-    for (int e = tid; e < W * W; e += TT) sw[e] = __ldg(Wt + wo + e);
-    __syncthreads();
+    // dZ_{l-1} = mask . (dZ_l W_l), j ascending
     float acc[RPT][CPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
@@ -791,7 +838,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       for (int i = 0; i < RPT; ++i) dv[i] = dzc[(tr * RPT + i) * WP + j];
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        const float wv = sw[j * W + tc + 16 * c];
+        const float wv = wl[j * WP + tc + 16 * c];
 #pragma unroll
         for (int i = 0; i < RPT; ++i) acc[i][c] = fmaf(dv[i], wv, acc[i][c]);
       }
@@ -820,28 +867,31 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       atomicAdd(gB + j, s);
     }
   }
-  if (tid >= RB || !valid) return;
-  // dx = dZ_0 W_0 -> grid scatter (grids.py:171-202)
-  float dx[kMaxIn];
-  for (int k = 0; k < IN; ++k) {
-    float s = 0.f;
-    const float* dc = dzc + (size_t)r_own * WP;
-    for (int j = 0; j < W; ++j) s = fmaf(dc[j], __ldg(Wt + (size_t)j * IN + k), s);
-    dx[k] = s;
-  }
+  // dx = dZ_0 W_0, one (row, input) per thread -> grid scatter
+  // (grids.py:171-202); j ascending as in the per-row kernel
   const size_t g2 = (size_t)f.R * f.R * f.N;
-  float* gpos = a.t.grad + a.t.off_pos + (size_t)o * g2;
-  float* gdir = a.t.grad + a.t.off_dir + (size_t)o * g2;
-  for (int c = 0; c < 4; ++c)
-    for (int k = 0; k < f.N; ++k) {
-      atomicAdd(gpos + (size_t)bp.c[c] * f.N + k, (float)(bp.w[c] * (double)dx[k]));
-      atomicAdd(gdir + (size_t)bd.c[c] * f.N + k, (float)(bd.w[c] * (double)dx[f.N + k]));
-    }
-  if (f.family == NIF_FAMILY_INNER) {
-    float* gr = a.t.grad + a.t.off_dist + (size_t)o * f.Rd * f.Nd;
-    for (int k = 0; k < f.Nd; ++k) {
-      atomicAdd(gr + (size_t)ad.i0 * f.Nd + k, (float)((1.0 - ad.w) * (double)dx[2 * f.N + k]));
-      atomicAdd(gr + (size_t)ad.i1 * f.Nd + k, (float)(ad.w * (double)dx[2 * f.N + k]));
+  for (int e = tid; e < RB * IN; e += TT) {
+    const int r = e / IN, k = e - (e / IN) * IN;
+    const int o = rwi[r * 11 + 10];
+    if (o < 0) continue;
+    float s = 0.f;
+    const float* dc = dzc + (size_t)r * WP;
+    for (int j = 0; j < W; ++j) s = fmaf(dc[j], sw[j * INP + k], s);
+    const double dx = (double)s;
+    if (k < 2 * f.N) {
+      const bool is_pos = k < f.N;
+      float* gg = a.t.grad + (is_pos ? a.t.off_pos : a.t.off_dir) + (size_t)o * g2;
+      const int kk = is_pos ? k : k - f.N;
+      const int cb = is_pos ? 0 : 4;
+      for (int c = 0; c < 4; ++c)
+        atomicAdd(gg + (size_t)rwi[r * 11 + cb + c] * f.N + kk,
+                  (float)(rwd[r * 9 + cb + c] * dx));
+    } else {
+      const int kk = k - 2 * f.N;
+      const double w = rwd[r * 9 + 8];
+      float* gr = a.t.grad + a.t.off_dist + (size_t)o * f.Rd * f.Nd;
+      atomicAdd(gr + (size_t)rwi[r * 11 + 8] * f.Nd + kk, (float)((1.0 - w) * dx));
+      atomicAdd(gr + (size_t)rwi[r * 11 + 9] * f.Nd + kk, (float)(w * dx));
     }
   }
 }
@@ -852,10 +902,9 @@ int g_train_variant = 0;  // 0 tiled where it applies, 1 per-row kernel, 2/3 oth
 template <int W, int RB, int TT>
 int launch_fwdbwd_tiled_rb(const TrainArgs& a, cudaStream_t st) {
   const int L = a.f.n_layers - 1;
-  const int K = a.f.dims[0] > W ? a.f.dims[0] : W;
-  const size_t smem = ((size_t)L * RB * (W + 1) + 2 * (size_t)RB * (W + 1) +
-                       (size_t)RB * kMaxIn + (size_t)RB * kMaxOut + (size_t)K * W) *
-                      sizeof(float);
+  const size_t smem =
+      (size_t)tiled_smem(W, RB, L, a.f.dims[0], a.f.dims[a.f.n_layers]).total_bytes;
+  if (smem > 200 * 1024) return fail(NIF_ERR_UNSUPPORTED, "MLP too large for the training kernel");
   auto kern = train_fwdbwd_tiled_kernel<W, RB, TT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
