@@ -298,6 +298,19 @@ int nif_train_fwdbwd_cur_dev(const nif_family_view* f, const nif_train_view* t,
                              const int64_t* idx, const int64_t* cursor, int64_t n_rows,
                              int64_t row0, int64_t row_step, double* sq_err, void* stream);
 int nif_cursor_advance_dev(int64_t* cursor, int64_t delta, void* stream);
+/* The three-launch step of a captured graph: prologue (one CTA: this
+ * batch's per-object counts, overwritten, plus the Adam step counters of
+ * the touched objects / heads), nif_train_fwdbwd_cur_dev, then the dense
+ * update alone (nif_adam_dev minus its step-counter and count-clearing
+ * kernels), which also advances the cursor by delta (cursor may be NULL).
+ * Counts are left holding the last batch's: clear them before using the
+ * accumulate-style nif_batch_counts_dev again.                             */
+int nif_train_prologue_cur_dev(const nif_family_view* f, const nif_train_view* t,
+                               const int64_t* obj, const int64_t* idx, const int64_t* cursor,
+                               int64_t n_rows, void* stream);
+int nif_adam_units_dev(const nif_family_view* f, const nif_train_view* t, double lr,
+                       double beta1, double beta2, double eps, int64_t* cursor, int64_t delta,
+                       void* stream);
 
 /* Adam (grids.py:31-45) on every touched object's grids (dense, all
  * cells) and on each touched MLP head; fp64 moments over fp32 storage,

@@ -166,6 +166,10 @@ _SIGS = {
     "nif_train_fwdbwd_cur_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P,
                                            P, P, I64, I64, I64, P, P]),
     "nif_cursor_advance_dev": (C.c_int, [P, I64, P]),
+    "nif_train_prologue_cur_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P,
+                                             P, I64, P]),
+    "nif_adam_units_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), D, D, D, D,
+                                     P, I64, P]),
     "nif_train_fwdbwd_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
                                        I64, I64, I64, P, P]),
     "nif_adam_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), D, D, D, D, P]),

@@ -386,6 +386,35 @@ __global__ void adam_steps_kernel(nif_train_view t, int n_obj, int n_heads, int 
   }
 }
 
+__global__ void cursor_advance_kernel(int64_t* cursor, int64_t delta) { *cursor += delta; }
+
+// One step's prologue for graph replay, one CTA: the batch's per-object row
+// counts (overwritten, so no clearing kernel is needed) and the Adam step
+// counters of the touched objects / heads (adam_steps_kernel's rule).
+__global__ void __launch_bounds__(1024) train_prologue_kernel(const int64_t* __restrict__ obj,
+                                                              const int64_t* __restrict__ idx,
+                                                              const int64_t* __restrict__ cursor,
+                                                              int64_t n, nif_train_view t,
+                                                              int n_obj, int n_heads,
+                                                              int shared) {
+  extern __shared__ int hist[];
+  for (int i = threadIdx.x; i < n_obj; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  idx = batch_idx(idx, cursor);
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+    const int64_t o = obj[idx ? idx[r] : r];
+    if (o >= 0 && o < n_obj) atomicAdd(hist + o, 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_obj || i < n_heads; i += blockDim.x) {
+    if (i < n_obj) {
+      t.counts[i] = hist[i];
+      if (hist[i] > 0) t.grid_steps[i] += 1;
+    }
+    if (i < n_heads && (shared || hist[i] > 0)) t.mlp_steps[i] += 1;
+  }
+}
+
 // grids.py:31-45 _adam_update per element
 __global__ void adam_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1, AdamSeg s2, AdamSeg s3,
                             AdamSeg s4, int nseg, int shared, double lr, double b1, double b2,
@@ -482,7 +511,11 @@ template <int AV>
 __global__ void __launch_bounds__(256, 4) adam_units_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1,
                                                          AdamSeg s2, AdamSeg s3, AdamSeg s4,
                                                          int shared, double lr, double b1,
-                                                         double b2, double eps) {
+                                                         double b2, double eps,
+                                                         int64_t* cursor, int64_t delta) {
+  // graph replay: the batch cursor moves on here (the step's readers of it
+  // have finished: they precede this kernel on the stream)
+  if (cursor && (blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0) *cursor += delta;
   const unsigned z = blockIdx.z;  // uniform selects (no local-memory array)
   const AdamSeg sg = z == 0 ? s0 : z == 1 ? s1 : z == 2 ? s2 : z == 3 ? s3 : s4;
   const int64_t unit = blockIdx.y;
@@ -949,8 +982,6 @@ int launch_fwdbwd(const TrainArgs& a, cudaStream_t st) {
 
 using namespace nif;
 
-__global__ void cursor_advance_kernel(int64_t* cursor, int64_t delta) { *cursor += delta; }
-
 extern "C" int nif_batch_counts_cur_dev(const int64_t* obj, const int64_t* idx,
                                         const int64_t* cursor, int64_t n_rows, int32_t n_obj,
                                         int32_t* counts, void* stream) {
@@ -1027,13 +1058,14 @@ extern "C" int nif_debug_set_train_variant(int v) {
   return NIF_OK;
 }
 
-extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, double lr,
-                            double beta1, double beta2, double eps, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+namespace {
+
+// the dense update of every touched unit; cursor: advanced by delta (graph replay)
+void launch_adam_units(const nif_family_view* f, const nif_train_view* t, double lr,
+                       double beta1, double beta2, double eps, int64_t* cursor, int64_t delta,
+                       cudaStream_t st) {
   const int n_heads = f->n_heads;
   const int shared = n_heads == 1;
-  const int n = f->n_obj > n_heads ? f->n_obj : n_heads;
-  adam_steps_kernel<<<(n + 127) / 128, 128, 0, st>>>(*t, f->n_obj, n_heads, shared);
   AdamSeg s[5];
   int ns = 0;
   const int64_t g2 = (int64_t)f->R * f->R * f->N;
@@ -1051,24 +1083,63 @@ extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, d
     if (blocks > cap) blocks = cap;
     adam_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(
         *t, s[0], s[1], s[2], s[3], s[4], 5, shared, lr, beta1, beta2, eps);
-  } else {
-    int64_t per_max = 0, units = 0;
-    for (int q = 0; q < 5; ++q) {
-      if (s[q].per > per_max) per_max = s[q].per;
-      if (s[q].n_units > units) units = s[q].n_units;
-    }
-    // ~4 float4 per thread per block: enough blocks to fill the GPU for the
-    // touched units without a per-element segment search
-    int64_t bx = (per_max / 4 + 1023) / 1024;
-    if (bx < 1) bx = 1;
-    dim3 grid((unsigned)bx, (unsigned)(units > 0 ? units : 1), 5);
-    if (g_train_variant == 4)
-      adam_units_kernel<1><<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr,
-                                                 beta1, beta2, eps);
-    else
-      adam_units_kernel<0><<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr,
-                                                 beta1, beta2, eps);
+    if (cursor) cursor_advance_kernel<<<1, 1, 0, st>>>(cursor, delta);
+    return;
   }
+  int64_t per_max = 0, units = 0;
+  for (int q = 0; q < 5; ++q) {
+    if (s[q].per > per_max) per_max = s[q].per;
+    if (s[q].n_units > units) units = s[q].n_units;
+  }
+  // ~4 float4 per thread per block: enough blocks to fill the GPU for the
+  // touched units without a per-element segment search
+  int64_t bx = (per_max / 4 + 1023) / 1024;
+  if (bx < 1) bx = 1;
+  dim3 grid((unsigned)bx, (unsigned)(units > 0 ? units : 1), 5);
+  if (g_train_variant == 4)
+    adam_units_kernel<1><<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr,
+                                               beta1, beta2, eps, cursor, delta);
+  else
+    adam_units_kernel<0><<<grid, 256, 0, st>>>(*t, s[0], s[1], s[2], s[3], s[4], shared, lr,
+                                               beta1, beta2, eps, cursor, delta);
+}
+
+}  // namespace
+
+extern "C" int nif_adam_dev(const nif_family_view* f, const nif_train_view* t, double lr,
+                            double beta1, double beta2, double eps, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_heads = f->n_heads;
+  const int n = f->n_obj > n_heads ? f->n_obj : n_heads;
+  adam_steps_kernel<<<(n + 127) / 128, 128, 0, st>>>(*t, f->n_obj, n_heads, n_heads == 1);
+  launch_adam_units(f, t, lr, beta1, beta2, eps, nullptr, 0, st);
   clear_counts_kernel<<<(f->n_obj + 127) / 128, 128, 0, st>>>(t->counts, f->n_obj);
   return check_launch("nif_adam_dev");
+}
+
+extern "C" int nif_train_prologue_cur_dev(const nif_family_view* f, const nif_train_view* t,
+                                          const int64_t* obj, const int64_t* idx,
+                                          const int64_t* cursor, int64_t n_rows, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_obj = f->n_obj, n_heads = f->n_heads;
+  if (n_obj > 12 * 1024) {  // histogram beyond one CTA's shared memory
+    clear_counts_kernel<<<(n_obj + 127) / 128, 128, 0, st>>>(t->counts, n_obj);
+    if (n_rows > 0)
+      batch_counts_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(obj, idx, n_rows,
+                                                                            n_obj, t->counts,
+                                                                            cursor);
+    const int n = n_obj > n_heads ? n_obj : n_heads;
+    adam_steps_kernel<<<(n + 127) / 128, 128, 0, st>>>(*t, n_obj, n_heads, n_heads == 1);
+    return check_launch("nif_train_prologue_cur_dev");
+  }
+  train_prologue_kernel<<<1, 1024, (size_t)n_obj * sizeof(int), st>>>(
+      obj, idx, cursor, n_rows, *t, n_obj, n_heads, n_heads == 1);
+  return check_launch("nif_train_prologue_cur_dev");
+}
+
+extern "C" int nif_adam_units_dev(const nif_family_view* f, const nif_train_view* t, double lr,
+                                  double beta1, double beta2, double eps, int64_t* cursor,
+                                  int64_t delta, void* stream) {
+  launch_adam_units(f, t, lr, beta1, beta2, eps, cursor, delta, (cudaStream_t)stream);
+  return check_launch("nif_adam_units_dev");
 }

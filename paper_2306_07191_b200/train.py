@@ -250,14 +250,15 @@ class _GraphStep:
         st, fam, model = self.step, self.step.fam, self.step.model
         p = _lib.ptr
         sp = _lib.stream_ptr()
-        L.nif_batch_counts_cur_dev(p(self.obj), p(self.perm), p(self.cursor), n_rows, fam.n_obj,
-                                   p(fam.counts), sp)
+        # three launches: counts + step counters, fused fwd/bwd, dense Adam
+        # (which also moves the cursor on)
+        L.nif_train_prologue_cur_dev(st.fv, st.tv, p(self.obj), p(self.perm), p(self.cursor),
+                                     n_rows, sp)
         L.nif_train_fwdbwd_cur_dev(st.fv, st.tv, p(self.obj), p(self.coord), p(self.label),
                                    p(self.perm), p(self.cursor), n_rows, 0, 1, p(st.sq), sp)
         a = model.config.adam
-        L.nif_adam_dev(st.fv, st.tv, model.learning_rate, a.beta1, a.beta2, a.epsilon, sp)
-        if advance:
-            L.nif_cursor_advance_dev(p(self.cursor), n_rows, sp)
+        L.nif_adam_units_dev(st.fv, st.tv, model.learning_rate, a.beta1, a.beta2, a.epsilon,
+                             p(self.cursor) if advance else None, n_rows, sp)
 
     def epoch(self, perm_host: np.ndarray):
         torch = _torch()
@@ -281,6 +282,9 @@ class _GraphStep:
             self.graph.replay()
         if n - n_full * self.bs:
             self._enqueue(n - n_full * self.bs, False)
+        # the prologue overwrites counts; leave them zero for the
+        # accumulate-style step (_Step.run) as nif_adam_dev does
+        self.step.fam.counts.zero_()
         self.step.fam.dirty = True
 
 
