@@ -4,10 +4,11 @@ per-batch optimiser step and the epoch loop (nif.py:507-795).
 Samples stay in HBM. The epoch loop reproduces the reference's schedule
 exactly -- per-epoch RNG `default_rng(SeedSequence([seed, 0x7472])
 .spawn(epochs)[e])`, outer family permuted first then inner with the same
-generator, batches `perm[k:k+bs]` -- and every batch runs as four
-stream-ordered launches (batch counts, fused forward/backward + grid
-scatter, Adam over touched grids + MLP) with no host synchronisation until
-the epoch's losses are read back.
+generator, batches `perm[k:k+bs]` -- and on one GPU every full batch is a
+replay of a captured three-launch step (batch counts + Adam step counters,
+fused forward/backward + grid scatter, dense Adam over touched grids + MLP)
+with no host synchronisation until the losses are read back after the last
+epoch; the host draws the next permutation while the GPU replays.
 
 Data parallel (torch.distributed over NCCL): every rank holds the same
 sample set and the same global permutation; rank r processes rows
@@ -233,8 +234,10 @@ class _GraphStep:
     """One family's optimiser step captured as a CUDA graph and replayed
     for every full batch of an epoch: the batch start lives on the device
     (a cursor into a persistent permutation buffer, advanced by the graph
-    itself), so an epoch is one H2D copy of the permutation plus one graph
-    launch per batch -- no per-step host work."""
+    itself), so an epoch is one async H2D copy of the permutation (from a
+    pinned staging buffer) plus one graph launch per batch -- no per-step
+    host work and no host synchronisation: the host is free to draw the
+    next permutation while the GPU replays this one."""
 
     def __init__(self, step: "_Step", obj, coord, label, n: int, bs: int):
         torch = _torch()
@@ -242,6 +245,11 @@ class _GraphStep:
         dev = step.model.device
         self.perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         self.cursor = torch.zeros(1, dtype=torch.int64, device=dev)
+        # two pinned staging buffers: epoch e+1's permutation is written
+        # while epoch e's copy may still be queued
+        self.host = [torch.empty(max(n, 1), dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self.copied = [None, None]
+        self.turn = 0
         self.obj, self.coord, self.label = obj, coord, label
         self.graph = None
 
@@ -261,9 +269,18 @@ class _GraphStep:
                              p(self.cursor) if advance else None, n_rows, sp)
 
     def epoch(self, perm_host: np.ndarray):
+        """Queue one epoch of this family (returns without synchronising)."""
         torch = _torch()
         n = len(perm_host)
-        self.perm[:n].copy_(torch.from_numpy(perm_host))
+        k = self.turn
+        self.turn ^= 1
+        if self.copied[k] is not None:
+            self.copied[k].synchronize()  # that buffer's previous copy is done
+        self.host[k][:n].numpy()[:] = perm_host
+        self.perm[:n].copy_(self.host[k][:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.copied[k] = ev
         self.cursor.zero_()
         n_full = n // self.bs
         if n_full and self.graph is None:
@@ -344,15 +361,31 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     gsteps = {}
     fams = ((0, bo, "outer", samples.outer_obj, samples.outer_coord, samples.outer_label),
             (1, bi, "inner", samples.inner_obj, samples.inner_coord, samples.inner_label))
-    for e in range(epochs):
+    # per (epoch, family) squared-error sums, read back once at the end (the
+    # graph path never synchronises inside the loop)
+    sq = torch.zeros((epochs, 2), dtype=torch.float64, device=model.device)
+    counts = np.zeros(2, np.int64)
+    sizes = [int(f[3].shape[0]) for f in fams]
+
+    def epoch_perms(e):
+        # outer first, then inner, from the epoch's generator (nif.py:769-788)
         rng = np.random.default_rng(epoch_ss[e])
-        sums = np.zeros(2)
-        counts = np.zeros(2, np.int64)
+        return [rng.permutation(n) if n else None for n in sizes]
+
+    # the next epoch's permutations are drawn on a host thread (numpy's
+    # shuffle releases the GIL) while this epoch is queued and replayed
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=1)
+    nxt = pool.submit(epoch_perms, 0)
+    for e in range(epochs):
+        perms = nxt.result()
+        if e + 1 < epochs:
+            nxt = pool.submit(epoch_perms, e + 1)
         for fam, bs, which, obj, coord, label in fams:
             n = int(obj.shape[0])
             if n == 0:
                 continue
-            perm_np = rng.permutation(n)
+            perm_np = perms[fam]
             st = steps[which]
             st.sq.zero_()
             if use_graph:
@@ -367,8 +400,12 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
                     st.run(obj, coord, label, None, m, rank, world, group, idx_ptr=base + 8 * k)
             # the reference's per-batch loss is the mean over rows x outputs
             width = int(label.shape[1]) if label.dim() > 1 else 1
-            sums[fam] = float(st.sq.item()) / width
+            sq[e, fam].copy_(st.sq[0] / width)
             counts[fam] = n
+    pool.shutdown()
+    sums_all = sq.cpu().numpy()
+    for e in range(epochs):
+        sums = sums_all[e]
         om = sums[0] / counts[0] if counts[0] else math.nan
         im = sums[1] / counts[1] if counts[1] else math.nan
         curve[e] = (om, im, sums.sum() / counts.sum())
