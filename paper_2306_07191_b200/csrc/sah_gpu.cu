@@ -184,11 +184,13 @@ __device__ void block_bounds(const SahIn& P, const int64_t* order, int64_t r0, i
 struct NodeGeo {
   double cmin[3], ext[3], sa;
   int axes;  // axes with a positive centroid extent, 0 if no split search
+  int pad;   // explicit, so whole-struct copies read initialised bytes
 };
 
 __device__ __forceinline__ NodeGeo node_geo(const Bounds& B, int64_t count) {
   NodeGeo G;
   G.axes = 0;
+  G.pad = 0;
   G.sa = 0.0;
   for (int a = 0; a < 3; ++a) {
     G.cmin[a] = B.c[a];
@@ -268,14 +270,15 @@ __device__ AxisBest warp_sweep(long long cnt, const double lo[3], const double h
 struct Decision {
   int mode;  // 0 leaf, 1 bin split, 2 halve
   int axis, k;
+  int pad;  // explicit, so whole-struct copies read initialised bytes
   long long nl;
 };
 __device__ __forceinline__ Decision decide(const SahIn& P, int64_t count, int axis,
                                            const AxisBest& b) {
   if (axis >= 0 && (count > P.max_leaf || b.cost < P.c_isect * (double)count))
-    return {1, axis, b.k, b.nl};
-  if (count > P.max_leaf) return {2, -1, -1, (long long)(count / 2)};
-  return {0, -1, -1, 0};
+    return {1, axis, b.k, 0, b.nl};
+  if (count > P.max_leaf) return {2, -1, -1, 0, (long long)(count / 2)};
+  return {0, -1, -1, 0, 0};
 }
 
 __device__ __forceinline__ void push_seg(const Emit& E, int s, int e, int id) {

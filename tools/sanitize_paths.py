@@ -2,7 +2,7 @@
 (tools/gpu_sanitize.sh): ordered + unordered gather, labels, sample
 collection, one training epoch (tiled fwd/bwd, per-head per-row kernel,
 unit-major Adam), fused / split / bucketed (per_object) queries, the native
-engine and device shading."""
+engine, device shading and the GPU SAH build (all three segment classes)."""
 import sys
 from pathlib import Path
 
@@ -43,5 +43,10 @@ for sharing in ("shared", "per_object"):
         if sharing == "shared":
             query_family(model, fam, o, c[:, :w], split=True)
 render(c1(32, 24, subdiv=2), config=RenderConfig(spp=1), backend=BvhBackend())
+from paper_2306_07191_b200 import meshgen  # noqa: E402
+from paper_2306_07191_b200.scene import build_bottoms  # noqa: E402
+meshes = [meshgen.mesh_arrays(*meshgen.icosphere(5)), meshgen.mesh_arrays(*meshgen.torus())]
+for h, d in zip(build_bottoms(meshes, workers=1), build_bottoms(meshes, device="cuda")):
+    assert h.order.tobytes() == d.order.tobytes() and h.node_a.tobytes() == d.node_a.tobytes()
 torch.cuda.synchronize()
 print("sanitize paths ok")
