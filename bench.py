@@ -394,6 +394,20 @@ def main():
         e1.record(stream)
     barrier()
     e2e_ms_local = float(np.sum([e0.elapsed_time(e1) for e0, e1 in e_evs]))
+    # the e2e roofline: pinned host -> device copy bandwidth of this box,
+    # measured on the same stream with one copy of a step's input bytes
+    h2d_src = torch.empty(n * 56, dtype=torch.uint8).pin_memory()
+    h2d_dst = torch.empty(n * 56, dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        h2d_dst.copy_(h2d_src, non_blocking=True)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(5):
+        h2d_dst.copy_(h2d_src, non_blocking=True)
+    c1.record(stream)
+    c1.synchronize()
+    h2d_gbs = n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9
+    del h2d_src, h2d_dst
 
     # --- reduce over ranks (max time) ---------------------------------------
     ms, e2e_ms = ms_local, e2e_ms_local
@@ -482,7 +496,11 @@ def main():
         "rooflines": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n)},
+                "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n),
+                # bound: the host -> device link (the pass itself is ~10x faster)
+                "h2d_achieved_gbs": n * 56 * args.steps / (e2e_ms / 1e3) / 1e9,
+                "h2d_peak_gbs": h2d_gbs,
+                "h2d_frac": (n * 56 * args.steps / (e2e_ms / 1e3) / 1e9) / h2d_gbs},
         # per step: gather_fused, query_tc outer (side stream), query_tc inner
         # (plus two memset nodes for the gather's counters / scan state)
         "gpu_launches": args.steps * 3,
