@@ -156,14 +156,18 @@ __device__ __forceinline__ void sph32f(float x, float y, float z, float n, float
   *v = fast_acos(zz) * (1.0f / CUDART_PI_F);
 }
 
-// The reference's degenerate test sqrt(r.r) < 1e-9 in fp64, exactly: the
-// squared norm is the reference's expression; the fp64 sqrt is only taken
-// when r.r < 1e-17 (otherwise sqrt >= 3.1e-9 and the test is false). The
-// returned norm is fp32 (it only feeds fp32 coordinates).
+// The reference's degenerate test sqrt(r.r) < 1e-9 in fp64, exactly,
+// without the square root: the squared norm is the reference's expression,
+// and since the fp64 sqrt is correctly rounded and monotone,
+// sqrt(r2) < 1e-9  <=>  r2 < T for T the least double with sqrt(T) >= 1e-9,
+// which is the double nearest 1e-18 (0x1.2725dd1d243acp-60; checked with a
+// nextafter search around it). The returned norm is fp32 (it only feeds
+// fp32 coordinates).
 __device__ __forceinline__ bool degenerate_f32(double rx, double ry, double rz, float* rn) {
+  static_assert(kDegenerateRadius == 1e-9, "threshold below is derived for 1e-9");
   const double r2 = rx * rx + ry * ry + rz * rz;
   *rn = sqrtf((float)r2);
-  return r2 < 1e-17 && sqrt(r2) < kDegenerateRadius;
+  return r2 < 1e-18;
 }
 
 constexpr uint64_t kFlagA = 1ull << 62;
