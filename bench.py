@@ -47,8 +47,8 @@ WORKLOADS = {
 # kernels of one visibility pass (names as ncu reports them) and their
 # algorithmic work: see DESIGN.md section 4
 K_GATHER = "gather_warp_kernel"
-K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4>"
-K_INNER = "query_ts_kernel<5, 3, 48, 3, 3, 6>"
+K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4, 0>"
+K_INNER = "query_ts_kernel<5, 3, 48, 3, 3, 6, 0>"
 
 
 def parse():
@@ -339,12 +339,21 @@ def main():
     from paper_2306_07191_b200.pipeline import gather_dev
     sp = _lib.stream_ptr()
     timed("gather", lambda: gather_dev(eng.ds, eng.route, eng.origins, eng.dirs, eng.tmaxs, n, b))
-    timed("query_outer", lambda: L.nif_query_dev(
-        vo, b.outer_obj.data_ptr(), b.outer_ray.data_ptr(), b.outer_coord.data_ptr(), None,
-        b.counts.data_ptr(), b.cap, eng.occ.data_ptr(), None, 0, sp))
-    timed("query_inner", lambda: L.nif_query_dev(
-        vi, b.inner_obj.data_ptr(), b.inner_ray.data_ptr(), b.inner_coord.data_ptr(),
-        b.inner_r.data_ptr(), b.counts.data_ptr() + 8, b.cap, eng.occ.data_ptr(), None, 0, sp))
+    if eng.bucket is not None:  # per_object: the bucketed tensor-core query, as in the frame
+        timed("query_outer", lambda: L.nif_query_bucketed_dev(
+            vo, b.outer_obj.data_ptr(), b.outer_ray.data_ptr(), b.outer_coord.data_ptr(), None,
+            b.counts.data_ptr(), b.cap, eng.occ.data_ptr(), None, eng.bucket[0].data_ptr(), sp))
+        timed("query_inner", lambda: L.nif_query_bucketed_dev(
+            vi, b.inner_obj.data_ptr(), b.inner_ray.data_ptr(), b.inner_coord.data_ptr(),
+            b.inner_r.data_ptr(), b.counts.data_ptr() + 8, b.cap, eng.occ.data_ptr(), None,
+            eng.bucket[1].data_ptr(), sp))
+    else:
+        timed("query_outer", lambda: L.nif_query_dev(
+            vo, b.outer_obj.data_ptr(), b.outer_ray.data_ptr(), b.outer_coord.data_ptr(), None,
+            b.counts.data_ptr(), b.cap, eng.occ.data_ptr(), None, 0, sp))
+        timed("query_inner", lambda: L.nif_query_dev(
+            vi, b.inner_obj.data_ptr(), b.inner_ray.data_ptr(), b.inner_coord.data_ptr(),
+            b.inner_r.data_ptr(), b.counts.data_ptr() + 8, b.cap, eng.occ.data_ptr(), None, 0, sp))
     bvh_out = torch.empty(n, dtype=torch.uint8, device=dev)
     timed("bvh_anyhit", lambda: L.nif_bvh_occluded_dev(
         eng.ds.view, o.data_ptr(), d.data_ptr(), t.data_ptr(), n, bvh_out.data_ptr(), sp))

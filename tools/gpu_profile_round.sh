@@ -3,7 +3,9 @@
 #   bash tools/gpu_profile_round.sh <tag>
 mkdir -p gpurun_out
 TAG=${1:-r1}
+# scene setup builds the BVHs on the GPU: keep those kernels out of the list
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  -k regex:"^(?!sah_|huge_|iota_kernel)" \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --profile --steps 2 --warmup 1 > gpurun_out/${TAG}_launch_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"gather_warp|query_ts" -c 3 -o gpurun_out/${TAG}_full -f \
