@@ -951,6 +951,11 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   __shared__ ObjC objs[kMaxObjFused];
   __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
   __shared__ float s_absmax;
+  // programmatic dependent launch: the query kernel queued behind this one
+  // may start its prologue (weights -> smem, TMEM) on SMs this persistent
+  // grid leaves free; it reads the queues only after griddepcontrol.wait,
+  // i.e. after this grid has completed and flushed
+  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int n_obj = s.n_obj;

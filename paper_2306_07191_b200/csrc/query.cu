@@ -1343,6 +1343,19 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
   const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
   const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
+  // prologue first (barriers, weights -> smem, TMEM): under programmatic
+  // dependent launch it overlaps the tail of the gather that fills the queues
+  if (tid == 0) {
+    for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
+    tc::fence_barrier_init();
+  }
+  if constexpr (!PO) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sW);
+    for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the queues are final from here
   const int64_t n = min(*a.count, a.cap);
   int64_t n_tiles, stride, first;
   if constexpr (PO) {  // contiguous tile range per warpgroup (objects change rarely)
@@ -1362,19 +1375,9 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
     else return load_rec(a, t, trow, n, INNER);
   };
 
-  if (tid == 0) {
-    for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
-    tc::fence_barrier_init();
-  }
   EncIn<N, ND> ea;
   issue_enc<N, ND>(ea, fetch(first), tpos, tdir, tdist, l.R, l.Rd);
   RecIn rb = fetch(first + stride);
-  if constexpr (!PO) {
-    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
-    uint4* dst = reinterpret_cast<uint4*>(sW);
-    for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
-  }
-  if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
   tc::fence_async_smem();
   tc::fence_before_sync();
   __syncthreads();
@@ -1479,7 +1482,18 @@ int launch_ts(const TcArgs& a, cudaStream_t st) {
   const int64_t need = (max_tiles + G - 1) / G;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, 128 * G, smem, st>>>(a);
+  // programmatic dependent launch behind the gather (see query_ts_kernel)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(128 * G);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
   return check_launch("nif_query_dev(tcgen05 TS)");
 }
 
