@@ -398,6 +398,9 @@ __global__ void __launch_bounds__(1024) train_prologue_kernel(const int64_t* __r
                                                               int n_obj, int n_heads,
                                                               int shared) {
   extern __shared__ int hist[];
+  // the step's fused fwd/bwd (programmatic dependent launch) may start now:
+  // it reads the counts written here only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int i = threadIdx.x; i < n_obj; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   idx = batch_idx(idx, cursor);
@@ -754,6 +757,9 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     zs[lr * WP + k] = leaky(zs[lr * WP + k]);
   }
   __syncthreads();
+  // the batch counts (per-object loss scale) come from the step's prologue
+  // kernel; everything above overlaps it under programmatic dependent launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // ---- head + loss: one (row, q) per thread --------------------------------
   const size_t wo_h = (size_t)W * IN + (size_t)(L - 1) * W * W, bo_h = (size_t)L * W;
   const float* swh = sw + T.o_head;
@@ -943,7 +949,17 @@ int launch_fwdbwd_tiled_rb(const TrainArgs& a, cudaStream_t st) {
   const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
   if (my_rows <= 0) return NIF_OK;
   const unsigned grid = (unsigned)((my_rows + RB - 1) / RB);
-  kern<<<grid, TT, smem, st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
   return check_launch("nif_train_fwdbwd_dev(tiled)");
 }
 
