@@ -15,6 +15,7 @@
 //    the geometry head, very wide inputs).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "common.h"
@@ -1039,6 +1040,7 @@ int launch_tc2_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, i
 
 constexpr int kFeatTileBytes = kTileRows * kK1 * 2;  // 4096
 
+
 template <int N, int ND>
 __device__ __forceinline__ RecIn load_rec_row(const int32_t* __restrict__ obj,
                                               const float* __restrict__ coord4,
@@ -1059,8 +1061,17 @@ __device__ __forceinline__ RecIn load_rec_row(const int32_t* __restrict__ obj,
   return r;
 }
 
+// feature row width in 16 B words: the layer-1 inputs plus the bias column
+// in 8 fp16 (outer, 2N + 1 <= 8) -> one word, else two. The MLP kernel
+// zero-fills the missing half of the K = 16 operand.
+template <int N, int ND>
+__host__ __device__ constexpr int feat_words() {
+  return 2 * N + ND + 1 <= 8 ? 1 : 2;
+}
+
 template <int N, int ND>
 __device__ __forceinline__ void store_feat(const EncIn<N, ND>& e, uint8_t* feat, int64_t row) {
+  constexpr int FW = feat_words<N, ND>();
   float x[16];
   finish_enc<N, ND>(e, x);
   uint4 v0, v1;
@@ -1068,19 +1079,21 @@ __device__ __forceinline__ void store_feat(const EncIn<N, ND>& e, uint8_t* feat,
   v0.y = h2u(__floats2half2_rn(x[2], x[3]));
   v0.z = h2u(__floats2half2_rn(x[4], x[5]));
   v0.w = h2u(__floats2half2_rn(x[6], x[7]));
-  v1.x = h2u(__floats2half2_rn(x[8], x[9]));
-  v1.y = h2u(__floats2half2_rn(x[10], x[11]));
-  v1.z = h2u(__floats2half2_rn(x[12], x[13]));
-  v1.w = h2u(__floats2half2_rn(x[14], x[15]));
-  uint4* p = reinterpret_cast<uint4*>(feat) + 2 * row;
+  uint4* p = reinterpret_cast<uint4*>(feat) + FW * row;
   __stcg(p, v0);
-  __stcg(p + 1, v1);
+  if constexpr (FW == 2) {
+    v1.x = h2u(__floats2half2_rn(x[8], x[9]));
+    v1.y = h2u(__floats2half2_rn(x[10], x[11]));
+    v1.z = h2u(__floats2half2_rn(x[12], x[13]));
+    v1.w = h2u(__floats2half2_rn(x[14], x[15]));
+    __stcg(p + 1, v1);
+  }
 }
 
-// Grid-stride over records, two records per thread per iteration and the
-// next iteration's record words prefetched, so each thread keeps two
-// corner-gather round trips and one record fetch in flight.
-template <int N, int ND>
+// Grid-stride over records, K records per thread per iteration and the
+// next iteration's record words prefetched, so each thread keeps K
+// corner-gather round trips and K record fetches in flight.
+template <int N, int ND, int K>
 __global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __restrict__ blob,
                                                            FastLayout l,
                                                            const int32_t* __restrict__ obj,
@@ -1095,22 +1108,26 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const uint8_t* __rest
   const __half* tdist = reinterpret_cast<const __half*>(blob + l.off_dist);
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
   int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  RecIn ra = load_rec_row<N, ND>(obj, coord4, rr, row, n);
-  RecIn rb = load_rec_row<N, ND>(obj, coord4, rr, row + nt, n);
-  for (; row < n_pad; row += 2 * nt) {
-    EncIn<N, ND> ea, eb;
-    issue_enc<N, ND>(ea, ra, tpos, tdir, tdist, l.R, l.Rd);
-    issue_enc<N, ND>(eb, rb, tpos, tdir, tdist, l.R, l.Rd);
-    ra = load_rec_row<N, ND>(obj, coord4, rr, row + 2 * nt, n);
-    rb = load_rec_row<N, ND>(obj, coord4, rr, row + 3 * nt, n);
-    store_feat<N, ND>(ea, feat, row);
-    if (row + nt < n_pad) store_feat<N, ND>(eb, feat, row + nt);
+  RecIn rq[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) rq[k] = load_rec_row<N, ND>(obj, coord4, rr, row + k * nt, n);
+  for (; row < n_pad; row += K * nt) {
+    EncIn<N, ND> e[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) issue_enc<N, ND>(e[k], rq[k], tpos, tdir, tdist, l.R, l.Rd);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      rq[k] = load_rec_row<N, ND>(obj, coord4, rr, row + (K + k) * nt, n);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (row + k * nt < n_pad) store_feat<N, ND>(e[k], feat, row + k * nt);
   }
 }
 
 struct MlpArgs {
   const uint8_t* blob;  // fast blob (weights at offset 0)
-  const uint8_t* feat;  // encoded features, 32 B (16 fp16) per record
+  const uint8_t* feat;  // encoded features, fw x 16 B (8 fp16 each) per record
+  int fw;               // 1 (outer shapes, 2N + 1 <= 8) or 2
   const int32_t* ray;
   const int64_t* count;
   int64_t cap;
@@ -1197,8 +1214,8 @@ __global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) 
   {
     const int64_t row = first * kTileRows + trow;
     if (first < n_tiles && row < n) {
-      f0 = __ldg(F + 2 * row);
-      f1 = __ldg(F + 2 * row + 1);
+      f0 = __ldg(F + a.fw * row);
+      if (a.fw == 2) f1 = __ldg(F + 2 * row + 1);
     }
   }
   {
@@ -1252,8 +1269,8 @@ __global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) 
       f0 = make_uint4(0, 0, 0, 0);
       f1 = f0;
       if (nrow < n) {
-        f0 = __ldg(F + 2 * nrow);
-        f1 = __ldg(F + 2 * nrow + 1);
+        f0 = __ldg(F + a.fw * nrow);
+        if (a.fw == 2) f1 = __ldg(F + 2 * nrow + 1);
       }
     }
     tc::tmem_wait_st();
@@ -1553,8 +1570,9 @@ int launch_encode_tiles(const uint8_t* blob, const FastLayout& l, const int32_t*
   int64_t blocks = (rows + 255) / 256;
   const int64_t max_blocks = (int64_t)sm_count() * 8;  // grid-stride: the count lives on the device
   if (blocks > max_blocks) blocks = max_blocks;
-  encode_tiles_kernel<N, ND><<<(unsigned)blocks, 256, 0, st>>>(blob, l, obj, coord4, r, count, cap,
-                                                               feat);
+  // two records in flight per thread (1: same speed, 4: slower -- C5 sweep)
+  encode_tiles_kernel<N, ND, 2><<<(unsigned)blocks, 256, 0, st>>>(blob, l, obj, coord4, r, count,
+                                                                  cap, feat);
   return check_launch("nif_encode_tiles");
 }
 
@@ -1609,7 +1627,8 @@ int launch_split(const nif_family_view& f, const FastLayout& l, const int32_t* o
     return 0;
   }
 mlp:
-  MlpArgs m{blob, feat, ray, count, cap, occ, logits, g_prof};
+  const int in1 = 2 * f.N + (outer ? 0 : f.Nd) + 1;  // layer-1 inputs + bias (feat_words)
+  MlpArgs m{blob, feat, in1 <= 8 ? 1 : 2, ray, count, cap, occ, logits, g_prof};
 #define NIF_MLP(WW, LL, GG, TT)                                              \
   if (l.W == WW && l.L == LL) {                                              \
     *rc = launch_mlp_tiles<WW, LL, GG, TT>(m, st);                           \

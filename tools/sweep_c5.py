@@ -11,12 +11,16 @@ U(-1, 1), Xavier MLP. Stages are timed separately through the split path
 (nif_query_split_dev flags: 2 = encoding kernel only, 4 = MLP kernel only)
 and the production fused kernel (nif_query_dev) end to end.
 
-Algorithmic work (DESIGN.md section 4):
+Algorithmic work (SURVEY.md 8(d), DESIGN.md section 4):
   encoding bytes / record = record in (obj i32 + 4 x f32 coords [+ f32 r])
-                            + 32 B features out (16 fp16)
-                            -> outer 20 + 32 = 52 B, inner 24 + 32 = 56 B;
-                            table bytes are gathered from L2 (reported
-                            separately as the distinct-table footprint)
+                            + features out (outer 6 fp16, inner 13 fp16)
+                            -> outer 20 + 12 = 32 B, inner 24 + 26 = 50 B
+                            ("frac_hbm"); the kernel writes the MMA-ready
+                            row (outer 16 B: 6 features + bias + pad; inner
+                            32 B), so it moves outer 36 B, inner 56 B
+                            ("frac_hbm_written"); table bytes are gathered
+                            from L2 (reported separately as the
+                            distinct-table footprint)
   MLP useful FLOP / record = 2 (in W + (L-1) W^2 + W)
   MLP executed MMA FLOP / record = 2 (16 W + (L-1) Kp W), Kp = ceil((W+1)/16)*16
 """
@@ -68,6 +72,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--records", type=int, default=1 << 22)
     ap.add_argument("--out", default="")
+    ap.add_argument("--enc-only", action="store_true", help="skip the MLP / fused sweeps")
+    ap.add_argument("--fam", default="outer,inner")
+    ap.add_argument("--R", default="", help="comma list overriding the resolutions")
+    ap.add_argument("--objs", default="1,16")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -103,9 +111,13 @@ def main():
             raise RuntimeError(L.nif_last_error().decode())
 
     # ---- encoding kernel: resolution x objects x order ----------------------
+    fams = a.fam.split(",")
+    r_over = [int(x) for x in a.R.split(",")] if a.R else None
     for which, Rs in (("outer", (64, 128, 256, 512, 1024)), ("inner", (64, 128, 256))):
-        for R in Rs:
-            for n_obj in (1, 16):
+        if which not in fams:
+            continue
+        for R in (r_over or Rs):
+            for n_obj in [int(x) for x in a.objs.split(",")]:
                 cfg = NifConfig(seed=0)
                 cfg.outer.grid_resolution = R
                 cfg.inner.grid_resolution = R
@@ -119,7 +131,8 @@ def main():
                     obj = torch.from_numpy(o_np.astype(np.int32)).to(dev)
                     t = timeit(lambda: run_split(v, obj, which, 2), flush=flush)
                     rec_b = 20 if which == "outer" else 24
-                    b = m * (rec_b + 32)
+                    b = m * (rec_b + (12 if which == "outer" else 26))
+                    bw = m * (rec_b + (16 if which == "outer" else 32))
                     N = fam.N
                     npad = 4 if N <= 4 else 8
                     table = n_obj * 2 * R * R * npad * 2
@@ -127,13 +140,15 @@ def main():
                         "family": which, "R": R, "objects": n_obj, "order": order,
                         "us": t * 1e6, "records_per_s": m / t,
                         "achieved_GBps": b / t / 1e9, "frac_hbm": b / t / 1e9 / peaks["hbm_gbs"],
+                        "written_GBps": bw / t / 1e9,
+                        "frac_hbm_written": bw / t / 1e9 / peaks["hbm_gbs"],
                         "algorithmic_bytes": b, "table_bytes_fp16": table})
                     print(json.dumps(results["encode"][-1]), flush=True)
                 del model
                 torch.cuda.empty_cache()
 
     # ---- MLP kernel: width x depth (features from the encoding kernel) -------
-    for which in ("outer", "inner"):
+    for which in (() if a.enc_only else ("outer", "inner")):
         for W in (64, 128):
             for Lh in (2, 3, 4):
                 cfg = NifConfig(seed=0)
