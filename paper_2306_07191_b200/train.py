@@ -22,6 +22,7 @@ broadcast.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -372,36 +373,59 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
         rng = np.random.default_rng(epoch_ss[e])
         return [rng.permutation(n) if n else None for n in sizes]
 
-    # the next epoch's permutations are drawn on a host thread (numpy's
-    # shuffle releases the GIL) while this epoch is queued and replayed
+    # Later epochs' permutations are drawn on host threads while this epoch is
+    # queued and replayed: each epoch has its own generator, so epochs are
+    # independent, and numpy's shuffle releases the GIL. One 2.7M-sample
+    # permutation takes ~47 ms on one core -- more than the GPU's epoch at
+    # C2 -- so several epochs are drawn at once (bounded to ~1 GB of
+    # permutations in flight).
+    from collections import deque
     from concurrent.futures import ThreadPoolExecutor
-    pool = ThreadPoolExecutor(max_workers=1)
-    nxt = pool.submit(epoch_perms, 0)
+    per_epoch_bytes = 8 * max(1, sum(sizes))
+    depth = max(1, min(4, epochs, (os.cpu_count() or 2) // 2, int(1e9 // per_epoch_bytes)))
+    pool = ThreadPoolExecutor(max_workers=depth)
+    ahead = deque(pool.submit(epoch_perms, k) for k in range(min(depth, epochs)))
+    # The two families are independent optimisers (disjoint parameters,
+    # counts and step counters), so on one GPU each runs its own sequence of
+    # steps -- in the reference's order within the family -- on its own
+    # stream, and the latency-bound steps of one overlap the other's.
+    import contextlib
+    fam_streams = {}
+    if use_graph:
+        cur = torch.cuda.current_stream(model.device)
+        for which in ("outer", "inner"):
+            fam_streams[which] = torch.cuda.Stream(device=model.device)
+            fam_streams[which].wait_stream(cur)
     for e in range(epochs):
-        perms = nxt.result()
-        if e + 1 < epochs:
-            nxt = pool.submit(epoch_perms, e + 1)
+        perms = ahead.popleft().result()
+        if e + depth < epochs:
+            ahead.append(pool.submit(epoch_perms, e + depth))
         for fam, bs, which, obj, coord, label in fams:
             n = int(obj.shape[0])
             if n == 0:
                 continue
             perm_np = perms[fam]
             st = steps[which]
-            st.sq.zero_()
-            if use_graph:
-                if which not in gsteps:
-                    gsteps[which] = _GraphStep(st, obj, coord, label, n, bs)
-                gsteps[which].epoch(perm_np)
-            else:
-                perm = torch.from_numpy(perm_np).to(model.device)
-                base = perm.data_ptr()
-                for k in range(0, n, bs):
-                    m = min(bs, n - k)
-                    st.run(obj, coord, label, None, m, rank, world, group, idx_ptr=base + 8 * k)
-            # the reference's per-batch loss is the mean over rows x outputs
-            width = int(label.shape[1]) if label.dim() > 1 else 1
-            sq[e, fam].copy_(st.sq[0] / width)
+            ctx = torch.cuda.stream(fam_streams[which]) if use_graph else contextlib.nullcontext()
+            with ctx:
+                st.sq.zero_()
+                if use_graph:
+                    if which not in gsteps:
+                        gsteps[which] = _GraphStep(st, obj, coord, label, n, bs)
+                    gsteps[which].epoch(perm_np)
+                else:
+                    perm = torch.from_numpy(perm_np).to(model.device)
+                    base = perm.data_ptr()
+                    for k in range(0, n, bs):
+                        m = min(bs, n - k)
+                        st.run(obj, coord, label, None, m, rank, world, group,
+                               idx_ptr=base + 8 * k)
+                # the reference's per-batch loss is the mean over rows x outputs
+                width = int(label.shape[1]) if label.dim() > 1 else 1
+                sq[e, fam].copy_(st.sq[0] / width)
             counts[fam] = n
+    for s_ in fam_streams.values():
+        torch.cuda.current_stream(model.device).wait_stream(s_)
     pool.shutdown()
     sums_all = sq.cpu().numpy()
     for e in range(epochs):

@@ -1,6 +1,6 @@
 """Per-CUDA-source-line instruction / stall totals from an ncu report.
 
-    python tools/ncu_lines.py report.ncu-rep [top] [function-substring]
+    python tools/ncu_lines.py report.ncu-rep [top] [kernel-base-name[:skip]]
 """
 import csv
 import io
@@ -10,8 +10,11 @@ import sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 want = sys.argv[3] if len(sys.argv) > 3 else ""
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if want:  # kernel base name[:n-th match] (import mode honours -k / --launch-skip)
+    name, _, skip = want.partition(":")
+    cmd[3:3] = ["-k", name] + (["--launch-skip", skip] if skip else [])
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 agg = []
 fname = ""
@@ -22,7 +25,7 @@ for r in rows:
         fname = r[1].split("/")[-1]
         continue
     if len(r) == 2 and r[0] == "Function Name":
-        func_ok = want in r[1]
+        func_ok = True
         continue
     if not func_ok:
         continue
