@@ -405,9 +405,20 @@ __global__ void __launch_bounds__(1024) train_prologue_kernel(const int64_t* __r
   for (int i = threadIdx.x; i < n_obj; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   idx = batch_idx(idx, cursor);
-  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
-    const int64_t o = obj[idx ? idx[r] : r];
-    if (o >= 0 && o < n_obj) atomicAdd(hist + o, 1);
+  // four rows per thread per round, their index and object loads issued
+  // together (the step's latency is two dependent global loads, not eight)
+  for (int64_t r0 = threadIdx.x; r0 < n; r0 += 4 * (int64_t)blockDim.x) {
+    int64_t rows[4], o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t r = r0 + k * (int64_t)blockDim.x;
+      rows[k] = r < n ? (idx ? idx[r] : r) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = rows[k] >= 0 ? obj[rows[k]] : -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (o[k] >= 0 && o[k] < n_obj) atomicAdd(hist + o[k], 1);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_obj || i < n_heads; i += blockDim.x) {
