@@ -410,12 +410,14 @@ def main():
     for _ in range(2):
         h2d_dst.copy_(h2d_src, non_blocking=True)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    c0.record(stream)
-    for _ in range(5):
-        h2d_dst.copy_(h2d_src, non_blocking=True)
-    c1.record(stream)
-    c1.synchronize()
-    h2d_gbs = n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9
+    h2d_gbs = 0.0
+    for _ in range(3):  # best of three trials of five copies (the link is noisy)
+        c0.record(stream)
+        for _ in range(5):
+            h2d_dst.copy_(h2d_src, non_blocking=True)
+        c1.record(stream)
+        c1.synchronize()
+        h2d_gbs = max(h2d_gbs, n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9)
     del h2d_src, h2d_dst
 
     # --- reduce over ranks (max time) ---------------------------------------
