@@ -102,3 +102,16 @@ def test_build_bottoms_on_device(cuda):
     for h, d in zip(host, dev):
         for nm in ("node_lo", "node_hi", "node_a", "node_b", "node_leaf", "order", "v0", "n2"):
             assert getattr(h, nm).tobytes() == getattr(d, nm).tobytes(), nm
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_sah_dev_clustered_and_skewed(seed, cuda):
+    """Quantised coordinates (many equal centroids, bin-boundary ties) and
+    heavy-tailed sizes, so segments cross the warp / CTA / chunked classes
+    at many depths."""
+    g = np.random.default_rng(seed)
+    n = int(g.integers(9000, 60000))
+    base = np.round(g.exponential(2.0, (n, 3)) * 4) / 4 * g.choice([-1, 1], (n, 3))
+    ext = g.exponential(0.05, (n, 3)) * (g.random((n, 1)) < 0.9)
+    lo, hi = base, base + ext
+    _compare(lo, hi, (lo + hi) * 0.5, 4 if seed != 23 else 1, cuda)
