@@ -377,12 +377,19 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     # queued and replayed: each epoch has its own generator, so epochs are
     # independent, and numpy's shuffle releases the GIL. One 2.7M-sample
     # permutation takes ~47 ms on one core -- more than the GPU's epoch at
-    # C2 -- so several epochs are drawn at once (bounded to ~1 GB of
-    # permutations in flight).
+    # C2 -- so several epochs are drawn at once (at C3, 107M samples, one
+    # epoch's permutations are 0.86 GB and take ~1.9 s on one core: up to
+    # 4 GB, and a quarter of the free host memory, are kept in flight).
     from collections import deque
     from concurrent.futures import ThreadPoolExecutor
     per_epoch_bytes = 8 * max(1, sum(sizes))
-    depth = max(1, min(4, epochs, (os.cpu_count() or 2) // 2, int(1e9 // per_epoch_bytes)))
+    budget = 4e9
+    try:
+        import psutil
+        budget = min(budget, 0.25 * psutil.virtual_memory().available)
+    except Exception:  # noqa: BLE001 -- psutil is optional
+        pass
+    depth = max(1, min(4, epochs, (os.cpu_count() or 2) // 2, int(budget // per_epoch_bytes)))
     pool = ThreadPoolExecutor(max_workers=depth)
     ahead = deque(pool.submit(epoch_perms, k) for k in range(min(depth, epochs)))
     # The two families are independent optimisers (disjoint parameters,
