@@ -522,6 +522,11 @@ __device__ __forceinline__ void adam_elem(float& p, float& gr, float& m, float& 
   gr = 0.f;
 }
 
+__device__ __forceinline__ bool changed4(const float4& a, const float4& b) {
+  return (__float_as_uint(a.x) ^ __float_as_uint(b.x)) | (__float_as_uint(a.y) ^ __float_as_uint(b.y)) |
+         (__float_as_uint(a.z) ^ __float_as_uint(b.z)) | (__float_as_uint(a.w) ^ __float_as_uint(b.w));
+}
+
 template <int AV>
 __global__ void __launch_bounds__(256, 4) adam_units_kernel(nif_train_view t, AdamSeg s0, AdamSeg s1,
                                                          AdamSeg s2, AdamSeg s3, AdamSeg s4,
@@ -559,15 +564,19 @@ __global__ void __launch_bounds__(256, 4) adam_units_kernel(nif_train_view t, Ad
     float4* V = reinterpret_cast<float4*>(t.v + base);
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
          e += (int64_t)gridDim.x * blockDim.x) {
-      float4 p = P[e], g = G[e], m = M[e], v = V[e];
+      const float4 p0 = P[e], g0 = G[e], m0 = M[e], v0 = V[e];
+      float4 p = p0, g = g0, m = m0, v = v0;
       adam_elem<AV>(p.x, g.x, m.x, v.x, lr, b1, b2, eps, c1, c2);
       adam_elem<AV>(p.y, g.y, m.y, v.y, lr, b1, b2, eps, c1, c2);
       adam_elem<AV>(p.z, g.z, m.z, v.z, lr, b1, b2, eps, c1, c2);
       adam_elem<AV>(p.w, g.w, m.w, v.w, lr, b1, b2, eps, c1, c2);
-      P[e] = p;
-      G[e] = g;
-      M[e] = m;
-      V[e] = v;
+      // store only what changed bit-wise: cells a step did not touch keep
+      // g == +0 (and, never touched so far, p / m / v too), so most of the
+      // write traffic of a sparsely touched grid is skipped
+      if (changed4(p, p0)) P[e] = p;
+      if (changed4(g, g0)) G[e] = g;
+      if (changed4(m, m0)) M[e] = m;
+      if (changed4(v, v0)) V[e] = v;
     }
   } else {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < sg.per;
