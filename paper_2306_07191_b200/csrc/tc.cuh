@@ -151,8 +151,23 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 // Blocking wait: try_wait suspends the warp until the phase flips (or a
 // hardware time limit), so waiting warps do not steal issue slots.
+// The suspend-time hint (ns) only caps how long a warp sleeps before it
+// retries; it wakes as soon as the phase completes, so a long hint just
+// removes retry instructions from the issue stream.
+#ifndef NIF_MBAR_HINT_NS
+#define NIF_MBAR_HINT_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#if NIF_MBAR_HINT_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TRY_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra TRY_%=;\n\t}" ::"r"(a),
+      "r"(parity), "n"(NIF_MBAR_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "TRY_%=:\n\t"
@@ -160,6 +175,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "@!P1 bra TRY_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // Split TMEM loads: several tcgen05.ld in flight, one wait. tmem_ld_fence
