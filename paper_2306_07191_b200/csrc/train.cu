@@ -679,7 +679,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     for (int e = tid; e < L * W + OUT; e += TT) sb[e] = __ldg(f.b + e);
   }
 
-  // ---- encode (rows 0..RB-1 on threads 0..RB-1) ------------------------------
+  // ---- encode: row setup on threads 0..RB-1 (corner cells and weights into
+  // shared memory), then one (row, input) feature per thread -----------------
   if (tid < RB) {
     const int64_t k_row = (int64_t)blockIdx.x * RB + tid;
     const int64_t g = a.row0 + k_row * a.row_step;
@@ -687,42 +688,16 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     const int64_t* bidx = batch_idx(a.idx, a.cursor);
     const int64_t row = valid ? (bidx ? bidx[g] : g) : 0;
     const int o = valid ? (int)a.obj[row] : 0;
-    float x[kMaxIn];
-#pragma unroll
-    for (int k = 0; k < kMaxIn; ++k) x[k] = 0.f;
     Bil64 bp{}, bd{};
     Axis ad{};
     if (valid) {
       const double* c = a.coord + row * cw;
-      const size_t g2 = (size_t)f.R * f.R * f.N;
-      const float* gp = f.pos + (size_t)o * g2;
-      const float* gd = f.dir + (size_t)o * g2;
       bp = bil64(c[0], c[1], f.R);
       bd = bil64(c[2], c[3], f.R);
-      for (int k = 0; k < f.N; ++k) {
-        const double sp = bp.w[0] * (double)gp[(size_t)bp.c[0] * f.N + k] +
-                          bp.w[1] * (double)gp[(size_t)bp.c[1] * f.N + k] +
-                          bp.w[2] * (double)gp[(size_t)bp.c[2] * f.N + k] +
-                          bp.w[3] * (double)gp[(size_t)bp.c[3] * f.N + k];
-        const double sd = bd.w[0] * (double)gd[(size_t)bd.c[0] * f.N + k] +
-                          bd.w[1] * (double)gd[(size_t)bd.c[1] * f.N + k] +
-                          bd.w[2] * (double)gd[(size_t)bd.c[2] * f.N + k] +
-                          bd.w[3] * (double)gd[(size_t)bd.c[3] * f.N + k];
-        x[k] = (float)sp;
-        x[f.N + k] = (float)sd;
-      }
-      if (f.family == NIF_FAMILY_INNER) {
-        ad = axis_indices(c[4], f.Rd, false);
-        const float* gr = f.dist + (size_t)o * f.Rd * f.Nd;
-        for (int k = 0; k < f.Nd; ++k) {
-          const double s = (1.0 - ad.w) * (double)gr[(size_t)ad.i0 * f.Nd + k] +
-                           ad.w * (double)gr[(size_t)ad.i1 * f.Nd + k];
-          x[2 * f.N + k] = (float)s;
-        }
-      }
+      if (f.family == NIF_FAMILY_INNER) ad = axis_indices(c[4], f.Rd, false);
     }
-    for (int k = 0; k < kMaxIn; ++k) xs[tid * kMaxIn + k] = x[k];
-    // the row's scatter targets, for the backward pass's (row, input) threads
+    // the row's corner cells / weights: the features below and the
+    // backward pass's grid scatter both read them
     for (int c = 0; c < 4; ++c) {
       rwd[tid * 9 + c] = bp.w[c];
       rwd[tid * 9 + 4 + c] = bd.w[c];
@@ -733,6 +708,38 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     rwi[tid * 11 + 8] = ad.i0;
     rwi[tid * 11 + 9] = ad.i1;
     rwi[tid * 11 + 10] = valid ? o : -1;
+  }
+  __syncthreads();
+  {
+    const int IN_ = f.family == NIF_FAMILY_INNER ? 2 * f.N + f.Nd : 2 * f.N;
+    const size_t g2 = (size_t)f.R * f.R * f.N;
+    for (int e = tid; e < RB * kMaxIn; e += TT) {
+      const int r = e / kMaxIn, k = e % kMaxIn;
+      const int o = rwi[r * 11 + 10];
+      float x = 0.f;
+      if (o >= 0 && k < IN_) {
+        // nif.py:286-311 per feature, the reference's corner order in fp64
+        if (k < 2 * f.N) {
+          const bool is_pos = k < f.N;
+          const float* gg = (is_pos ? f.pos : f.dir) + (size_t)o * g2;
+          const int kk = is_pos ? k : k - f.N;
+          const int cb = is_pos ? 0 : 4;
+          const double s = rwd[r * 9 + cb + 0] * (double)gg[(size_t)rwi[r * 11 + cb + 0] * f.N + kk] +
+                           rwd[r * 9 + cb + 1] * (double)gg[(size_t)rwi[r * 11 + cb + 1] * f.N + kk] +
+                           rwd[r * 9 + cb + 2] * (double)gg[(size_t)rwi[r * 11 + cb + 2] * f.N + kk] +
+                           rwd[r * 9 + cb + 3] * (double)gg[(size_t)rwi[r * 11 + cb + 3] * f.N + kk];
+          x = (float)s;
+        } else {
+          const int kk = k - 2 * f.N;
+          const float* gr = f.dist + (size_t)o * f.Rd * f.Nd;
+          const double w = rwd[r * 9 + 8];
+          const double s = (1.0 - w) * (double)gr[(size_t)rwi[r * 11 + 8] * f.Nd + kk] +
+                           w * (double)gr[(size_t)rwi[r * 11 + 9] * f.Nd + kk];
+          x = (float)s;
+        }
+      }
+      xs[r * kMaxIn + k] = x;
+    }
   }
 
   // ---- forward: Z_l = bias + act(prev) . W_l^T (k ascending) ---------------
