@@ -660,21 +660,24 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
 
   // ---- stage the whole MLP once (its loads overlap the encode's) -----------
   {
-    const int n0 = W * IN, nh = (L - 1) * W * W, total = n0 + nh + OUT * W;
-    for (int e = tid; e < total; e += TT) {
-      const float v = __ldg(f.w + e);
-      int d;
-      if (e < n0) {
-        const int j = e / IN;
-        d = j * INP + (e - j * IN);
-      } else if (e < n0 + nh) {
-        const int e2 = e - n0, l = e2 / (W * W), r2 = e2 - l * W * W;
-        d = T.o_h1 + l * W * WP + (r2 / W) * WP + r2 % W;
-      } else {
-        const int e2 = e - n0 - nh;
-        d = T.o_head + (e2 / W) * WP + e2 % W;
-      }
-      sw[d] = v;
+    const int n0 = W * IN;
+    for (int e = tid; e < n0; e += TT) {  // layer 0: rows of IN (odd) floats
+      const int j = e / IN;
+      sw[j * INP + (e - j * IN)] = __ldg(f.w + e);
+    }
+    // hidden layers and head: rows of W floats (W % 16 == 0), read as float4
+    constexpr int Q = W / 4;
+    const int rows = (L - 1) * W + OUT;
+    const float4* src = reinterpret_cast<const float4*>(f.w + n0);
+    for (int e = tid; e < rows * Q; e += TT) {
+      const int rr = e / Q, c4 = e - (e / Q) * Q;
+      const float4 v = __ldg(src + e);
+      const int d = (rr < (L - 1) * W ? T.o_h1 + (rr / W) * W * WP + (rr % W) * WP
+                                      : T.o_head + (rr - (L - 1) * W) * WP) + 4 * c4;
+      sw[d] = v.x;
+      sw[d + 1] = v.y;
+      sw[d + 2] = v.z;
+      sw[d + 3] = v.w;
     }
     for (int e = tid; e < L * W + OUT; e += TT) sb[e] = __ldg(f.b + e);
   }
