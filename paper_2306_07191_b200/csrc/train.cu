@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   const int INP = IN + 1;
   const int OUT = f.dims[f.n_layers];
   const TiledSmem T = tiled_smem(W, RB, L, IN, OUT);
-  float* zs = sm + T.zs;    // [L][RB][WP] pre-activations, then activations
+  float* zs = sm + T.zs;    // [L][RB][WP] activations leaky(z)
   float* dzA = sm + T.dzA;  // [RB][WP]
   float* dzB = sm + T.dzB;  // [RB][WP]
   float* xs = sm + T.xs;    // [RB][kMaxIn]
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const float v = prev[(tr * RPT + i) * ps + k];
-        av[i] = l == 0 ? v : leaky(v);
+        av[i] = v;  // x, or the previous layer's activation
       }
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
@@ -778,15 +778,11 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) z[(tr * RPT + i) * WP + tc + 16 * c] = acc[i][c];
+      for (int c = 0; c < CPT; ++c) z[(tr * RPT + i) * WP + tc + 16 * c] = leaky(acc[i][c]);
   }
-  __syncthreads();
-  // from here on the hidden layers hold activations leaky(z) (same sign as z,
-  // so the backward masks `z > 0` read them unchanged)
-  for (int e = tid; e < L * RB * W; e += TT) {
-    const int lr = e / W, k = e % W;
-    zs[lr * WP + k] = leaky(zs[lr * WP + k]);
-  }
+  // the hidden layers hold activations leaky(z), stored once by their
+  // producer (same sign as z, so the backward masks `z > 0` read them
+  // unchanged)
   __syncthreads();
   // the batch counts (per-object loss scale) come from the step's prologue
   // kernel; everything above overlaps it under programmatic dependent launch
