@@ -14,6 +14,7 @@ from paper_2306_07191_b200.synthetic import c2  # noqa: E402
 from paper_2306_07191_b200.train import _GraphStep, _Step, collect_samples, train  # noqa: E402
 
 torch.cuda.set_device(0)
+VARIANT = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 scene = c2(build_device=torch.device("cuda", 0))
 smp = collect_samples(scene, spp=2, seed=scene.seed)
 model = build_model(NifConfig(seed=0), scene)
@@ -26,6 +27,7 @@ for which, bs in (("outer", 2048), ("inner", 4096)):
     label = getattr(smp, f"{which}_label")
     n = int(obj.shape[0])
     st = _Step(model, which)
+    _lib.lib().nif_debug_set_train_variant(VARIANT)
     g = _GraphStep(st, obj, coord, label, n, bs)
     g.epoch(np.random.default_rng(0).permutation(n))  # captures the graph
     torch.cuda.synchronize()
