@@ -500,6 +500,8 @@ def main():
                    "trained_epochs": args.train_epochs, "l2": "flushed (256 MiB write) per step",
                    "parallelism": f"{ws} independent frames (sample index = rank)"},
         "frame_ms": ms / args.steps,
+        # SURVEY 8(d) metric (i) also asks for (ray, object) records per second
+        "records_per_s": (n_outer + n_inner) * ws * args.steps / (ms / 1e3),
         "bvh_ms_per_frame": kt["bvh_anyhit"],
         "render_ms_per_frame_1spp": render_ms,
         "kernel_ms": kt,
