@@ -1340,6 +1340,9 @@ __global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) 
 // tiles (nif_query_bucketed_dev); each warpgroup walks a contiguous range of
 // tiles and keeps its own copy of the current object's weights, reloading
 // it only when the object changes.
+#ifndef NIF_ENC_ISSUE
+#define NIF_ENC_ISSUE 0  // 0: under the last hidden MMA; k: under the k-th (k=1 spills, slower)
+#endif
 template <int N, int ND, int W, int L, int G, int TPS, bool PO = false>
 __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   using C = MlpCfg<W, L, G>;
@@ -1464,7 +1467,8 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
           tc::mma_f16_ts(acc, a_op + s * 8, tc::smem_desc(wb + s * 256, 128, Kp * 16), idW, s > 0);
         tc::mma_commit(bar);
       }
-      if (layer == L - 1) {  // next tile's gathers in flight under the last MMA + head
+      if (layer == (NIF_ENC_ISSUE > 0 && NIF_ENC_ISSUE < L ? NIF_ENC_ISSUE : L - 1)) {
+        // next tile's gathers in flight under the remaining MMAs + head
         issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
         rb = fetch(t + 2 * stride);
       }
