@@ -1723,6 +1723,33 @@ inline BucketWs bucket_ws(void* scratch, int64_t capacity, int n_obj) {
   return w;
 }
 
+// tile offsets (exclusive scan of padded counts), tile -> object, and the
+// -1 padding rows of each object's last tile; run by one block
+__device__ void bucket_scan_block(const BucketWs& w, int n_obj) {
+  __shared__ int64_t s_off;
+  if (threadIdx.x == 0) {
+    int64_t off = 0;
+    for (int o = 0; o < n_obj; ++o) {
+      w.tile_off[o] = off;
+      off += (__ldcg(w.hist + o) + kTileRows - 1) / kTileRows;
+      w.cursor[o] = 0;
+    }
+    w.tile_off[n_obj] = off;
+    *w.n_tiles = off;
+    s_off = off;
+  }
+  __syncthreads();
+  for (int o = 0; o < n_obj; ++o) {
+    const int64_t t0 = w.tile_off[o], t1 = w.tile_off[o + 1];
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) w.tile_obj[t] = o;
+    // every other slot of the used tiles is written by the scatter
+    for (int64_t p = t0 * kTileRows + __ldcg(w.hist + o) + threadIdx.x; p < t1 * kTileRows;
+         p += blockDim.x)
+      w.perm[p] = -1;
+  }
+  (void)s_off;
+}
+
 __global__ void bucket_hist_kernel(const int32_t* __restrict__ obj,
                                    const int64_t* __restrict__ count, int64_t cap, int n_obj,
                                    int32_t* __restrict__ hist) {
@@ -1738,26 +1765,9 @@ __global__ void bucket_hist_kernel(const int32_t* __restrict__ obj,
     if (sh[o]) atomicAdd(hist + o, sh[o]);
 }
 
-// one block: tile offsets (exclusive scan of padded counts), tile -> object
-__global__ void bucket_scan_kernel(BucketWs w, int n_obj) {
-  __shared__ int64_t s_total;
-  if (threadIdx.x == 0) {
-    int64_t off = 0;
-    for (int o = 0; o < n_obj; ++o) {
-      w.tile_off[o] = off;
-      off += (w.hist[o] + kTileRows - 1) / kTileRows;
-      w.cursor[o] = 0;
-    }
-    w.tile_off[n_obj] = off;
-    *w.n_tiles = off;
-    s_total = off;
-  }
-  __syncthreads();
-  for (int o = 0; o < n_obj; ++o)
-    for (int64_t t = w.tile_off[o] + threadIdx.x; t < w.tile_off[o + 1]; t += blockDim.x)
-      w.tile_obj[t] = o;
-  (void)s_total;
-}
+// one block (a separate launch measured faster than a last-block scan
+// folded into the histogram kernel)
+__global__ void bucket_scan_kernel(BucketWs w, int n_obj) { bucket_scan_block(w, n_obj); }
 
 __global__ void bucket_scatter_kernel(const int32_t* __restrict__ obj,
                                       const int64_t* __restrict__ count, int64_t cap,
@@ -1779,6 +1789,58 @@ __global__ void bucket_scatter_kernel(const int32_t* __restrict__ obj,
       const int rank = __popc(peers & ((1u << lane) - 1u));
       w.perm[w.tile_off[o] * kTileRows + base + rank] = (int32_t)i;
     }
+  }
+}
+
+// Block-aggregated scatter: a block takes a chunk of kBucketChunk records,
+// counts them per object in shared memory, reserves each object's range
+// with one global atomic per (chunk, object) -- not one per (warp, object):
+// a dozen objects made the per-warp reservations serialise on a dozen
+// addresses -- and places each record at its reserved base plus a
+// shared-memory rank. Order within a bucket is irrelevant (per-record
+// logits, OR per ray).
+constexpr int kBucketChunk = 1024;
+
+__device__ __forceinline__ int warp_agg_add(int* ctr, int o, bool v) {
+  const int lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(0xffffffffu, v ? o : -1);
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (v && lane == leader) base = atomicAdd(ctr + o, __popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(peers & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(256) bucket_scatter_block_kernel(
+    const int32_t* __restrict__ obj, const int64_t* __restrict__ count, int64_t cap, BucketWs w,
+    int n_obj) {
+  extern __shared__ int sm_b[];
+  int* s_cnt = sm_b;              // [n_obj] records per object in this chunk
+  int* s_base = sm_b + n_obj;     // [n_obj] reserved base in the object's bucket
+  int* s_rank = sm_b + 2 * n_obj;  // [n_obj] placement counters
+  const int64_t n = min(*count, cap);
+  for (int64_t c0 = (int64_t)blockIdx.x * kBucketChunk; c0 < n;
+       c0 += (int64_t)gridDim.x * kBucketChunk) {
+    const int64_t c1 = min(c0 + (int64_t)kBucketChunk, n);
+    for (int o = threadIdx.x; o < n_obj; o += blockDim.x) s_cnt[o] = s_rank[o] = 0;
+    __syncthreads();
+    for (int64_t b = c0; b < c1; b += blockDim.x) {
+      const int64_t i = b + threadIdx.x;
+      const bool v = i < c1;
+      warp_agg_add(s_cnt, v ? __ldg(obj + i) : 0, v);
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < n_obj; o += blockDim.x)
+      if (s_cnt[o]) s_base[o] = atomicAdd(w.cursor + o, s_cnt[o]);
+    __syncthreads();
+    for (int64_t b = c0; b < c1; b += blockDim.x) {
+      const int64_t i = b + threadIdx.x;
+      const bool v = i < c1;
+      const int o = v ? __ldg(obj + i) : 0;
+      const int r = warp_agg_add(s_rank, o, v);
+      if (v) w.perm[w.tile_off[o] * kTileRows + s_base[o] + r] = (int32_t)i;
+    }
+    __syncthreads();
   }
 }
 
@@ -1880,14 +1942,20 @@ extern "C" int nif_query_bucketed_dev(const nif_family_view* f, const int32_t* o
   cudaStream_t st = (cudaStream_t)stream;
   const BucketWs w = bucket_ws(scratch, capacity, f->n_obj);
   cudaMemsetAsync(w.hist, 0, (size_t)f->n_obj * 4, st);
-  cudaMemsetAsync(w.perm, 0xff, (size_t)w.max_tiles * kTileRows * 4, st);
   int64_t blocks = (capacity + 255) / 256;
   const int64_t cap_blocks = (int64_t)sm_count() * 8;
   if (blocks > cap_blocks) blocks = cap_blocks;
   bucket_hist_kernel<<<(unsigned)blocks, 256, (size_t)f->n_obj * 4, st>>>(obj, count_dev, capacity,
                                                                           f->n_obj, w.hist);
   bucket_scan_kernel<<<1, 256, 0, st>>>(w, f->n_obj);
-  bucket_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(obj, count_dev, capacity, w);
+  if (f->n_obj <= 4096) {
+    int64_t cb = (capacity + kBucketChunk - 1) / kBucketChunk;
+    if (cb > cap_blocks) cb = cap_blocks;
+    bucket_scatter_block_kernel<<<(unsigned)(cb > 0 ? cb : 1), 256, (size_t)f->n_obj * 12, st>>>(
+        obj, count_dev, capacity, w, f->n_obj);
+  } else {
+    bucket_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(obj, count_dev, capacity, w);
+  }
   TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
            logits, nullptr, w.perm, w.tile_obj, w.n_tiles};
   // the tile range is bounded by max_tiles (read from the device count in-kernel)
