@@ -1727,7 +1727,26 @@ inline BucketWs bucket_ws(void* scratch, int64_t capacity, int n_obj) {
 // -1 padding rows of each object's last tile; run by one block
 __device__ void bucket_scan_block(const BucketWs& w, int n_obj) {
   __shared__ int64_t s_off;
-  if (threadIdx.x == 0) {
+  if (n_obj <= 32) {  // one warp: lane o scans object o (no serial chain)
+    if (threadIdx.x < 32) {
+      const int o = threadIdx.x;
+      const int64_t tiles = o < n_obj ? (__ldcg(w.hist + o) + kTileRows - 1) / kTileRows : 0;
+      int64_t incl = tiles;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (o >= d) incl += v;
+      }
+      if (o < n_obj) {
+        w.tile_off[o] = incl - tiles;
+        w.cursor[o] = 0;
+      }
+      if (o == n_obj - 1) {
+        w.tile_off[n_obj] = incl;
+        *w.n_tiles = incl;
+      }
+    }
+  } else if (threadIdx.x == 0) {
     int64_t off = 0;
     for (int o = 0; o < n_obj; ++o) {
       w.tile_off[o] = off;
