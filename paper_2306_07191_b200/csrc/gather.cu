@@ -39,7 +39,8 @@ struct ObjC {
   double lt[3], ht[3];  // lo - tol, hi + tol  (geometry.py:260-262)
   double c[3];          // 0.5 * (lo + hi)     (geometry.py:275-277, 295-297)
   double hn;            // |half diagonal|      (geometry.py:302-305)
-  int id, route, root, pad;
+  int id, route, root;
+  float hinv;           // 1 / (float)hn: the hot path's fp32 r' = |o - c| / hn
 };
 
 struct RayX {
@@ -143,7 +144,10 @@ __device__ __forceinline__ float fast_acos(float z) {
   q = fmaf(q, za, 0.08897905f);
   q = fmaf(q, za, -0.2145988f);
   q = fmaf(q, za, 1.5707963f);
-  const float r = sqrtf(1.0f - za) * q;
+  const float x = 1.0f - za;
+  // sqrt(x) as x * rsqrt(x): MUFU.RSQ alone (within 2 ulp; the map's
+  // tolerance is 2e-7), exact 0 at the pole
+  const float r = (x > 0.f ? x * rsqrtf(x) : 0.f) * q;
   return z < 0.f ? 3.14159265359f - r : r;
 }
 
@@ -315,6 +319,7 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     const double hx = 0.5 * (bx[3] - bx[0]), hy = 0.5 * (bx[4] - bx[1]),
                  hz = 0.5 * (bx[5] - bx[2]);
     b.hn = sqrt(hx * hx + hy * hy + hz * hz);
+    b.hinv = 1.0f / (float)b.hn;
     b.id = ob;
     b.route = route[ob];
     b.root = s.roots[ob];
@@ -515,7 +520,7 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; rr = 0.f; }
         else {
           sph32f((float)rx, (float)ry, (float)rz, rnf, &c4[0], &c4[1]);
-          rr = fminf(rnf / (float)b.hn, 1.0f);
+          rr = fminf(rnf * b.hinv, 1.0f);
         }
         c4[2] = du;
         c4[3] = dv;
@@ -658,6 +663,7 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     const double hx = 0.5 * (bx[3] - bx[0]), hy = 0.5 * (bx[4] - bx[1]),
                  hz = 0.5 * (bx[5] - bx[2]);
     b.hn = sqrt(hx * hx + hy * hy + hz * hz);
+    b.hinv = 1.0f / (float)b.hn;
     b.id = ob;
     b.route = route[ob];
     b.root = s.roots[ob];
@@ -895,7 +901,7 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
             if (deg) { c0 = 0.5f; c1 = 0.5f; rr = 0.f; }
             else {
               sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
-              rr = fminf(rnf / (float)b.hn, 1.0f);
+              rr = fminf(rnf * b.hinv, 1.0f);
             }
             if (ji < out.cap_inner) {
               out.inner_obj[ji] = b.id;
@@ -979,6 +985,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     const double hx = 0.5 * (bx[3] - bx[0]), hy = 0.5 * (bx[4] - bx[1]),
                  hz = 0.5 * (bx[5] - bx[2]);
     b.hn = sqrt(hx * hx + hy * hy + hz * hz);
+    b.hinv = 1.0f / (float)b.hn;
     b.id = ob;
     b.route = route[ob];
     b.root = s.roots[ob];
@@ -1128,7 +1135,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         if (deg) { c0 = 0.5f; c1 = 0.5f; rr = 0.f; }
         else {
           sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
-          rr = fminf(rnf / (float)b.hn, 1.0f);
+          rr = fminf(rnf * b.hinv, 1.0f);  // within 1 ulp of rnf / hn (fp32)
         }
         if (ji < out.cap_inner) {
           out.inner_obj[ji] = b.id;
