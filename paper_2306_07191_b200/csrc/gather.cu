@@ -151,11 +151,12 @@ __device__ __forceinline__ float fast_acos(float z) {
   return z < 0.f ? 3.14159265359f - r : r;
 }
 
-__device__ __forceinline__ void sph32f(float x, float y, float z, float n, float* u, float* v) {
+// ninv: 1 / |(x, y, z)| (1 for unit directions)
+__device__ __forceinline__ void sph32f(float x, float y, float z, float ninv, float* u, float* v) {
   float uu = fmaf(fast_atan2(y, x), 0.5f / CUDART_PI_F, 0.5f);
   if (uu >= 1.0f) uu -= 1.0f;
   else if (uu < 0.0f) uu += 1.0f;
-  const float zz = fminf(fmaxf(__fdividef(z, n), -1.0f), 1.0f);
+  const float zz = fminf(fmaxf(z * ninv, -1.0f), 1.0f);
   *u = uu;
   *v = fast_acos(zz) * (1.0f / CUDART_PI_F);
 }
@@ -167,10 +168,17 @@ __device__ __forceinline__ void sph32f(float x, float y, float z, float n, float
 // which is the double nearest 1e-18 (0x1.2725dd1d243acp-60; checked with a
 // nextafter search around it). The returned norm is fp32 (it only feeds
 // fp32 coordinates).
-__device__ __forceinline__ bool degenerate_f32(double rx, double ry, double rz, float* rn) {
+__device__ __forceinline__ bool degenerate_f32(double rx, double ry, double rz, float* rn,
+                                               float* rinv) {
   static_assert(kDegenerateRadius == 1e-9, "threshold below is derived for 1e-9");
   const double r2 = rx * rx + ry * ry + rz * rz;
-  *rn = sqrtf((float)r2);
+  // fp32 norm and inverse from one MUFU.RSQ (within 2 ulp; both only feed
+  // fp32 coordinates); not used for a degenerate record (r2 < 1e-18 keeps
+  // (float)r2 a normal number otherwise)
+  const float r2f = (float)r2;
+  const float ri = rsqrtf(r2f);
+  *rn = r2f * ri;
+  *rinv = ri;
   return r2 < 1e-18;
 }
 
@@ -503,10 +511,10 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy,
                      ez = r.oz + hh.t0 * r.dz;
         const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
-        float rnf;
-        deg = degenerate_f32(rx, ry, rz, &rnf);
+        float rnf, rinvf;
+        deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
         if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; }
-        else sph32f((float)rx, (float)ry, (float)rz, rnf, &c4[0], &c4[1]);
+        else sph32f((float)rx, (float)ry, (float)rz, rinvf, &c4[0], &c4[1]);
         c4[2] = du;
         c4[3] = dv;
       }
@@ -515,11 +523,11 @@ gather_fused_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         deg = transform_inner(r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, b.lo, b.hi, cc);
       } else {
         const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
-        float rnf;
-        deg = degenerate_f32(rx, ry, rz, &rnf);
+        float rnf, rinvf;
+        deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
         if (deg) { c4[0] = 0.5f; c4[1] = 0.5f; rr = 0.f; }
         else {
-          sph32f((float)rx, (float)ry, (float)rz, rnf, &c4[0], &c4[1]);
+          sph32f((float)rx, (float)ry, (float)rz, rinvf, &c4[0], &c4[1]);
           rr = fminf(rnf * b.hinv, 1.0f);
         }
         c4[2] = du;
@@ -873,7 +881,7 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
           m &= ~(3ull << (2 * k));
           const ObjC& b = objs[k];
           float c0, c1, rr = 0.f;
-          float rnf;
+          float rnf, rinvf;
           bool deg;
           if (kind == 1) {
             if (!have_inv) {
@@ -886,9 +894,9 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
             const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy,
                          ez = r.oz + hh.t0 * r.dz;
             const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
-            deg = degenerate_f32(rx, ry, rz, &rnf);
+            deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
             if (deg) { c0 = 0.5f; c1 = 0.5f; }
-            else sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+            else sph32f((float)rx, (float)ry, (float)rz, rinvf, &c0, &c1);
             if (jo < out.cap_outer) {
               out.outer_obj[jo] = b.id;
               out.outer_ray[jo] = (int32_t)i;
@@ -897,10 +905,10 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
             ++jo;
           } else {
             const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
-            deg = degenerate_f32(rx, ry, rz, &rnf);
+            deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
             if (deg) { c0 = 0.5f; c1 = 0.5f; rr = 0.f; }
             else {
-              sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+              sph32f((float)rx, (float)ry, (float)rz, rinvf, &c0, &c1);
               rr = fminf(rnf * b.hinv, 1.0f);
             }
             if (ji < out.cap_inner) {
@@ -1114,15 +1122,15 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       m &= ~(3ull << (2 * k));
       const ObjC& b = objs[k];
       float c0, c1, rr = 0.f;
-      float rnf;
+      float rnf, rinvf;
       bool deg;
       if (kind == 1) {
         const Hit3 hh = slab(r, b);
         const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy, ez = r.oz + hh.t0 * r.dz;
         const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
-        deg = degenerate_f32(rx, ry, rz, &rnf);
+        deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
         if (deg) { c0 = 0.5f; c1 = 0.5f; }
-        else sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+        else sph32f((float)rx, (float)ry, (float)rz, rinvf, &c0, &c1);
         if (jo < out.cap_outer) {
           out.outer_obj[jo] = b.id;
           out.outer_ray[jo] = (int32_t)i;
@@ -1131,10 +1139,10 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         ++jo;
       } else {
         const double rx = r.ox - b.c[0], ry = r.oy - b.c[1], rz = r.oz - b.c[2];
-        deg = degenerate_f32(rx, ry, rz, &rnf);
+        deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
         if (deg) { c0 = 0.5f; c1 = 0.5f; rr = 0.f; }
         else {
-          sph32f((float)rx, (float)ry, (float)rz, rnf, &c0, &c1);
+          sph32f((float)rx, (float)ry, (float)rz, rinvf, &c0, &c1);
           rr = fminf(rnf * b.hinv, 1.0f);  // within 1 ulp of rnf / hn (fp32)
         }
         if (ji < out.cap_inner) {
