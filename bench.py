@@ -307,6 +307,16 @@ def main():
                 graph.replay()
             torch.cuda.synchronize()
         barrier()
+        # gate the stream behind a sleep on a side stream while all K steps
+        # are queued, so host jitter (the clock sampler, the OS) can never
+        # leave the GPU idle inside a timed step
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(int(50e6))  # ~25 ms at 1.9 GHz
+        gate = torch.cuda.Event()
+        gate.record(side)
+        stream.wait_event(gate)
         for e0, e1 in evs:
             flush.fill_(1.0)
             e0.record(stream)
