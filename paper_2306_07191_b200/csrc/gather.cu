@@ -961,7 +961,8 @@ __global__ void __launch_bounds__(kThreads, NIF_GATHER_MINB_U)
 gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
                    const double* __restrict__ org, const double* __restrict__ dir,
                    const double* __restrict__ tms, int64_t n, nif_gather_out out,
-                   unsigned long long* __restrict__ reserve, unsigned int* __restrict__ done) {
+                   unsigned long long* __restrict__ reserve, unsigned int* __restrict__ done,
+                   unsigned int* __restrict__ tail) {
   __shared__ ObjC objs[kMaxObjFused];
   __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
   __shared__ float s_absmax;
@@ -1006,7 +1007,21 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   const int64_t nw = (int64_t)gridDim.x * (kThreads / 32);
   const float absmax = s_absmax;
   int deg_count = 0;
-  for (int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + warp; c < n_chunks; c += nw) {
+  // every warp takes n_chunks / nw chunks statically (interleaved), the
+  // remainder is handed out one chunk at a time on demand, so warps that
+  // drew cheap chunks absorb the tail instead of idling
+  const int64_t wid = (int64_t)blockIdx.x * (kThreads / 32) + warp;
+  const int64_t rounds = n_chunks / nw;
+  for (int64_t k = 0;; ++k) {
+    int64_t c;
+    if (k < rounds) {
+      c = wid + k * nw;
+    } else {
+      unsigned int t = 0;
+      if (lane == 0) t = atomicAdd(tail, 1u);
+      c = rounds * nw + __shfl_sync(0xffffffffu, t, 0);
+      if (c >= n_chunks) break;
+    }
     const int64_t i = c * 32 + lane;
     const bool valid = i < n;
     RayX r{};
@@ -1213,7 +1228,7 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
   int* ctr = (int*)(ws + align_up((size_t)tiles * 8, 256));
   const bool unordered = out->rec_kind == nullptr && g_gprof == nullptr && g_gather_variant == 0;
   if (!unordered) cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
-  else cudaMemsetAsync(ctr, 0, 16, st);  // reservation counter + done counter
+  else cudaMemsetAsync(ctr, 0, 16, st);  // reservation, done and tail counters
   if (out->rec_kind != nullptr)
     gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
@@ -1226,7 +1241,8 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
     if (grid * (kThreads / 32) > chunks) grid = (chunks + kThreads / 32 - 1) / (kThreads / 32);
     gather_warp_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, (unsigned long long*)ctr,
-        (unsigned int*)((unsigned long long*)ctr + 1));
+        (unsigned int*)((unsigned long long*)ctr + 1),
+        (unsigned int*)((unsigned long long*)ctr + 1) + 1);
   } else {
     const int smem = kStages * kStageBytes;
     static bool attr = false;
