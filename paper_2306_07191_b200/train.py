@@ -277,7 +277,8 @@ class _GraphStep:
         self.turn ^= 1
         if self.copied[k] is not None:
             self.copied[k].synchronize()  # that buffer's previous copy is done
-        self.host[k][:n].numpy()[:] = perm_host
+        # torch's copy runs on the intra-op thread pool (C3: 0.7 GB per epoch)
+        self.host[k][:n].copy_(torch.from_numpy(perm_host))
         self.perm[:n].copy_(self.host[k][:n], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
