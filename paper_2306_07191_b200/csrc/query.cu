@@ -39,6 +39,9 @@ constexpr int kTpc = 1;
 // fast blob layout
 // ---------------------------------------------------------------------------
 
+#ifndef NIF_CPACK8
+#define NIF_CPACK8 1  // corner-packed 64 B entries for 8-latent tables (inner family)
+#endif
 struct FastLayout {
   int W, L, in_dim, Kp, NP, NPd, R, Rd, N, Nd, n_obj;
   size_t off_w1, off_hidden, off_head, off_headf, w_bytes;
@@ -79,8 +82,8 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   // loads. With 8 latents per cell (inner) the packed entry would be 64 B
   // for the same four 16 B loads and a 4x larger footprint (measured
   // slower at R <= 128), so those stay one cell per 16 B. 1-D: corner pairs.
-  const size_t tab = l.NP == 4 ? (size_t)f.n_obj * f.R * (f.R + 1) * 4 * l.NP * 2
-                               : (size_t)f.n_obj * f.R * f.R * l.NP * 2;
+  const size_t tab = (l.NP == 4 || NIF_CPACK8) ? (size_t)f.n_obj * f.R * (f.R + 1) * 4 * l.NP * 2
+                                              : (size_t)f.n_obj * f.R * f.R * l.NP * 2;
   l.off_dir = al16(l.off_pos + tab);
   l.off_dist = al16(l.off_dir + tab);
   const size_t dtab =
@@ -159,7 +162,7 @@ __global__ void pack_weights_kernel(nif_family_view f, FastLayout l, uint8_t* bl
 // floor(v R - 0.5) = jq - 1. 1-D entry jq in [0, Rd]: (clamp(jq-1), clamp(jq)).
 __global__ void pack_tables_kernel(nif_family_view f, FastLayout l, uint8_t* blob) {
   const int R = l.R, Rd = l.Rd;
-  const bool quad = l.NP == 4;
+  const bool quad = l.NP == 4 || NIF_CPACK8;
   const int64_t ent2 = quad ? (int64_t)l.n_obj * R * (R + 1) * 4 : (int64_t)l.n_obj * R * R;
   const int64_t ent1 = f.family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * (Rd + 1) * 2 : 0;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -457,13 +460,17 @@ __device__ __forceinline__ void issue_enc(EncIn<N, ND>& e, const RecIn& r, const
   e.ray = r.ray;
   e.rec = r.rec;
   if (!r.valid) return;
-  if constexpr (NP == 4) {  // corner-packed 32 B entries: one 256-bit load each
+  if constexpr (NP == 4 || NIF_CPACK8) {  // corner-packed entries: 32 B (NP 4) or 64 B (NP 8)
     const size_t g2 = (size_t)R * (R + 1) * NQ;  // uint4 per object table
     const BilQ bp = bilinear_q(r.c.x, r.c.y, R), bd = bilinear_q(r.c.z, r.c.w, R);
     const uint4* P = reinterpret_cast<const uint4*>(tpos) + (size_t)r.obj * g2 + (size_t)bp.q * NQ;
     const uint4* D = reinterpret_cast<const uint4*>(tdir) + (size_t)r.obj * g2 + (size_t)bd.q * NQ;
     ldg256(P, e.qp[0], e.qp[1]);
     ldg256(D, e.qd[0], e.qd[1]);
+    if constexpr (NQ == 4) {
+      ldg256(P + 2, e.qp[2], e.qp[3]);
+      ldg256(D + 2, e.qd[2], e.qd[3]);
+    }
     e.wp[0] = bp.w00; e.wp[1] = bp.w01; e.wp[2] = bp.w10; e.wp[3] = bp.w11;
     e.wd[0] = bd.w00; e.wd[1] = bd.w01; e.wd[2] = bd.w10; e.wd[3] = bd.w11;
   } else {  // one 16 B cell per corner
@@ -1881,7 +1888,7 @@ extern "C" int nif_fast_pack_dev(const nif_family_view* f, void* blob, void* str
     pack_weights_kernel<<<dim3((nw + 255) / 256, f->n_heads), 256, 0, st>>>(*f, l,
                                                                             (uint8_t*)blob);
   }
-  const int64_t cells = 2 * (l.NP == 4 ? (int64_t)l.n_obj * l.R * (l.R + 1) * 4
+  const int64_t cells = 2 * ((l.NP == 4 || NIF_CPACK8) ? (int64_t)l.n_obj * l.R * (l.R + 1) * 4
                                       : (int64_t)l.n_obj * l.R * l.R) +
                         (f->family == NIF_FAMILY_INNER ? (int64_t)l.n_obj * (l.Rd + 1) * 2 : 0);
   pack_tables_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, st>>>(*f, l, (uint8_t*)blob);
