@@ -51,6 +51,15 @@ K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4, 0>"
 K_INNER = "query_ts_kernel<5, 3, 48, 3, 3, 6, 0>"
 
 
+def workload_label(args):
+    """The workload string of the configuration actually run (resolution
+    overrides included)."""
+    base = WORKLOADS[args.config]
+    if args.config != "c1" and (args.width, args.height) != (1920, 1080):
+        base = base.replace("1920x1080", f"{args.width}x{args.height}")
+    return base
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -180,11 +189,12 @@ def cpu_path_step(scene, model, rays_np, n):
     return one
 
 
-def cpu_baseline_leg(scene, model, rays_np, max_rays=20000, budget_s=20.0):
-    """Oracle port of the reference CPU path on a bounded sample, all host
-    threads (cmd_bench method: 1 warm-up + median of up to 5)."""
+def cpu_baseline_leg(scene, model, rays_np, config, budget_s=20.0):
+    """Oracle port of the reference CPU path on the whole frame, all host
+    threads (cmd_bench method: 1 warm-up + median of up to 5 within the
+    budget)."""
     from oracle import oracle
-    n = min(len(rays_np[0]), max_rays)
+    n = len(rays_np[0])
     one = cpu_path_step(scene, model, rays_np, n)
     one()
     times = []
@@ -195,8 +205,8 @@ def cpu_baseline_leg(scene, model, rays_np, max_rays=20000, budget_s=20.0):
         times.append(time.perf_counter() - t0)
     med = float(np.median(times))
     return {"value": n / med, "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
-            "sample": f"{n} C2 shadow rays (first {n} of the frame), gather+encode+MLP, "
-                      f"median of {len(times)}"}
+            "sample": f"the whole {config.upper()} frame ({n} shadow rays): gather + encode + "
+                      f"row-sequential MLP + per-ray OR, median of {len(times)}"}
 
 
 def run_reference(args, rank, ws):
@@ -387,7 +397,33 @@ def main():
         render_ms[name] = e0.elapsed_time(e1) / 5
     del nif_be
 
-    # --- e2e through the public API with pinned host buffers ----------------
+    # --- e2e through the drop-in plugin: NifBackend.occluded (the reference's
+    # PredictorBackend.occluded, renderer.py:675-683) on pageable numpy rays,
+    # answered through the native engine's C-ABI (pinned staging ring,
+    # upload / staging copy / device pass of neighbouring chunks overlapped);
+    # synchronous host call, timed on the host clock around each call
+    from paper_2306_07191_b200.pipeline import ShadowRays
+    rays_host = ShadowRays(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+    plugin = NifBackend(model)
+    want = eng.occ[:n].cpu().numpy().astype(bool)
+    got = plugin.occluded(scene, rays_host)
+    e2e_parity = bool(np.array_equal(got, want))
+    for _ in range(args.warmup):
+        plugin.occluded(scene, rays_host)
+    barrier()
+    e2e_s = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plugin.occluded(scene, rays_host)
+        e2e_s.append(time.perf_counter() - t0)
+    barrier()
+    e2e_ms_local = float(np.sum(e2e_s)) * 1e3
+    staging = plugin.native_engine(scene, n).info()
+
+    # the same on pinned torch tensors through VisibilityEngine.occluded_host
+    # (the bound the staging ring is measured against)
     ho = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     hd = torch.empty((n, 3), dtype=torch.float64).pin_memory()
     ht = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -395,24 +431,18 @@ def main():
     hd.copy_(d)
     ht.copy_(t)
     hocc = torch.empty(n, dtype=torch.uint8).pin_memory()
-
-    def e2e_step():
-        # public host API: chunked, H2D of chunk k+1 overlapped with the pass
-        # over chunk k, D2H of each chunk's answer as soon as it is final
-        eng.occluded_host(ho, hd, ht, hocc, n, chunks=args.e2e_chunks)
-
     for _ in range(args.warmup):
-        e2e_step()
-    barrier()
-    e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        eng.occluded_host(ho, hd, ht, hocc, n, chunks=args.e2e_chunks)
+    torch.cuda.synchronize()
+    p_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(args.steps)]
-    for e0, e1 in e_evs:
+    for e0, e1 in p_evs:
         flush.fill_(1.0)
         e0.record(stream)
-        e2e_step()
+        eng.occluded_host(ho, hd, ht, hocc, n, chunks=args.e2e_chunks)
         e1.record(stream)
-    barrier()
-    e2e_ms_local = float(np.sum([e0.elapsed_time(e1) for e0, e1 in e_evs]))
+    torch.cuda.synchronize()
+    pinned_ms = float(np.sum([e0.elapsed_time(e1) for e0, e1 in p_evs]))
     # the e2e roofline: pinned host -> device copy bandwidth of this box,
     # measured on the same stream with one copy of a step's input bytes
     h2d_src = torch.empty(n * 56, dtype=torch.uint8).pin_memory()
@@ -493,9 +523,8 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and not args.profile:
         try:
-            rays_np = (o[:20000].cpu().numpy(), d[:20000].cpu().numpy(),
-                       t[:20000].cpu().numpy())
-            cpu = cpu_baseline_leg(scene, model, rays_np)
+            rays_np = (rays_host.origins, rays_host.dirs, rays_host.tmaxs)
+            cpu = cpu_baseline_leg(scene, model, rays_np, args.config)
         except Exception as e:  # the checker must never hide the main number
             cpu = {"value": None, "error": str(e)[:200]}
 
@@ -504,7 +533,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp16-mma/fp32-acc (fp64 gather)",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "rays_per_frame_per_gpu": n,
+        "config": {"workload": workload_label(args), "rays_per_frame_per_gpu": n,
                    "outer_records": n_outer,
                    "inner_records": n_inner, "model": f"NifConfig() defaults (R 256/128), sharing={args.sharing}",
                    "trained_epochs": args.train_epochs, "l2": "flushed (256 MiB write) per step",
@@ -520,10 +549,15 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n),
+                "api": "NifBackend.occluded(scene, ShadowRays of numpy f64 arrays) -> bool[n] "
+                       "(native engine, C-ABI nif_engine_occluded_host)",
+                "parity_with_device_path": e2e_parity,
+                "staging": staging,
                 # bound: the host -> device link (the pass itself is ~10x faster)
                 "h2d_achieved_gbs": n * 56 * args.steps / (e2e_ms / 1e3) / 1e9,
                 "h2d_peak_gbs": h2d_gbs,
-                "h2d_frac": (n * 56 * args.steps / (e2e_ms / 1e3) / 1e9) / h2d_gbs},
+                "h2d_frac": (n * 56 * args.steps / (e2e_ms / 1e3) / 1e9) / h2d_gbs,
+                "pinned_torch_value": n_total * args.steps / (pinned_ms / 1e3)},
         # per step: gather_fused, query_tc outer (side stream), query_tc inner
         # (plus two memset nodes for the gather's counters / scan state)
         "gpu_launches": args.steps * 3,

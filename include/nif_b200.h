@@ -228,30 +228,6 @@ int nif_query_bucketed_dev(const nif_family_view* f, const int32_t* obj, const i
                               when instantiated, else generic) */
 #define NIF_IMPL_TCGEN05_GENERIC 3 /* force the runtime-shape tcgen05 kernel */
 
-/* Diagnostics: when buf != NULL the tcgen05 query kernel records clock64()
- * phase stamps of its first 4 tiles per CTA into buf[cta][4][16].      */
-int nif_debug_set_prof(void* buf);
-/* Same for the gather (one-tile-per-CTA variant): buf[tile][8].        */
-int nif_debug_set_prof_gather(void* buf);
-/* Gather hot-path variant: 0 unordered warp-chunk compaction (default;
- * queue order is arbitrary, per-ray results identical), 1 one tile per CTA
- * with look-back (reference order), 2 persistent TMA-pipelined look-back
- * (reference order). All produce the same records.                     */
-int nif_debug_set_gather_variant(int v);
-/* Culling statistics of the hot-path gather since the last call (rays,
- * bundle survivors, prefilter survivors, classified hits); only in a
- * library built with -DNIF_GATHER_STATS (tools/gather_stats.py).       */
-int nif_debug_gather_stats(unsigned long long* out4);
-/* Query-kernel variant (benchmarks / equivalence tests): 0 fused with the
- * A operand in TMEM (default); 1 / 9 shared-memory-operand specialisations
- * (6 / 4 tiles per SM); 2 runtime-shape generic kernel; 11 TMEM operand,
- * one tile per CTA.                                                     */
-int nif_debug_set_query_variant(int v);
-/* Training fwd/bwd kernel: 0 tiled CTA-GEMM kernel where it applies
- * (shared MLP, width a multiple of 16; 16 rows x 256 threads; default),
- * 1 one row per thread, 2 tiled 32 x 128, 3 tiled 32 x 256.            */
-int nif_debug_set_train_variant(int v);
-
 /* occ_ray |= bvh_occ (renderer.py:680-683 seeds the OR with bvh_occ).  */
 int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_ray, void* stream);
 
@@ -369,21 +345,32 @@ int nif_label_geometry_dev(const nif_scene_view* s, const int32_t* rec_obj,
 
 /* ---- native engine: the whole pass behind one handle ------------------
  * (SURVEY.md §8b "nif_occluded"; replaces PredictorBackend.occluded,
- * renderer.py:675-683, for FFI callers with rays in host memory). The
- * engine owns the ray buffers, record queues, gather workspace and, for
- * per_object models, the bucketing scratch, for up to `capacity` rays;
- * scene / route / families are views of caller-owned device memory (call
- * nif_fast_pack_dev after optimiser steps, then nif_engine_update_model).
- * nif_engine_occluded_host: host rays in, one byte per ray out (1 =
- * shadowed), synchronous; chunk k+1's upload overlaps chunk k's pass.   */
+ * renderer.py:675-683, of a NifBackend, nif.py:486-499, for FFI callers
+ * with rays in host memory). The engine owns the device ray buffers
+ * (`capacity` rays), the record queues (a few slots per ray, grown when a
+ * chunk overflows), the gather workspace, the per_object bucketing scratch
+ * and a ring of pinned host staging slots; scene / route / families are
+ * views of caller-owned device memory.
+ * producer_stream: the stream the caller enqueued the model's
+ * nif_fast_pack_dev on (NULL = legacy stream); the engine's streams wait
+ * for it before the next query, so a repack can never be read half-written.
+ * After optimiser steps: repack, then nif_engine_update_model.
+ * nif_engine_occluded_host: pageable host rays in, one byte per ray out
+ * (1 = shadowed), synchronous. Rays stream through the pinned ring in
+ * chunks (chunks = 0: 256K-ray chunks; > 0: at least that many chunks):
+ * the staging memcpy of chunk k+1 (host thread pool), its upload and the
+ * device pass of chunk k overlap.
+ * nif_engine_info: out4 = {chunk rays, record slots per ray, staging
+ * threads, overflow re-runs so far}.                                     */
 typedef struct nif_engine nif_engine;
 int nif_engine_create(const nif_scene_view* scene, const uint8_t* route_dev, int32_t n_net_obj,
                       const nif_family_view* outer, const nif_family_view* inner,
-                      int64_t capacity, nif_engine** out_engine);
+                      int64_t capacity, void* producer_stream, nif_engine** out_engine);
 int nif_engine_update_model(nif_engine* e, const nif_family_view* outer,
-                            const nif_family_view* inner);
+                            const nif_family_view* inner, void* producer_stream);
 int nif_engine_occluded_host(nif_engine* e, const double* origins, const double* dirs,
                              const double* tmaxs, int64_t n, uint8_t* occ_out, int32_t chunks);
+int nif_engine_info(const nif_engine* e, int64_t* out4);
 int nif_engine_destroy(nif_engine* e);
 
 /* One progressive sample's shading (renderer.py:826-849): for the n_cast

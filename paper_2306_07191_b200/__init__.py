@@ -14,7 +14,7 @@ from .meshgen import ground_plane, icosphere, mesh_arrays, torus
 from .nif import (
     AdamParams, InnerConfig, NifConfig, NifModel, OuterConfig, build_model,
     encode_inner_arrays, encode_outer_arrays, forward_inner_arrays, forward_outer_arrays,
-    infer_occlusion, infer_records, logits_arrays,
+    infer_geometry, infer_occlusion, infer_records, logits_arrays,
 )
 from .pipeline import (
     BvhBackend, HdrImage, NativeEngine, NifBackend, OracleBackend, PredictorBackend, RenderConfig,

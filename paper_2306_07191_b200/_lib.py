@@ -150,8 +150,9 @@ _SIGS = {
     "nif_feat_scratch_bytes": (C.c_size_t, [I64]),
     "nif_bucket_scratch_bytes": (C.c_size_t, [I64, I32]),
     "nif_engine_create": (C.c_int, [C.POINTER(SceneView), P, I32, C.POINTER(FamilyView),
-                                    C.POINTER(FamilyView), I64, C.POINTER(C.c_void_p)]),
-    "nif_engine_update_model": (C.c_int, [P, C.POINTER(FamilyView), C.POINTER(FamilyView)]),
+                                    C.POINTER(FamilyView), I64, P, C.POINTER(C.c_void_p)]),
+    "nif_engine_update_model": (C.c_int, [P, C.POINTER(FamilyView), C.POINTER(FamilyView), P]),
+    "nif_engine_info": (C.c_int, [P, P]),
     "nif_engine_occluded_host": (C.c_int, [P, P, P, P, I64, P, I32]),
     "nif_engine_destroy": (C.c_int, [P]),
     "nif_query_bucketed_dev": (C.c_int, [C.POINTER(FamilyView), P, P, P, P, P, I64, P, P, P, P]),
@@ -198,6 +199,7 @@ def declared_symbols():
     """Every function the public header declares (for the export test)."""
     import re
     hdr = (_HERE.parent / "include" / "nif_b200.h").read_text()
+    hdr += (_HERE.parent / "include" / "nif_b200_debug.h").read_text()
     return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(nif_\w+)\s*\(",
                                  hdr, re.M)))
 

@@ -10,9 +10,11 @@ written here loads in the reference and vice versa; malformed files raise
 SceneFormatError with the reference's messages.
 
 Optimiser state (not part of NIF1, whose reader rejects trailing bytes) is
-written to an optional sidecar `<path>.adam` (b"NIFA": per family the flat
-m / v buffers and the per-tensor step counters) so training can resume on
-the device.
+written to an optional sidecar `<path>.adam` (b"NIFA", the sha256 of the
+NIF1 file it belongs to, then per family the flat m / v buffers and the
+per-tensor step counters) so training can resume on the device. Saving
+without `adam` removes a stale sidecar; a sidecar whose digest does not
+match the checkpoint beside it is rejected.
 """
 
 from __future__ import annotations
@@ -49,8 +51,23 @@ def save_checkpoint(model: NifModel, path, adam: bool = False) -> None:
             fh.write(struct.pack("<I", a.ndim))
             fh.write(struct.pack(f"<{a.ndim}Q", *a.shape))
             fh.write(a.tobytes())
+    side = Path(str(path) + ".adam")
     if adam:
-        _save_adam(model, Path(str(path) + ".adam"))
+        _save_adam(model, side, _digest(path))
+    elif side.exists():
+        # a sidecar from an earlier save would otherwise be restored with
+        # these weights on the next load
+        side.unlink()
+
+
+def _digest(path) -> bytes:
+    """sha256 of a NIF1 file: binds an Adam sidecar to the exact weights."""
+    import hashlib
+    h = hashlib.sha256()
+    with open(path, "rb") as fh:
+        for block in iter(lambda: fh.read(1 << 20), b""):
+            h.update(block)
+    return h.digest()
 
 
 def _read_exact(fh, n: int, path) -> bytes:
@@ -97,7 +114,7 @@ def load_checkpoint(path, into: Optional[NifModel] = None, device=None) -> NifMo
     _install(model, arrays)
     side = Path(str(path) + ".adam")
     if side.exists():
-        _load_adam(model, side)
+        _load_adam(model, side, _digest(path))
     return model
 
 
@@ -116,9 +133,10 @@ def _install(model: NifModel, arrays) -> None:
     model.load_arrays(heads["outer"], heads["inner"], grids)
 
 
-def _save_adam(model: NifModel, path: Path) -> None:
+def _save_adam(model: NifModel, path: Path, digest: bytes) -> None:
     with open(path, "wb") as fh:
         fh.write(ADAM_MAGIC)
+        fh.write(digest)
         for fam in (model.outer, model.inner):
             for t in (fam.m, fam.v):
                 a = t.detach().cpu().numpy().astype("<f4")
@@ -130,11 +148,14 @@ def _save_adam(model: NifModel, path: Path) -> None:
                 fh.write(a.tobytes())
 
 
-def _load_adam(model: NifModel, path: Path) -> None:
+def _load_adam(model: NifModel, path: Path, digest: bytes) -> None:
     import torch
     with open(path, "rb") as fh:
         if _read_exact(fh, 4, path) != ADAM_MAGIC:
             raise SceneFormatError(f"{path}: not an optimiser-state sidecar")
+        if _read_exact(fh, 32, path) != digest:
+            raise SceneFormatError(
+                f"{path}: optimiser state belongs to a different checkpoint")
         for fam in (model.outer, model.inner):
             for t, dt, w in ((fam.m, "<f4", 4), (fam.v, "<f4", 4), (fam.grid_steps, "<i8", 8),
                              (fam.mlp_steps, "<i8", 8)):

@@ -1,33 +1,137 @@
 // Native visibility engine: the whole split pass behind one C-ABI object
 // (SURVEY.md §8b "nif_occluded (fused whole path)"), for FFI callers that
-// hold rays in host memory -- the drop-in for PredictorBackend.occluded
-// (renderer.py:675-683) / NifBackend (nif.py:486-499) from a ctypes stub.
+// hold rays in (pageable) host memory -- the drop-in for
+// PredictorBackend.occluded (renderer.py:675-683) / NifBackend
+// (nif.py:486-499) from a ctypes stub.
 //
 // The engine owns every device buffer of the pass for a fixed ray capacity:
 // rays, the gather's record queues and workspace, the per-ray answer and,
-// for per_object models, the bucketing scratch of each family. One call
-// copies a chunk of rays in, runs gather -> outer / inner query (the two
-// families on two streams) and copies the chunk's answer out; chunk k+1's
-// host->device copy is issued on a copy stream while chunk k computes.
-// Scene and model stay owned by the caller (views of device memory, e.g.
-// built by the Python package); call nif_fast_pack_dev after each optimiser
-// step before the next query, as for nif_query_dev.
+// for per_object models, the bucketing scratch of each family -- plus a
+// ring of pinned host staging slots. One call streams the caller's rays
+// through the ring in chunks:
+//
+//   host threads: memcpy chunk k (pageable -> pinned slot k % S)
+//   copy stream : H2D of slot k                      (overlaps chunk k-1's pass)
+//   main stream : gather -> outer || inner query of chunk k
+//   d2h stream  : the chunk's answer bytes -> pinned out slot -> caller
+//
+// so the PCIe upload, the staging memcpy (spread over a small pool of host
+// threads) and the device pass of neighbouring chunks all overlap.
+//
+// Record queues hold `slots_per_ray` records per ray of a chunk (a bound, not
+// the worst case n_obj): the gather never writes past it and always reports
+// the true totals, so a chunk that overflowed is detected from its counts
+// and re-run after the queues grow.
+//
+// Scene and model stay owned by the caller (views of device memory). After
+// an optimiser step, repack (nif_fast_pack_dev) and call
+// nif_engine_update_model with the stream the pack was enqueued on: the
+// engine's streams wait for it before the next query.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <new>
+#include <thread>
+#include <vector>
 
 #include "kernels.h"
 #include "nif_b200.h"
 #include "status.h"
 
+namespace {
+
+// A few persistent host threads for the pageable <-> pinned staging copies.
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  int size() const { return (int)threads_.size() + 1; }
+  // runs fn(i) for i in [0, parts) on the pool plus the calling thread
+  void run(int parts, const std::function<void(int)>& fn) {
+    if (threads_.empty() || parts <= 1) {
+      for (int i = 0; i < parts; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_ = &fn;
+      next_ = 0;
+      parts_ = parts;
+      pending_ = parts;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      int i;
+      const std::function<void(int)>* fn;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (fn_ == nullptr || next_ >= parts_) return;
+        i = next_++;
+        fn = fn_;
+      }
+      (*fn)(i);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int next_ = 0, parts_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+constexpr int kSlots = 3;                 // staging ring depth
+constexpr int64_t kChunkRays = 1 << 18;   // default chunk: 256K rays, 14.7 MB in
+constexpr int kMaxChunks = 4096;
+
+}  // namespace
+
 struct nif_engine {
   nif_scene_view scene;
   nif_family_view outer, inner;
   const uint8_t* route;  // device
-  int64_t capacity = 0;
+  int64_t capacity = 0;  // rays
   int n_net = 0;
+  int64_t chunk_cap = 0;       // rays per chunk (staging slot size)
+  int64_t slots_per_ray = 0;   // record slots per ray of a chunk, per queue
+  int64_t qcap = 0;            // record slots per queue = chunk_cap * slots_per_ray
   double* org = nullptr;
   double* dir = nullptr;
   double* tms = nullptr;
@@ -36,10 +140,19 @@ struct nif_engine {
   void* workspace = nullptr;
   size_t ws_bytes = 0;
   void* bucket[2] = {nullptr, nullptr};
-  int64_t* counts = nullptr;
+  int64_t* counts = nullptr;     // device [4]
   nif_gather_out out{};
-  cudaStream_t main = nullptr, side = nullptr, copy = nullptr;
-  cudaEvent_t ev_side = nullptr, ev_join = nullptr;
+  // pinned staging ring
+  uint8_t* pin_in[kSlots] = {};   // chunk_cap * 56 B: o | d | t
+  uint8_t* pin_out[kSlots] = {};  // chunk_cap B
+  int64_t* pin_counts = nullptr;  // [kMaxChunks][4] per-chunk record totals
+  cudaEvent_t ev_in[kSlots] = {};    // H2D of the slot done (slot reusable)
+  cudaEvent_t ev_out[kSlots] = {};   // D2H into the out slot done
+  cudaEvent_t ev_pass[kSlots] = {};  // pass of the slot's chunk done (main)
+  cudaStream_t main = nullptr, side = nullptr, copy = nullptr, d2h = nullptr;
+  cudaEvent_t ev_side = nullptr, ev_join = nullptr, ev_model = nullptr;
+  CopyPool* pool = nullptr;
+  int64_t overflow_reruns = 0;
 };
 
 namespace {
@@ -51,55 +164,47 @@ int dev_alloc(T** p, size_t bytes) {
   return NIF_OK;
 }
 
+void free_queues(nif_engine* e) {
+  for (void** p : {&e->queues, &e->bucket[0], &e->bucket[1]})
+    if (*p) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+}
+
 void release(nif_engine* e) {
-  for (void* p : {(void*)e->org, (void*)e->dir, (void*)e->tms, (void*)e->occ, e->queues,
-                  e->workspace, e->bucket[0], e->bucket[1], (void*)e->counts})
+  free_queues(e);
+  for (void* p : {(void*)e->org, (void*)e->dir, (void*)e->tms, (void*)e->occ, e->workspace,
+                  (void*)e->counts})
     if (p) cudaFree(p);
-  if (e->ev_side) cudaEventDestroy(e->ev_side);
-  if (e->ev_join) cudaEventDestroy(e->ev_join);
-  for (cudaStream_t s : {e->main, e->side, e->copy})
+  for (int s = 0; s < kSlots; ++s) {
+    if (e->pin_in[s]) cudaFreeHost(e->pin_in[s]);
+    if (e->pin_out[s]) cudaFreeHost(e->pin_out[s]);
+    for (cudaEvent_t ev : {e->ev_in[s], e->ev_out[s], e->ev_pass[s]})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (e->pin_counts) cudaFreeHost(e->pin_counts);
+  for (cudaEvent_t ev : {e->ev_side, e->ev_join, e->ev_model})
+    if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t s : {e->main, e->side, e->copy, e->d2h})
     if (s) cudaStreamDestroy(s);
+  delete e->pool;
   delete e;
 }
 
-}  // namespace
-
-extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* route_dev,
-                                 int32_t n_net_obj, const nif_family_view* outer,
-                                 const nif_family_view* inner, int64_t capacity,
-                                 nif_engine** out_engine) {
-  if (out_engine == nullptr) return nif::fail(NIF_ERR_VALUE, "engine: null output handle");
-  *out_engine = nullptr;
-  if (capacity <= 0) return nif::fail(NIF_ERR_VALUE, "engine capacity must be positive");
-  if (outer == nullptr || inner == nullptr || outer->fast == nullptr || inner->fast == nullptr)
-    return nif::fail(NIF_ERR_VALUE, "engine needs both families packed (nif_fast_pack_dev)");
-  nif_engine* e = new (std::nothrow) nif_engine();
-  if (e == nullptr) return nif::fail(NIF_ERR_CUDA, "engine: out of host memory");
-  e->scene = *scene;
-  e->outer = *outer;
-  e->inner = *inner;
-  e->route = route_dev;
-  e->capacity = capacity;
-  e->n_net = n_net_obj > 0 ? n_net_obj : 1;
-  const int64_t cap = capacity * e->n_net;  // record slots per queue (gather bound)
-  int rc = NIF_OK;
-  // queues: outer obj/ray/coord4, inner obj/ray/coord4/r
-  // 7 arrays, each rounded up to 256 B by carve()
+// (re)allocate the record queues for qcap slots each
+int alloc_queues(nif_engine* e, int64_t slots_per_ray) {
+  free_queues(e);
+  e->slots_per_ray = slots_per_ray;
+  const int64_t cap = e->chunk_cap * slots_per_ray;
+  e->qcap = cap;
+  // outer obj/ray/coord4, inner obj/ray/coord4/r; 7 arrays, 256 B aligned
   const size_t qbytes = (size_t)cap * (4 + 4 + 16) + (size_t)cap * (4 + 4 + 16 + 4) + 8 * 256;
-  e->ws_bytes = nif_gather_workspace_bytes(capacity);
-  if ((rc = dev_alloc(&e->org, (size_t)capacity * 24)) || (rc = dev_alloc(&e->dir, (size_t)capacity * 24)) ||
-      (rc = dev_alloc(&e->tms, (size_t)capacity * 8)) || (rc = dev_alloc(&e->occ, (size_t)capacity)) ||
-      (rc = dev_alloc(&e->queues, qbytes)) || (rc = dev_alloc(&e->workspace, e->ws_bytes)) ||
-      (rc = dev_alloc(&e->counts, 4 * sizeof(int64_t)))) {
-    release(e);
-    return rc;
-  }
-  if (outer->n_heads > 1) {
-    const size_t nb = nif_bucket_scratch_bytes(cap, outer->n_obj);
-    if ((rc = dev_alloc(&e->bucket[0], nb)) || (rc = dev_alloc(&e->bucket[1], nb))) {
-      release(e);
-      return rc;
-    }
+  int rc = dev_alloc(&e->queues, qbytes);
+  if (rc) return rc;
+  if (e->outer.n_heads > 1) {
+    const size_t nb = nif_bucket_scratch_bytes(cap, e->outer.n_obj);
+    if ((rc = dev_alloc(&e->bucket[0], nb)) || (rc = dev_alloc(&e->bucket[1], nb))) return rc;
   }
   uint8_t* q = (uint8_t*)e->queues;
   auto carve = [&](size_t bytes) {
@@ -114,37 +219,123 @@ extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* rou
   e->out.inner_ray = (int32_t*)carve((size_t)cap * 4);
   e->out.inner_coord = (float*)carve((size_t)cap * 16);
   e->out.inner_r = (float*)carve((size_t)cap * 4);
-  if ((size_t)(q - (uint8_t*)e->queues) > qbytes) {
-    release(e);
+  if ((size_t)(q - (uint8_t*)e->queues) > qbytes)
     return nif::fail(NIF_ERR_CUDA, "engine: queue carve overflow");
-  }
   e->out.cap_outer = cap;
   e->out.cap_inner = cap;
   e->out.counts = e->counts;
-  if (cudaStreamCreateWithFlags(&e->main, cudaStreamNonBlocking) != cudaSuccess ||
+  return NIF_OK;
+}
+
+// the engine's streams wait for work the caller enqueued on `producer`
+// (e.g. nif_fast_pack_dev of the model the engine is about to read)
+void wait_producer(nif_engine* e, void* producer) {
+  cudaEventRecord(e->ev_model, (cudaStream_t)producer);
+  cudaStreamWaitEvent(e->main, e->ev_model, 0);
+  cudaStreamWaitEvent(e->side, e->ev_model, 0);
+}
+
+}  // namespace
+
+extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* route_dev,
+                                 int32_t n_net_obj, const nif_family_view* outer,
+                                 const nif_family_view* inner, int64_t capacity,
+                                 void* producer_stream, nif_engine** out_engine) {
+  if (out_engine == nullptr) return nif::fail(NIF_ERR_VALUE, "engine: null output handle");
+  *out_engine = nullptr;
+  if (capacity <= 0) return nif::fail(NIF_ERR_VALUE, "engine capacity must be positive");
+  if (outer == nullptr || inner == nullptr || outer->fast == nullptr || inner->fast == nullptr)
+    return nif::fail(NIF_ERR_VALUE, "engine needs both families packed (nif_fast_pack_dev)");
+  if (outer->sigmoid_head != 1 || inner->sigmoid_head != 1)
+    return nif::fail(NIF_ERR_VALUE, "model was built with the geometry head");
+  nif_engine* e = new (std::nothrow) nif_engine();
+  if (e == nullptr) return nif::fail(NIF_ERR_CUDA, "engine: out of host memory");
+  e->scene = *scene;
+  e->outer = *outer;
+  e->inner = *inner;
+  e->route = route_dev;
+  e->capacity = capacity;
+  e->n_net = n_net_obj > 0 ? n_net_obj : 1;
+  e->chunk_cap = std::min<int64_t>(capacity, kChunkRays);
+  int rc = NIF_OK;
+  e->ws_bytes = nif_gather_workspace_bytes(e->chunk_cap);
+  if ((rc = dev_alloc(&e->org, (size_t)capacity * 24)) ||
+      (rc = dev_alloc(&e->dir, (size_t)capacity * 24)) ||
+      (rc = dev_alloc(&e->tms, (size_t)capacity * 8)) ||
+      (rc = dev_alloc(&e->occ, (size_t)capacity)) ||
+      (rc = dev_alloc(&e->workspace, e->ws_bytes)) ||
+      (rc = dev_alloc(&e->counts, 4 * sizeof(int64_t)))) {
+    release(e);
+    return rc;
+  }
+  // a shadow ray meets only a few network-routed boxes; start at 4 slots per
+  // ray (C2: 1.16 records per ray) and grow on overflow
+  if ((rc = alloc_queues(e, std::min(e->n_net, 4)))) {
+    release(e);
+    return rc;
+  }
+  for (int s = 0; s < kSlots; ++s) {
+    if (cudaHostAlloc((void**)&e->pin_in[s], (size_t)e->chunk_cap * 56, cudaHostAllocDefault) !=
+            cudaSuccess ||
+        cudaHostAlloc((void**)&e->pin_out[s], (size_t)e->chunk_cap, cudaHostAllocDefault) !=
+            cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_in[s], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_out[s], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_pass[s], cudaEventDisableTiming) != cudaSuccess) {
+      release(e);
+      return nif::fail(NIF_ERR_CUDA, "engine: pinned staging allocation failed");
+    }
+  }
+  if (cudaHostAlloc((void**)&e->pin_counts, sizeof(int64_t) * 4 * kMaxChunks,
+                    cudaHostAllocDefault) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->main, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_side, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->ev_model, cudaEventDisableTiming) != cudaSuccess) {
     release(e);
     return nif::fail(NIF_ERR_CUDA, "engine: stream / event creation failed");
   }
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int threads = (int)std::max(1u, std::min(8u, hw > 1 ? hw / 2 : 1u));
+  e->pool = new (std::nothrow) CopyPool(threads - 1);
+  if (e->pool == nullptr) {
+    release(e);
+    return nif::fail(NIF_ERR_CUDA, "engine: out of host memory");
+  }
+  wait_producer(e, producer_stream);
   *out_engine = e;
   return NIF_OK;
 }
 
 extern "C" int nif_engine_update_model(nif_engine* e, const nif_family_view* outer,
-                                       const nif_family_view* inner) {
+                                       const nif_family_view* inner, void* producer_stream) {
   if (e == nullptr) return nif::fail(NIF_ERR_VALUE, "engine: null handle");
+  if (outer == nullptr || inner == nullptr || outer->fast == nullptr || inner->fast == nullptr)
+    return nif::fail(NIF_ERR_VALUE, "engine needs both families packed (nif_fast_pack_dev)");
+  if (outer->sigmoid_head != 1 || inner->sigmoid_head != 1)
+    return nif::fail(NIF_ERR_VALUE, "model was built with the geometry head");
   e->outer = *outer;
   e->inner = *inner;
+  wait_producer(e, producer_stream);
+  return NIF_OK;
+}
+
+extern "C" int nif_engine_info(const nif_engine* e, int64_t* out4) {
+  if (e == nullptr || out4 == nullptr) return nif::fail(NIF_ERR_VALUE, "engine: null argument");
+  out4[0] = e->chunk_cap;
+  out4[1] = e->slots_per_ray;
+  out4[2] = e->pool->size();
+  out4[3] = e->overflow_reruns;
   return NIF_OK;
 }
 
 namespace {
 
 // the pass over rays [s0, s1) of the resident buffers, on e->main (outer
-// family forked onto e->side and joined back)
+// family forked onto e->side and joined back); ray ids are chunk-relative
 int run_range(nif_engine* e, int64_t s0, int64_t s1) {
   const int64_t n = s1 - s0;
   nif_gather_out out = e->out;
@@ -174,6 +365,23 @@ int run_range(nif_engine* e, int64_t s0, int64_t s1) {
   return rc;
 }
 
+// pageable -> pinned (or back) over the copy pool, in ~1 MB pieces
+void pooled_copy(CopyPool* pool, std::vector<std::pair<void*, const void*>>& dst_src,
+                 std::vector<size_t>& bytes) {
+  constexpr size_t kPiece = 1 << 20;
+  struct Piece {
+    uint8_t* d;
+    const uint8_t* s;
+    size_t n;
+  };
+  std::vector<Piece> pieces;
+  for (size_t k = 0; k < bytes.size(); ++k)
+    for (size_t off = 0; off < bytes[k]; off += kPiece)
+      pieces.push_back({(uint8_t*)dst_src[k].first + off, (const uint8_t*)dst_src[k].second + off,
+                        std::min(kPiece, bytes[k] - off)});
+  pool->run((int)pieces.size(), [&](int i) { std::memcpy(pieces[i].d, pieces[i].s, pieces[i].n); });
+}
+
 }  // namespace
 
 extern "C" int nif_engine_occluded_host(nif_engine* e, const double* origins,
@@ -185,36 +393,75 @@ extern "C" int nif_engine_occluded_host(nif_engine* e, const double* origins,
     return nif::fail(NIF_ERR_VALUE, "%lld rays exceed the engine capacity %lld", (long long)n,
                      (long long)e->capacity);
   if (n == 0) return NIF_OK;
-  if (chunks < 1) chunks = 1;
-  const int64_t step = (n + chunks - 1) / chunks;
-  cudaEvent_t ready[64];
-  const int nc = (int)std::min<int64_t>((n + step - 1) / step, 64);
-  const int64_t step2 = (n + nc - 1) / nc;
-  for (int k = 0; k < nc; ++k) cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
-  for (int k = 0; k < nc; ++k) {  // all copies in, in order, on the copy stream
-    const int64_t s0 = k * step2, s1 = std::min(n, s0 + step2);
-    cudaMemcpyAsync(e->org + 3 * s0, origins + 3 * s0, (size_t)(s1 - s0) * 24,
-                    cudaMemcpyHostToDevice, e->copy);
-    cudaMemcpyAsync(e->dir + 3 * s0, dirs + 3 * s0, (size_t)(s1 - s0) * 24,
-                    cudaMemcpyHostToDevice, e->copy);
-    cudaMemcpyAsync(e->tms + s0, tmaxs + s0, (size_t)(s1 - s0) * 8, cudaMemcpyHostToDevice,
-                    e->copy);
-    cudaEventRecord(ready[k], e->copy);
-  }
+  // chunk size: the staging slot, or smaller when the caller asks for more
+  // chunks (more overlap on small batches)
+  int64_t step = e->chunk_cap;
+  if (chunks > 0) step = std::min(step, (n + chunks - 1) / chunks);
+  step = std::max<int64_t>(step, (n + kMaxChunks - 1) / kMaxChunks);
+  if (step > e->chunk_cap) return nif::fail(NIF_ERR_VALUE, "engine: too many rays per call");
+  const int nc = (int)((n + step - 1) / step);
   int rc = NIF_OK;
-  for (int k = 0; k < nc && rc == NIF_OK; ++k) {  // chunk k computes as k+1 streams in
-    const int64_t s0 = k * step2, s1 = std::min(n, s0 + step2);
-    cudaStreamWaitEvent(e->main, ready[k], 0);
+  auto drain = [&](int k) {  // chunk k's answer: pinned out slot -> caller
+    const int s = k % kSlots;
+    const int64_t s0 = (int64_t)k * step, s1 = std::min(n, s0 + step);
+    cudaEventSynchronize(e->ev_out[s]);
+    std::memcpy(occ_out + s0, e->pin_out[s], (size_t)(s1 - s0));
+  };
+  for (int k = 0; k < nc && rc == NIF_OK; ++k) {
+    const int s = k % kSlots;
+    const int64_t s0 = (int64_t)k * step, s1 = std::min(n, s0 + step), m = s1 - s0;
+    if (k >= kSlots) {
+      cudaEventSynchronize(e->ev_in[s]);  // the slot's previous upload is done
+      drain(k - kSlots);                  // and its previous answer is out
+    }
+    uint8_t* pin = e->pin_in[s];
+    std::vector<std::pair<void*, const void*>> ds = {
+        {pin, origins + 3 * s0}, {pin + m * 24, dirs + 3 * s0}, {pin + m * 48, tmaxs + s0}};
+    std::vector<size_t> bytes = {(size_t)m * 24, (size_t)m * 24, (size_t)m * 8};
+    pooled_copy(e->pool, ds, bytes);
+    cudaMemcpyAsync(e->org + 3 * s0, pin, (size_t)m * 24, cudaMemcpyHostToDevice, e->copy);
+    cudaMemcpyAsync(e->dir + 3 * s0, pin + m * 24, (size_t)m * 24, cudaMemcpyHostToDevice,
+                    e->copy);
+    cudaMemcpyAsync(e->tms + s0, pin + m * 48, (size_t)m * 8, cudaMemcpyHostToDevice, e->copy);
+    cudaEventRecord(e->ev_in[s], e->copy);
+    cudaStreamWaitEvent(e->main, e->ev_in[s], 0);
     rc = run_range(e, s0, s1);
-    if (rc == NIF_OK)
-      cudaMemcpyAsync(occ_out + s0, e->occ + s0, (size_t)(s1 - s0), cudaMemcpyDeviceToHost,
-                      e->main);
+    if (rc != NIF_OK) break;
+    cudaMemcpyAsync(e->pin_counts + 4 * k, e->counts, 4 * sizeof(int64_t),
+                    cudaMemcpyDeviceToHost, e->main);
+    cudaEventRecord(e->ev_pass[s], e->main);
+    cudaStreamWaitEvent(e->d2h, e->ev_pass[s], 0);
+    cudaMemcpyAsync(e->pin_out[s], e->occ + s0, (size_t)m, cudaMemcpyDeviceToHost, e->d2h);
+    cudaEventRecord(e->ev_out[s], e->d2h);
   }
+  if (rc == NIF_OK)
+    for (int k = std::max(0, nc - kSlots); k < nc; ++k) drain(k);
   const cudaError_t err = cudaStreamSynchronize(e->main);
   cudaStreamSynchronize(e->copy);
-  for (int k = 0; k < nc; ++k) cudaEventDestroy(ready[k]);
+  cudaStreamSynchronize(e->d2h);
   if (rc != NIF_OK) return rc;
   if (err != cudaSuccess) return nif::fail(NIF_ERR_CUDA, "engine: %s", cudaGetErrorString(err));
+  // overflowed chunks: grow the queues to the largest total seen and re-run
+  // them (their rays are still resident)
+  const int64_t qcap_run = e->qcap;
+  auto total = [&](int k) { return std::max(e->pin_counts[4 * k], e->pin_counts[4 * k + 1]); };
+  int64_t need = 0;
+  for (int k = 0; k < nc; ++k) need = std::max(need, total(k));
+  if (need > qcap_run) {
+    // a chunk holds at most chunk_cap * n_net records per queue
+    const int64_t want = (need + need / 4 + e->chunk_cap - 1) / e->chunk_cap;
+    if ((rc = alloc_queues(e, std::min<int64_t>(e->n_net, want)))) return rc;
+    for (int k = 0; k < nc; ++k) {
+      if (total(k) <= qcap_run) continue;
+      const int64_t s0 = (int64_t)k * step, s1 = std::min(n, s0 + step);
+      ++e->overflow_reruns;
+      if ((rc = run_range(e, s0, s1))) return rc;
+      cudaMemcpyAsync(occ_out + s0, e->occ + s0, (size_t)(s1 - s0), cudaMemcpyDeviceToHost,
+                      e->main);
+      if (cudaStreamSynchronize(e->main) != cudaSuccess)
+        return nif::fail(NIF_ERR_CUDA, "engine: re-run failed");
+    }
+  }
   return NIF_OK;
 }
 
@@ -223,6 +470,7 @@ extern "C" int nif_engine_destroy(nif_engine* e) {
   cudaStreamSynchronize(e->main);
   cudaStreamSynchronize(e->side);
   cudaStreamSynchronize(e->copy);
+  cudaStreamSynchronize(e->d2h);
   release(e);
   return NIF_OK;
 }

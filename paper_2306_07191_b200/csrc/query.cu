@@ -44,6 +44,7 @@ constexpr int kTpc = 1;
 #endif
 struct FastLayout {
   int W, L, in_dim, Kp, NP, NPd, R, Rd, N, Nd, n_obj;
+  int HD;  // head outputs: 1 (occlusion logit) or 4 (geometry: normal + depth)
   size_t off_w1, off_hidden, off_head, off_headf, w_bytes;
   size_t w_stride_blob;  // bytes between the weight blocks of two heads
   int n_heads;
@@ -70,8 +71,10 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   l.off_w1 = 0;
   l.off_hidden = l.off_w1 + (size_t)l.W * kK1 * 2;
   l.off_head = l.off_hidden + (size_t)(l.L > 0 ? l.L - 1 : 0) * l.W * l.Kp * 2;
-  l.off_headf = l.off_head + (size_t)16 * l.Kp * 2;  // fp32 head row + bias (CUDA-core head)
-  l.w_bytes = l.off_headf + ((size_t)(l.W + 1) * 4 + 15) / 16 * 16;
+  // fp32 head rows [HD][W] then the HD biases (CUDA-core head)
+  l.HD = f.dims[f.n_layers];
+  l.off_headf = l.off_head + (size_t)16 * l.Kp * 2;
+  l.w_bytes = l.off_headf + ((size_t)l.HD * (l.W + 1) * 4 + 15) / 16 * 16;
   // one weight block per head (per_object sharing: one MLP per object)
   l.n_heads = f.n_heads;
   l.w_stride_blob = al16(l.w_bytes);
@@ -96,7 +99,8 @@ __host__ __device__ inline FastLayout make_layout(const nif_family_view& f) {
   const bool inst = (f.family == NIF_FAMILY_OUTER && (f.N == 2 || f.N == 3 || f.N == 4)) ||
                     (f.family == NIF_FAMILY_INNER &&
                      ((f.N == 5 && (f.Nd == 3 || f.Nd == 4)) || (f.N == 4 && f.Nd == 3)));
-  l.tc_ok = inst && f.n_heads >= 1 && f.sigmoid_head == 1 && f.dims[f.n_layers] == 1 &&
+  const bool head_ok = (f.sigmoid_head == 1 && l.HD == 1) || (f.sigmoid_head == 0 && l.HD == 4);
+  l.tc_ok = inst && f.n_heads >= 1 && head_ok &&
             l.L >= 1 && hidden_same && l.W % 16 == 0 && l.W >= 16 && l.W <= 240 &&
             l.in_dim + 1 <= kK1;
   return l;
@@ -118,11 +122,12 @@ __global__ void pack_weights_kernel(nif_family_view f, FastLayout l, uint8_t* bl
   const int n1 = l.W * kK1;
   const int nh = (l.L - 1) * l.W * l.Kp;
   const int nhead = 16 * l.Kp;
-  if (idx >= n1 + nh + nhead + l.W + 1) return;
-  if (idx >= n1 + nh + nhead) {  // fp32 copy of the head row and bias
+  if (idx >= n1 + nh + nhead + l.HD * (l.W + 1)) return;
+  if (idx >= n1 + nh + nhead) {  // fp32 copy of the head rows [HD][W], then the HD biases
     const int k = idx - n1 - nh - nhead;
     const size_t wo = (size_t)f.dims[0] * l.W + (size_t)(l.L - 1) * l.W * l.W;
-    reinterpret_cast<float*>(blob + l.off_headf)[k] = k < l.W ? f.w[wo + k] : f.b[(size_t)l.W * l.L];
+    reinterpret_cast<float*>(blob + l.off_headf)[k] =
+        k < l.HD * l.W ? f.w[wo + k] : f.b[(size_t)l.W * l.L + (k - l.HD * l.W)];
     return;
   }
   float val = 0.f;
@@ -854,6 +859,49 @@ __device__ __forceinline__ float head_simt(uint32_t taddr, const float* __restri
   return s.x + s.y;
 }
 
+// HD-output head (geometry: 4-wide identity head) from the same fp32
+// accumulator columns: each activation chunk is loaded once and feeds all
+// HD dot products. Rows at hw + j * W, biases at hw + HD * W; for HD = 1 the
+// arithmetic (and its order) is head_simt's.
+template <int W, int CH, int HD>
+__device__ __forceinline__ void head_simt_n(uint32_t taddr, const float* __restrict__ hw,
+                                            float (&out)[HD]) {
+  unsigned long long acc[HD];
+#pragma unroll
+  for (int j = 0; j < HD; ++j) acc[j] = f2pack(hw[HD * W + j], 0.f);
+  const unsigned long long slope = f2pack(kSlope, kSlope);
+#pragma unroll
+  for (int g0 = 0; g0 < W; g0 += CH) {
+    uint32_t r[CH];
+    const int gw = (W - g0) < CH ? (W - g0) : CH;
+    tc::tmem_ld16_nw(taddr + g0, r);
+    if (CH > 16 && gw > 16) tc::tmem_ld16_nw(taddr + g0 + 16, r + (CH > 16 ? 16 : 0));
+    tc::tmem_ld_fence<CH>(r);
+#pragma unroll
+    for (int c = 0; c < CH; c += 4) {
+      if (c >= gw) break;
+      const unsigned long long z01 = f2pack(__uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+      const unsigned long long z23 = f2pack(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+      const float2 t01 = f2unpack(fmul2(z01, slope)), t23 = f2unpack(fmul2(z23, slope));
+      const unsigned long long a01 =
+          f2pack(fmaxf(__uint_as_float(r[c]), t01.x), fmaxf(__uint_as_float(r[c + 1]), t01.y));
+      const unsigned long long a23 = f2pack(fmaxf(__uint_as_float(r[c + 2]), t23.x),
+                                            fmaxf(__uint_as_float(r[c + 3]), t23.y));
+#pragma unroll
+      for (int j = 0; j < HD; ++j) {
+        const float4 w4 = *reinterpret_cast<const float4*>(hw + j * W + g0 + c);
+        acc[j] = ffma2(a01, f2pack(w4.x, w4.y), acc[j]);
+        acc[j] = ffma2(a23, f2pack(w4.z, w4.w), acc[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < HD; ++j) {
+    const float2 s = f2unpack(acc[j]);
+    out[j] = s.x + s.y;
+  }
+}
+
 template <int N, int ND, int W, int L, int G, int TPS>
 __global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
   using C = Tc2<N, ND, W, L, G>;
@@ -1147,7 +1195,7 @@ struct MlpArgs {
 // column) [AOFF, AOFF + Kp/2). Keeping A in TMEM means the tensor core reads
 // only the weights from shared memory: with N = 48-64 the A tile re-read
 // per K step would otherwise make the MLP shared-memory-bandwidth bound.
-template <int W, int L, int G>
+template <int W, int L, int G, int HD = 1>
 struct MlpCfg {
   static constexpr int Kp = ((W + 1) + 15) / 16 * 16;
   static constexpr int AOFF = (W + 15) / 16 * 16;
@@ -1157,7 +1205,7 @@ struct MlpCfg {
                               : COLS_RAW <= 256 ? 256 : 512;
   static constexpr size_t OFF_HEADF =
       (size_t)W * kK1 * 2 + (size_t)(L - 1) * W * Kp * 2 + (size_t)16 * Kp * 2;
-  static constexpr size_t W_BYTES = OFF_HEADF + ((size_t)(W + 1) * 4 + 15) / 16 * 16;
+  static constexpr size_t W_BYTES = OFF_HEADF + ((size_t)HD * (W + 1) * 4 + 15) / 16 * 16;
   static constexpr size_t W_AL = (W_BYTES + 1023) / 1024 * 1024;
   static constexpr size_t SMEM = W_AL + 128;
   static_assert(W % 16 == 0 && L >= 2, "shape");
@@ -1350,9 +1398,9 @@ __global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) 
 #ifndef NIF_ENC_ISSUE
 #define NIF_ENC_ISSUE 0  // 0: under the last hidden MMA; k: under the k-th (k=1 spills, slower)
 #endif
-template <int N, int ND, int W, int L, int G, int TPS, bool PO = false>
+template <int N, int ND, int W, int L, int G, int TPS, bool PO = false, int HD = 1>
 __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
-  using C = MlpCfg<W, L, G>;
+  using C = MlpCfg<W, L, G, HD>;
   constexpr bool INNER = ND > 0;
   constexpr int Kp = C::Kp;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1483,10 +1531,16 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
       phase ^= 1;
       tc::fence_after_sync();
     }
-    const float logit = head_simt<W, 16>(lane_acc, headw);
+    float hout[HD];
+    head_simt_n<W, 16, HD>(lane_acc, headw, hout);
     if (valid) {
-      if (a.logits) a.logits[row] = logit;
-      if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
+      if constexpr (HD == 1) {
+        if (a.logits) a.logits[row] = hout[0];
+        if (a.occ && hout[0] < 0.f) a.occ[my_ray] = 1;
+      } else if (a.logits) {  // geometry head: raw (normal, depth) outputs
+#pragma unroll
+        for (int j = 0; j < HD; ++j) a.logits[row * HD + j] = hout[j];
+      }
     }
     tc::fence_before_sync();
   }
@@ -1494,10 +1548,10 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
 }
 
-template <int N, int ND, int W, int L, int G, int TPS, bool PO = false>
+template <int N, int ND, int W, int L, int G, int TPS, bool PO = false, int HD = 1>
 int launch_ts(const TcArgs& a, cudaStream_t st) {
-  using C = MlpCfg<W, L, G>;
-  auto kern = query_ts_kernel<N, ND, W, L, G, TPS, PO>;
+  using C = MlpCfg<W, L, G, HD>;
+  auto kern = query_ts_kernel<N, ND, W, L, G, TPS, PO, HD>;
   const size_t smem = C::SMEM + (PO ? (size_t)(G - 1) * C::W_AL : 0);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
@@ -1528,6 +1582,7 @@ int launch_ts(const TcArgs& a, cudaStream_t st) {
 // per_object sharing (bucketed tiles): default shapes; 0 = launched
 int launch_ts_po(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
   const int W = a.l.W, L = a.l.L;
+  if (a.l.HD != 1) return 1;
   if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
     *rc = launch_ts<3, 0, 64, 2, 2, 4, true>(a, st);
     return 0;
@@ -1542,6 +1597,17 @@ int launch_ts_po(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int
 // 0 = launched, 1 = no specialisation
 int launch_ts_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
   const int W = a.l.W, L = a.l.L;
+  if (a.l.HD == 4) {  // geometry head (infer_geometry), default shapes
+    if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
+      *rc = launch_ts<3, 0, 64, 2, 2, 4, false, 4>(a, st);
+      return 0;
+    }
+    if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
+      *rc = launch_ts<5, 3, 48, 3, 3, 6, false, 4>(a, st);
+      return 0;
+    }
+    return 1;
+  }
 #define NIF_TS(NN, NDD, WW, LL, GG, TT)                                        \
   if (f.N == NN && (NDD == 0 ? f.family == NIF_FAMILY_OUTER                    \
                              : (f.family == NIF_FAMILY_INNER && f.Nd == NDD)) && \
@@ -1884,7 +1950,7 @@ extern "C" int nif_fast_pack_dev(const nif_family_view* f, void* blob, void* str
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(blob, 0, l.total, st);
   if (l.tc_ok) {
-    const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp + l.W + 1;
+    const int nw = l.W * kK1 + (l.L - 1) * l.W * l.Kp + 16 * l.Kp + l.HD * (l.W + 1);
     pack_weights_kernel<<<dim3((nw + 255) / 256, f->n_heads), 256, 0, st>>>(*f, l,
                                                                             (uint8_t*)blob);
   }
@@ -1917,6 +1983,13 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
     if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
     TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
              logits, g_prof};
+    if (l.HD != 1) {  // geometry head: the TMEM-operand kernel only
+      int rc = NIF_OK;
+      if (launch_ts_any(a, *f, st, &rc) == 0) return rc;
+      if (impl != NIF_IMPL_AUTO)
+        return fail(NIF_ERR_UNSUPPORTED, "no tcgen05 geometry-head kernel for W=%d L=%d", l.W, l.L);
+      goto simt;
+    }
     if (impl != NIF_IMPL_TCGEN05_GENERIC && g_prof == nullptr && g_query_variant != 2) {
       int rc = NIF_OK;
       if (g_query_variant == 1 || g_query_variant == 9) {
@@ -1933,6 +2006,7 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
     if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 4) return launch_tc<5, 4>(a, st);
     return fail(NIF_ERR_UNSUPPORTED, "no tcgen05 instantiation for N=%d Nd=%d", f->N, f->Nd);
   }
+simt:
   if (f->dims[0] > kSimtMaxIn) return fail(NIF_ERR_UNSUPPORTED, "input width above %d", kSimtMaxIn);
   for (int i = 1; i <= f->n_layers; ++i)
     if (f->dims[i] > kSimtMaxW) return fail(NIF_ERR_UNSUPPORTED, "width above %d", kSimtMaxW);
@@ -2006,7 +2080,8 @@ extern "C" int nif_query_split_dev(const nif_family_view* f, const int32_t* obj,
     return fail(NIF_ERR_VALUE, "inner queries need the radial coordinate");
   if (feat == nullptr) return fail(NIF_ERR_VALUE, "split query needs a feature scratch buffer");
   const FastLayout l = make_layout(*f);
-  if (!l.tc_ok) return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernels");
+  if (!l.tc_ok || l.HD != 1)
+    return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernels");
   if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
   int rc = NIF_OK;
   if (launch_split(*f, l, obj, ray, coord4, r, count_dev, capacity, occ_ray, logits,

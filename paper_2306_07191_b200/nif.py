@@ -506,6 +506,8 @@ def query_family(model: NifModel, which: str, obj, coord, impl: int = _lib.IMPL_
     d_r = _to_dev(coord[:, 4], np.float32, dev) if which == "inner" else None
     d_cnt = torch.tensor([m], dtype=torch.int64, device=dev)
     d_log = torch.empty(m * fam.dims[-1], dtype=torch.float32, device=dev)
+    if fam.n_heads > 1 and fam.dims[-1] != 1 and impl == _lib.IMPL_AUTO:
+        impl = _lib.IMPL_SIMT  # per-object geometry heads: no bucketed 4-wide kernel
     if fam.n_heads > 1 and impl in (_lib.IMPL_AUTO, _lib.IMPL_TCGEN05) and not split:
         # per_object sharing: bucket by object, then the tensor-core kernel
         L = _lib.lib()
@@ -562,14 +564,51 @@ def _split_queries(queries):
             np.asarray(i_obj, np.int64), np.asarray(i_coord, np.float64).reshape(-1, 5))
 
 
-def infer_occlusion(model: NifModel, queries) -> np.ndarray:
-    """nif.py:428-442 (outer batch first, then inner)."""
+def infer_occlusion(model: NifModel, queries, exact: bool = True) -> np.ndarray:
+    """nif.py:428-442: True = occluded (p < 0.5; exactly 0.5 is visible).
+    Outer batch first, then inner, results in query order. exact=True runs
+    the reference's arithmetic (fp64 weights / accumulation, stable
+    sigmoid: bit-identical to the reference, so SPEC.md's batching
+    invariant holds bit for bit); exact=False runs the fused tensor-core
+    query (fp16 operands, logit < 0)."""
     if model.config.head != "occlusion":
         raise ValueError("model was built with the geometry head")
     o_idx, o_obj, o_coord, i_idx, i_obj, i_coord = _split_queries(queries)
     out = np.zeros(len(queries), bool)
-    if len(o_idx):
-        out[o_idx] = query_family(model, "outer", o_obj, o_coord) < 0.0
-    if len(i_idx):
-        out[i_idx] = query_family(model, "inner", i_obj, i_coord) < 0.0
+    for idx, obj, coord, which in ((o_idx, o_obj, o_coord, "outer"),
+                                   (i_idx, i_obj, i_coord, "inner")):
+        if not len(idx):
+            continue
+        if exact:
+            p = _forward(model, which, obj, _encode(model, which, obj, coord))
+            out[idx] = p[:, 0] < 0.5
+        else:
+            out[idx] = query_family(model, which, obj, coord) < 0.0
     return out
+
+
+def infer_geometry(model: NifModel, queries, exact: bool = False):
+    """nif.py:445-464: (unit normal [q,3], depth [q]) per query from the
+    4-wide identity head; normals renormalised (a zero vector maps to +z),
+    depth rescaled by the scene diagonal. exact=False runs the fused
+    tensor-core query with the 4-wide head (fp16 operands, fp32 head);
+    exact=True the reference's fp64-accumulation arithmetic."""
+    if model.config.head != "geometry":
+        raise ValueError("model was built with the occlusion head")
+    o_idx, o_obj, o_coord, i_idx, i_obj, i_coord = _split_queries(queries)
+    raw = np.zeros((len(queries), 4), np.float64)
+    for idx, obj, coord, which in ((o_idx, o_obj, o_coord, "outer"),
+                                   (i_idx, i_obj, i_coord, "inner")):
+        if not len(idx):
+            continue
+        if exact:
+            raw[idx] = _forward(model, which, obj, _encode(model, which, obj, coord))
+        else:
+            raw[idx] = query_family(model, which, obj, coord).reshape(-1, 4)
+    normals = raw[:, 0:3]
+    norms = np.linalg.norm(normals, axis=1)
+    ok = norms > 1e-20
+    normals = np.where(ok[:, None], normals / np.maximum(norms, 1e-300)[:, None],
+                       np.array([0.0, 0.0, 1.0]))
+    depth = raw[:, 3] * model.scene_diagonal
+    return normals, depth

@@ -40,13 +40,24 @@ def rays_to_device(rays: ShadowRays, device):
     return o, d, t
 
 
-class GatherBuffers:
-    """Device outputs of nif_gather_dev for up to `n` rays."""
+# record slots per ray the queues start with: a shadow ray meets only a few
+# network-routed boxes (C2: 1.16 records per ray, C3: 1.2); the gather bounds
+# its writes and reports true totals, so callers grow on overflow
+DEFAULT_SLOTS_PER_RAY = 4
 
-    def __init__(self, n, n_net_obj, device, interleaved=False):
+
+class GatherBuffers:
+    """Device outputs of nif_gather_dev for up to `n` rays, `slots` record
+    slots per ray per queue (default: n_net_obj, the worst case the
+    reference allocates, renderer.py:619-624)."""
+
+    def __init__(self, n, n_net_obj, device, interleaved=False, slots=None):
         torch = _torch()
-        cap = max(1, n * max(1, n_net_obj))
+        slots = max(1, n_net_obj) if slots is None else max(1, min(slots, max(1, n_net_obj)))
+        cap = max(1, n * slots)
         self.n = n
+        self.n_net = max(1, n_net_obj)
+        self.slots = slots
         self.cap = cap
         i32 = dict(dtype=torch.int32, device=device)
         f32 = dict(dtype=torch.float32, device=device)
@@ -88,6 +99,33 @@ def gather_dev(dscene, route_dev, o, d, t, n, buf: GatherBuffers, stream=None):
                      _lib.stream_ptr(stream))
 
 
+def overflowed(buf: GatherBuffers, counts) -> bool:
+    """True when the last gather into `buf` emitted more records than its
+    queues hold (counts: host copy of buf.counts)."""
+    if max(int(counts[0]), int(counts[1])) > buf.cap:
+        return True
+    return buf.interleaved and int(counts[2]) > buf.cap
+
+
+def slots_for(counts, n) -> int:
+    """Record slots per ray that hold the totals in `counts` (+25 %)."""
+    need = max(int(counts[0]), int(counts[1]), int(counts[2]))
+    return max(1, -(-(need + need // 4) // max(n, 1)))
+
+
+def gather_sized(dscene, route_dev, o, d, t, n, n_net, device, interleaved=True):
+    """gather_dev into buffers sized from a small per-ray bound, re-run once
+    with exact-fit buffers if a queue overflowed; returns (buf, counts)."""
+    buf = GatherBuffers(n, n_net, device, interleaved=interleaved, slots=DEFAULT_SLOTS_PER_RAY)
+    gather_dev(dscene, route_dev, o, d, t, n, buf)
+    counts = buf.counts.cpu().numpy()
+    if overflowed(buf, counts):
+        buf = GatherBuffers(n, n_net, device, interleaved=interleaved, slots=slots_for(counts, n))
+        gather_dev(dscene, route_dev, o, d, t, n, buf)
+        counts = buf.counts.cpu().numpy()
+    return buf, counts
+
+
 def gather_queries(scene: Scene, rays: ShadowRays, route: np.ndarray, threads: int = 1):
     """renderer.py:613-644 on the device. Returns (QueryRecords,
     bvh_occluded) with records in the reference's order (ray-major, top-level
@@ -100,9 +138,7 @@ def gather_queries(scene: Scene, rays: ShadowRays, route: np.ndarray, threads: i
                             np.zeros((0, 5)), 0), np.zeros(0, bool)
     o, d, t = rays_to_device(rays, ds.device)
     n_net = int(np.asarray(route, np.uint8).sum())
-    buf = GatherBuffers(n, n_net, ds.device, interleaved=True)
-    gather_dev(ds, ds.route(route), o, d, t, n, buf)
-    counts = buf.counts.cpu().numpy()
+    buf, counts = gather_sized(ds, ds.route(route), o, d, t, n, n_net, ds.device)
     m = int(counts[2])
     rec = QueryRecords(kind=buf.rec_kind[:m].cpu().numpy(), obj=buf.rec_obj[:m].cpu().numpy(),
                        ray=buf.rec_ray[:m].cpu().numpy(),
@@ -189,17 +225,30 @@ class OracleBackend(PredictorBackend):
         super().__init__(oracle_predictor, hybrid_threshold)
 
 
+def _require_occlusion_head(model):
+    """nif.py:470-471: visibility needs the occlusion head."""
+    if model is not None and model.config.head != "occlusion":
+        raise ValueError("model was built with the geometry head")
+
+
 class VisibilityEngine:
     """Device-resident split visibility pass for one (scene, model, route).
 
     Buffers are sized for `capacity` rays; `run(n)` enqueues the whole pass
     for the first n rays already in `origins/dirs/tmaxs` and leaves one byte
     per ray in `occ` (1 = shadowed). No host synchronisation inside.
+
+    The record queues hold `slots` records per ray (default
+    DEFAULT_SLOTS_PER_RAY, not the n_obj worst case); the gather never
+    writes past them and reports the true totals. `checked_run` (and the
+    synchronous callers) re-run with grown queues when a batch overflowed;
+    `capture` sizes the queues from an eager run of the same rays first.
     """
 
     def __init__(self, scene: Scene, model, capacity: int, hybrid_threshold=None,
-                 impl: int = _lib.IMPL_AUTO):
+                 impl: int = _lib.IMPL_AUTO, slots: Optional[int] = None):
         torch = _torch()
+        _require_occlusion_head(model)
         self.scene = scene
         self.ds = scene.device()
         self.model = model
@@ -212,20 +261,26 @@ class VisibilityEngine:
         self.origins = torch.empty((capacity, 3), dtype=torch.float64, device=dev)
         self.dirs = torch.empty((capacity, 3), dtype=torch.float64, device=dev)
         self.tmaxs = torch.empty(capacity, dtype=torch.float64, device=dev)
-        self.buf = GatherBuffers(capacity, int(route.sum()), dev)
-        # the gather writes the hybrid any-hit result straight into the
-        # per-ray answer, which the query kernels then OR into
-        self.occ = self.buf.bvh_occ
         self.side = torch.cuda.Stream(device=dev)
         self._views = None
         self.graphs = {}
+        self._alloc(DEFAULT_SLOTS_PER_RAY if slots is None else slots)
+
+    def _alloc(self, slots):
+        torch = _torch()
+        dev = self.ds.device
+        self.buf = GatherBuffers(self.capacity, int(self.route_np.sum()), dev, slots=slots)
+        # the gather writes the hybrid any-hit result straight into the
+        # per-ray answer, which the query kernels then OR into
+        self.occ = self.buf.bvh_occ
         # per_object sharing: per-family scratch for the bucketed tensor-core query
         self.bucket = None
-        if model is not None and model.outer.n_heads > 1:
+        if self.model is not None and self.model.outer.n_heads > 1:
             L = _lib.lib()
-            nb = int(L.nif_bucket_scratch_bytes(self.buf.cap, model.outer.n_obj))
+            nb = int(L.nif_bucket_scratch_bytes(self.buf.cap, self.model.outer.n_obj))
             self.bucket = (torch.empty(nb, dtype=torch.uint8, device=dev),
                            torch.empty(nb, dtype=torch.uint8, device=dev))
+        self.graphs = {}
 
     def _family_views(self):
         if self._views is None or self.model.outer.dirty or self.model.inner.dirty:
@@ -262,6 +317,19 @@ class VisibilityEngine:
         self.side.wait_stream(main)
         self._query(vo, vi, p(self.occ), self.side.cuda_stream, sp)
         main.wait_stream(self.side)
+
+    def overflowed(self) -> bool:
+        """Did the last run emit more records than the queues hold? (syncs)"""
+        return overflowed(self.buf, self.counts())
+
+    def checked_run(self, n: int, stream=None):
+        """run(n), then (one host read of the record totals) grow the queues
+        and re-run if they overflowed; the answer in `occ` is then exact."""
+        self.run(n, stream)
+        counts = self.counts()
+        if overflowed(self.buf, counts):
+            self._alloc(slots_for(counts, n))
+            self.run(n, stream)
 
     def _query(self, vo, vi, occ, side_sp, main_sp):
         """Outer family on the side stream, inner on the main one; per_object
@@ -312,7 +380,8 @@ class VisibilityEngine:
         pinned host tensors ho/hd (n,3) f64 and ht (n,) f64, answer into the
         pinned uint8 tensor hocc. Chunk k+1 is copied in on a copy stream
         while chunk k is classified and queried; the answer of chunk k is
-        copied out as soon as it is final."""
+        copied out as soon as it is final. (The queues must already hold a
+        chunk's records: size them with one checked_run first.)"""
         torch = _torch()
         if n > self.capacity:
             raise ValueError(f"{n} rays exceed the engine capacity {self.capacity}")
@@ -344,13 +413,15 @@ class VisibilityEngine:
         main.wait_stream(self._d2h)
 
     def capture(self, n: int):
-        """CUDA-graph the pass for a fixed ray count (replayed by `replay`)."""
+        """CUDA-graph the pass for a fixed ray count (replayed by `replay`).
+        The rays to replay must already be resident: an eager checked run
+        over them sizes the queues before the capture."""
         torch = _torch()
         self._family_views()  # pack outside the capture
         s = torch.cuda.Stream(device=self.ds.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            self.run(n, s)  # warm (kernel attributes, lazy module load)
+            self.checked_run(n, s)  # warm (kernel attributes, lazy module load) + sizing
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
@@ -365,36 +436,58 @@ class VisibilityEngine:
 class NativeEngine:
     """The whole pass behind the native engine object (nif_engine_*): host
     rays in, per-ray answer out, one C-ABI call -- what a ctypes stub inside
-    the reference binds for PredictorBackend.occluded."""
+    the reference binds for PredictorBackend.occluded.
+    Pageable numpy rays are staged through the engine's pinned ring (host
+    copy threads, upload and device pass of neighbouring chunks overlap)."""
 
     def __init__(self, scene: Scene, model, capacity: int, hybrid_threshold=None):
+        _require_occlusion_head(model)
         self.scene, self.model, self.capacity = scene, model, capacity
         self.ds = scene.device()
         route = scene.nif_route_mask(hybrid_threshold)
+        self.route_np = route
         self.route = self.ds.route(route)
         L = _lib.lib()
+        # the packs (if the model is dirty) are enqueued on torch's current
+        # stream; the engine's streams wait for that stream before reading
         vo = model.outer.view(with_fast=True)
         vi = model.inner.view(with_fast=True)
         h = C.c_void_p()
         L.nif_engine_create(self.ds.view, _lib.ptr(self.route), int(route.sum()), vo, vi,
-                            int(capacity), C.byref(h))
+                            int(capacity), _lib.stream_ptr(), C.byref(h))
         self.handle = h
 
     def update_model(self):
-        """After optimiser steps: repack and point the engine at the blobs."""
+        """After optimiser steps: repack and point the engine at the blobs
+        (the engine waits for the repack's stream)."""
         _lib.lib().nif_engine_update_model(self.handle, self.model.outer.view(with_fast=True),
-                                           self.model.inner.view(with_fast=True))
+                                           self.model.inner.view(with_fast=True),
+                                           _lib.stream_ptr())
 
-    def occluded(self, rays: ShadowRays, chunks: int = 4) -> np.ndarray:
-        n = len(rays)
-        out = np.zeros(n, np.uint8)
+    def info(self) -> dict:
+        out = np.zeros(4, np.int64)
+        _lib.lib().nif_engine_info(self.handle, out.ctypes.data)
+        return {"chunk_rays": int(out[0]), "slots_per_ray": int(out[1]),
+                "staging_threads": int(out[2]), "overflow_reruns": int(out[3])}
+
+    def occluded_into(self, origins, dirs, tmaxs, out: np.ndarray, chunks: int = 0):
+        """Host arrays in (f64 [n,3], [n,3], [n]), uint8 answer into `out`."""
+        n = len(tmaxs)
         if n:
-            o = np.ascontiguousarray(rays.origins, np.float64)
-            d = np.ascontiguousarray(rays.dirs, np.float64)
-            t = np.ascontiguousarray(rays.tmaxs, np.float64)
+            if self.model.outer.dirty or self.model.inner.dirty:
+                self.update_model()
+            o = np.ascontiguousarray(origins, np.float64)
+            d = np.ascontiguousarray(dirs, np.float64)
+            t = np.ascontiguousarray(tmaxs, np.float64)
             _lib.lib().nif_engine_occluded_host(self.handle, o.ctypes.data, d.ctypes.data,
-                                                t.ctypes.data, n, out.ctypes.data, chunks)
-        return out.astype(bool)
+                                                t.ctypes.data, n, out.ctypes.data, int(chunks))
+        return out
+
+    def occluded(self, rays: ShadowRays, chunks: int = 0) -> np.ndarray:
+        n = len(rays)
+        out = np.empty(n, np.uint8)
+        self.occluded_into(rays.origins, rays.dirs, rays.tmaxs, out, chunks)
+        return out.view(bool)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -410,7 +503,15 @@ class NativeEngine:
 
 class NifBackend(PredictorBackend):
     """nif.py:486-499: visibility from the learned model, optionally hybrid.
-    occluded() runs the fused device pass; predict() keeps the record API."""
+    occluded() (host rays) runs the whole pass behind the native engine
+    handle (C-ABI, pinned staging); occluded_dev() (device rays) runs the
+    device-resident VisibilityEngine; predict() keeps the record API.
+    Engines are cached per (scene, route mask) -- the mask is recomputed on
+    every call like the reference's PredictorBackend.occluded, so edits to
+    scene.nif_enabled or hybrid_threshold take effect -- keeping the most
+    recent few."""
+
+    MAX_ENGINES = 4
 
     def __init__(self, model, hybrid_threshold: Optional[int] = None,
                  impl: int = _lib.IMPL_AUTO, keep_records: bool = False):
@@ -426,39 +527,58 @@ class NifBackend(PredictorBackend):
 
         super().__init__(predict, hybrid_threshold)
         self.name = "nif" if hybrid_threshold is None else "hybrid"
-        self._engines = {}
+        from collections import OrderedDict
+        self._engines = OrderedDict()
 
-    def engine(self, scene: Scene, n: int) -> VisibilityEngine:
-        key = id(scene)
-        eng = self._engines.get(key)
-        if eng is None or eng.capacity < n:
-            cap = max(n, 1024)
-            eng = VisibilityEngine(scene, self.model, cap, self.hybrid_threshold, self.impl)
-            self._engines[key] = eng
+    def _cached(self, kind, scene, n, make):
+        route = scene.nif_route_mask(self.hybrid_threshold)
+        key = (kind, id(scene), bytes(route))
+        eng = self._engines.pop(key, None)
+        if eng is not None and (eng.scene is not scene or eng.capacity < n):
+            eng = None
+        if eng is None:
+            eng = make(max(n, 1024))
+        self._engines[key] = eng
+        while len(self._engines) > self.MAX_ENGINES:
+            _, old = self._engines.popitem(last=False)
+            if hasattr(old, "close"):
+                old.close()
         return eng
 
+    def engine(self, scene: Scene, n: int) -> VisibilityEngine:
+        return self._cached("dev", scene, n, lambda cap: VisibilityEngine(
+            scene, self.model, cap, self.hybrid_threshold, self.impl))
+
+    def native_engine(self, scene: Scene, n: int) -> NativeEngine:
+        return self._cached("host", scene, n, lambda cap: NativeEngine(
+            scene, self.model, cap, self.hybrid_threshold))
+
     def occluded(self, scene: Scene, rays: ShadowRays, threads: int = 1) -> np.ndarray:
+        _require_occlusion_head(self.model)
         if self.keep_records:
             return super().occluded(scene, rays, threads)
         n = len(rays)
         if n == 0:
             return np.zeros(0, bool)
-        eng = self.engine(scene, n)
-        eng.load(rays)
-        eng.run(n)
-        return eng.occ[:n].cpu().numpy().astype(bool)
+        if self.impl not in (_lib.IMPL_AUTO, _lib.IMPL_TCGEN05):
+            eng = self.engine(scene, n)
+            eng.load(rays)
+            eng.checked_run(n)
+            return eng.occ[:n].cpu().numpy().astype(bool)
+        return self.native_engine(scene, n).occluded(rays)
 
     def occluded_dev(self, scene: Scene, o, d, t):
         """Device rays in, device uint8 answer out (valid until the next
         call on this scene); the engine's buffers are filled device to
-        device."""
+        device. One host read of the record totals guards queue overflow."""
+        _require_occlusion_head(self.model)
         n = int(t.numel())
         eng = self.engine(scene, max(n, 1))
         if n:
             eng.origins[:n].copy_(o)
             eng.dirs[:n].copy_(d)
             eng.tmaxs[:n].copy_(t)
-            eng.run(n)
+            eng.checked_run(n)
         return eng.occ[:n]
 
 

@@ -88,7 +88,7 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
     camera origin, infinite t_max) and labels each record with the closest
     hit in its own object (unit normal, t / diagonal), keeping hit rows."""
     torch = _torch()
-    from .pipeline import GatherBuffers, gather_dev, sample_pass_dev
+    from .pipeline import gather_sized, sample_pass_dev
     camera = camera or scene.camera
     if camera is None:
         raise ValueError("no camera given and the scene has none")
@@ -126,9 +126,7 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
             o = data["point"][idx].contiguous()
             d = data["ldir"][idx].contiguous()
             t = data["tmax"][idx].contiguous()
-        buf = GatherBuffers(n, int(route.sum()), dev, interleaved=True)
-        gather_dev(ds, ds.route(route), o, d, t, n, buf)
-        counts = buf.counts.cpu().numpy()
+        buf, counts = gather_sized(ds, ds.route(route), o, d, t, n, int(route.sum()), dev)
         m = int(counts[2])
         shadow_rays += n
         degenerate += int(counts[3])

@@ -79,3 +79,29 @@ def test_adam_sidecar_round_trip(tmp_path):
     for fam, fam2 in ((m.outer, m2.outer), (m.inner, m2.inner)):
         assert torch.equal(fam.m, fam2.m) and torch.equal(fam.v, fam2.v)
         assert int(fam2.grid_steps[0]) == 7 and int(fam2.mlp_steps[0]) == 9
+
+
+def test_adam_sidecar_stale(tmp_path):
+    """A re-save without optimiser state removes the old sidecar; a sidecar
+    belonging to different weights is rejected."""
+    import shutil
+    from paper_2306_07191_b200.checkpoint import (SceneFormatError, load_checkpoint,
+                                                  save_checkpoint)
+    m = load_checkpoint(GOLD / "ckpt_shared.nif1", device="cpu")
+    m.outer.grid_steps.fill_(5)
+    p = tmp_path / "m.nif1"
+    save_checkpoint(m, p, adam=True)
+    side = tmp_path / "m.nif1.adam"
+    assert side.exists()
+    keep = tmp_path / "old.adam"
+    shutil.copy(side, keep)
+    save_checkpoint(m, p)  # weights only
+    assert not side.exists()
+    m2 = load_checkpoint(p, device="cpu")
+    assert int(m2.outer.grid_steps[0]) == 0
+    # a sidecar written for other weights
+    m.outer.part("w").add_(1.0)
+    save_checkpoint(m, p)
+    shutil.copy(keep, side)
+    with pytest.raises(SceneFormatError, match="different checkpoint"):
+        load_checkpoint(p, device="cpu")
