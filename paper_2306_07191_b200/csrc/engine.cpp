@@ -28,8 +28,13 @@
 // nif_engine_update_model with the stream the pack was enqueued on: the
 // engine's streams wait for it before the next query.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -51,6 +56,7 @@ class CopyPool {
     for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
   ~CopyPool() {
+    stop_flag_.store(true);
     {
       std::lock_guard<std::mutex> g(mu_);
       stop_ = true;
@@ -71,7 +77,7 @@ class CopyPool {
       next_ = 0;
       parts_ = parts;
       pending_ = parts;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     work();
@@ -99,26 +105,148 @@ class CopyPool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      // spin briefly before sleeping: staging jobs arrive every ~0.2 ms
+      // within a call and calls come back to back, so a condvar wake-up
+      // (tens of us) would otherwise sit in front of every chunk
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen && !stop_flag_.load() &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(kSpinUs))
+        _mm_pause();
       {
         std::unique_lock<std::mutex> g(mu_);
-        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        cv_.wait(g, [&] { return stop_ || gen_.load() != seen; });
         if (stop_) return;
-        seen = gen_;
+        seen = gen_.load();
       }
       work();
     }
   }
+  static constexpr int kSpinUs = 300;
+  std::atomic<bool> stop_flag_{false};
   std::vector<std::thread> threads_;
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;
   int next_ = 0, parts_ = 0, pending_ = 0;
-  uint64_t gen_ = 0;
+  std::atomic<uint64_t> gen_{0};
   bool stop_ = false;
 };
 
-constexpr int kSlots = 3;                 // staging ring depth
-constexpr int64_t kChunkRays = 1 << 18;   // default chunk: 256K rays, 14.7 MB in
+// One persistent thread that runs a job (the staging loop of one call) while
+// the calling thread issues uploads and launches: the staging copy of chunk
+// k+1 proceeds while chunk k's launches are being enqueued.
+class Stager {
+ public:
+  Stager() : t_([this] { loop(); }) {}
+  ~Stager() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    t_.join();
+  }
+  void start(std::function<void()> job) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = std::move(job);
+      busy_ = true;
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [this] { return !busy_; });
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [this] { return stop_ || (busy_ && job_); });
+        if (stop_) return;
+        job = std::move(job_);
+        job_ = nullptr;
+      }
+      job();
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        busy_ = false;
+      }
+      done_cv_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void()> job_;
+  bool busy_ = false, stop_ = false;
+  std::thread t_;
+};
+
+// spin (then yield) until counter >= target or abort is set
+inline bool wait_counter(const std::atomic<int>& counter, int target,
+                         const std::atomic<bool>& abort) {
+  for (int spins = 0; counter.load(std::memory_order_acquire) < target; ++spins) {
+    if (abort.load(std::memory_order_relaxed)) return false;
+    if (spins < 4096) _mm_pause();
+    else std::this_thread::yield();
+  }
+  return true;
+}
+
+// Pageable -> pinned copy with non-temporal (streaming) stores: the pinned
+// slot is read next by the DMA engine, not by this core, so write-allocate
+// reads of the destination lines would only add host-DRAM traffic (which
+// the staging copy shares with the upload itself).
+__attribute__((target("avx2"))) void copy_nt_avx2(uint8_t* dst, const uint8_t* src, size_t n) {
+  size_t head = (32 - ((uintptr_t)dst & 31)) & 31;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256((const __m256i*)(src + i));
+    const __m256i b = _mm256_loadu_si256((const __m256i*)(src + i + 32));
+    const __m256i c = _mm256_loadu_si256((const __m256i*)(src + i + 64));
+    const __m256i d = _mm256_loadu_si256((const __m256i*)(src + i + 96));
+    _mm256_stream_si256((__m256i*)(dst + i), a);
+    _mm256_stream_si256((__m256i*)(dst + i + 32), b);
+    _mm256_stream_si256((__m256i*)(dst + i + 64), c);
+    _mm256_stream_si256((__m256i*)(dst + i + 96), d);
+  }
+  std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+
+bool use_nt_copy() {
+  static const bool v = [] {
+    const char* e = std::getenv("NIF_STAGING_NT");
+    if (e != nullptr && e[0] == '0') return false;
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx2") != 0;
+  }();
+  return v;
+}
+
+void stage_copy(void* dst, const void* src, size_t n) {
+  if (use_nt_copy()) copy_nt_avx2((uint8_t*)dst, (const uint8_t*)src, n);
+  else std::memcpy(dst, src, n);
+}
+
+constexpr int kMaxSlots = 16;  // staging ring depth bound (NIF_STAGING_SLOTS)
+constexpr int kDefaultSlots = 3;
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e != nullptr && std::atoi(e) > 0 ? std::atoi(e) : dflt;
+}
+int64_t chunk_rays_default() {  // default chunk: 256K rays, 14.7 MB in (NIF_STAGING_CHUNK)
+  const char* e = std::getenv("NIF_STAGING_CHUNK");
+  return e != nullptr && std::atoll(e) > 0 ? std::atoll(e) : (int64_t)1 << 18;
+}
 constexpr int kMaxChunks = 4096;
 
 }  // namespace
@@ -143,15 +271,18 @@ struct nif_engine {
   int64_t* counts = nullptr;     // device [4]
   nif_gather_out out{};
   // pinned staging ring
-  uint8_t* pin_in[kSlots] = {};   // chunk_cap * 56 B: o | d | t
-  uint8_t* pin_out[kSlots] = {};  // chunk_cap B
+  int slots = 0;                     // staging ring depth
+  bool ramp = true;                  // geometric first chunks
+  uint8_t* pin_in[kMaxSlots] = {};   // chunk_cap * 56 B: o | d | t
+  uint8_t* pin_out[kMaxSlots] = {};  // chunk_cap B
   int64_t* pin_counts = nullptr;  // [kMaxChunks][4] per-chunk record totals
-  cudaEvent_t ev_in[kSlots] = {};    // H2D of the slot done (slot reusable)
-  cudaEvent_t ev_out[kSlots] = {};   // D2H into the out slot done
-  cudaEvent_t ev_pass[kSlots] = {};  // pass of the slot's chunk done (main)
+  cudaEvent_t ev_in[kMaxSlots] = {};    // H2D of the slot done (slot reusable)
+  cudaEvent_t ev_out[kMaxSlots] = {};   // D2H into the out slot done
+  cudaEvent_t ev_pass[kMaxSlots] = {};  // pass of the slot's chunk done (main)
   cudaStream_t main = nullptr, side = nullptr, copy = nullptr, d2h = nullptr;
   cudaEvent_t ev_side = nullptr, ev_join = nullptr, ev_model = nullptr;
   CopyPool* pool = nullptr;
+  Stager* stager = nullptr;
   int64_t overflow_reruns = 0;
 };
 
@@ -177,7 +308,7 @@ void release(nif_engine* e) {
   for (void* p : {(void*)e->org, (void*)e->dir, (void*)e->tms, (void*)e->occ, e->workspace,
                   (void*)e->counts})
     if (p) cudaFree(p);
-  for (int s = 0; s < kSlots; ++s) {
+  for (int s = 0; s < kMaxSlots; ++s) {
     if (e->pin_in[s]) cudaFreeHost(e->pin_in[s]);
     if (e->pin_out[s]) cudaFreeHost(e->pin_out[s]);
     for (cudaEvent_t ev : {e->ev_in[s], e->ev_out[s], e->ev_pass[s]})
@@ -188,6 +319,7 @@ void release(nif_engine* e) {
     if (ev) cudaEventDestroy(ev);
   for (cudaStream_t s : {e->main, e->side, e->copy, e->d2h})
     if (s) cudaStreamDestroy(s);
+  delete e->stager;
   delete e->pool;
   delete e;
 }
@@ -256,7 +388,7 @@ extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* rou
   e->route = route_dev;
   e->capacity = capacity;
   e->n_net = n_net_obj > 0 ? n_net_obj : 1;
-  e->chunk_cap = std::min<int64_t>(capacity, kChunkRays);
+  e->chunk_cap = std::min<int64_t>(capacity, chunk_rays_default());
   int rc = NIF_OK;
   e->ws_bytes = nif_gather_workspace_bytes(e->chunk_cap);
   if ((rc = dev_alloc(&e->org, (size_t)capacity * 24)) ||
@@ -274,7 +406,10 @@ extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* rou
     release(e);
     return rc;
   }
-  for (int s = 0; s < kSlots; ++s) {
+  e->slots = std::min(kMaxSlots, env_int("NIF_STAGING_SLOTS", kDefaultSlots));
+  const char* ramp_env = std::getenv("NIF_STAGING_RAMP");
+  e->ramp = ramp_env == nullptr || ramp_env[0] != '0';
+  for (int s = 0; s < e->slots; ++s) {
     if (cudaHostAlloc((void**)&e->pin_in[s], (size_t)e->chunk_cap * 56, cudaHostAllocDefault) !=
             cudaSuccess ||
         cudaHostAlloc((void**)&e->pin_out[s], (size_t)e->chunk_cap, cudaHostAllocDefault) !=
@@ -299,9 +434,12 @@ extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* rou
     return nif::fail(NIF_ERR_CUDA, "engine: stream / event creation failed");
   }
   const unsigned hw = std::thread::hardware_concurrency();
-  const int threads = (int)std::max(1u, std::min(8u, hw > 1 ? hw / 2 : 1u));
+  int threads = (int)std::max(1u, std::min(8u, hw > 1 ? hw / 2 : 1u));
+  if (const char* env = std::getenv("NIF_STAGING_THREADS")) threads = std::max(1, std::atoi(env));
+  // the stager thread joins the copy pool's workers in every staging copy
   e->pool = new (std::nothrow) CopyPool(threads - 1);
-  if (e->pool == nullptr) {
+  e->stager = new (std::nothrow) Stager();
+  if (e->pool == nullptr || e->stager == nullptr) {
     release(e);
     return nif::fail(NIF_ERR_CUDA, "engine: out of host memory");
   }
@@ -379,7 +517,7 @@ void pooled_copy(CopyPool* pool, std::vector<std::pair<void*, const void*>>& dst
     for (size_t off = 0; off < bytes[k]; off += kPiece)
       pieces.push_back({(uint8_t*)dst_src[k].first + off, (const uint8_t*)dst_src[k].second + off,
                         std::min(kPiece, bytes[k] - off)});
-  pool->run((int)pieces.size(), [&](int i) { std::memcpy(pieces[i].d, pieces[i].s, pieces[i].n); });
+  pool->run((int)pieces.size(), [&](int i) { stage_copy(pieces[i].d, pieces[i].s, pieces[i].n); });
 }
 
 }  // namespace
@@ -393,37 +531,70 @@ extern "C" int nif_engine_occluded_host(nif_engine* e, const double* origins,
     return nif::fail(NIF_ERR_VALUE, "%lld rays exceed the engine capacity %lld", (long long)n,
                      (long long)e->capacity);
   if (n == 0) return NIF_OK;
-  // chunk size: the staging slot, or smaller when the caller asks for more
-  // chunks (more overlap on small batches)
+  // chunk boundaries. Default: geometric ramp-up (slot/8, slot/4, slot/2,
+  // then whole slots) so the first upload starts after a short staging copy
+  // and the pipeline fill costs little; chunks > 0: uniform chunks.
   int64_t step = e->chunk_cap;
   if (chunks > 0) step = std::min(step, (n + chunks - 1) / chunks);
   step = std::max<int64_t>(step, (n + kMaxChunks - 1) / kMaxChunks);
   if (step > e->chunk_cap) return nif::fail(NIF_ERR_VALUE, "engine: too many rays per call");
-  const int nc = (int)((n + step - 1) / step);
+  std::vector<int64_t> bound{0};
+  for (int64_t size = chunks > 0 || !e->ramp ? step : std::max<int64_t>(1, step / 8);
+       bound.back() < n;
+       size = std::min(step, 2 * size)) {
+    if ((int)bound.size() > kMaxChunks) return nif::fail(NIF_ERR_VALUE, "engine: too many chunks");
+    bound.push_back(std::min(n, bound.back() + size));
+  }
+  const int nc = (int)bound.size() - 1;
   int rc = NIF_OK;
   auto drain = [&](int k) {  // chunk k's answer: pinned out slot -> caller
-    const int s = k % kSlots;
-    const int64_t s0 = (int64_t)k * step, s1 = std::min(n, s0 + step);
+    const int s = k % e->slots;
+    const int64_t s0 = bound[k], s1 = bound[k + 1];
     cudaEventSynchronize(e->ev_out[s]);
     std::memcpy(occ_out + s0, e->pin_out[s], (size_t)(s1 - s0));
   };
-  for (int k = 0; k < nc && rc == NIF_OK; ++k) {
-    const int s = k % kSlots;
-    const int64_t s0 = (int64_t)k * step, s1 = std::min(n, s0 + step), m = s1 - s0;
-    if (k >= kSlots) {
-      cudaEventSynchronize(e->ev_in[s]);  // the slot's previous upload is done
-      drain(k - kSlots);                  // and its previous answer is out
+  // Staging runs on the stager thread (+ copy pool), one chunk ahead of the
+  // uploads: it fills slot k % S once the upload of chunk k - S (the slot's
+  // previous tenant) has been issued and has completed, then publishes
+  // `staged` = k + 1. This thread waits for `staged`, issues the upload and
+  // the chunk's pass, and publishes `issued`.
+  std::atomic<int> staged{0}, issued{0};
+  std::atomic<bool> abort{false};
+  // NIF_STAGING_TRACE=1: host timeline of the call on stderr (diagnostics)
+  static const bool trace = std::getenv("NIF_STAGING_TRACE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t_call = clk::now();
+  std::vector<double> t_staged(trace ? nc : 0), t_issued(trace ? nc : 0);
+  auto us = [&] { return std::chrono::duration<double, std::micro>(clk::now() - t_call).count(); };
+  e->stager->start([&] {
+    for (int k = 0; k < nc; ++k) {
+      const int s = k % e->slots;
+      if (k >= e->slots) {
+        if (!wait_counter(issued, k - e->slots + 1, abort)) return;
+        cudaEventSynchronize(e->ev_in[s]);  // the slot's previous upload is done
+      }
+      const int64_t s0 = bound[k], m = bound[k + 1] - s0;
+      uint8_t* pin = e->pin_in[s];
+      std::vector<std::pair<void*, const void*>> ds = {
+          {pin, origins + 3 * s0}, {pin + m * 24, dirs + 3 * s0}, {pin + m * 48, tmaxs + s0}};
+      std::vector<size_t> bytes = {(size_t)m * 24, (size_t)m * 24, (size_t)m * 8};
+      pooled_copy(e->pool, ds, bytes);
+      if (trace) t_staged[k] = us();
+      staged.store(k + 1, std::memory_order_release);
     }
+  });
+  for (int k = 0; k < nc && rc == NIF_OK; ++k) {
+    const int s = k % e->slots;
+    const int64_t s0 = bound[k], s1 = bound[k + 1], m = s1 - s0;
+    if (k >= e->slots) drain(k - e->slots);  // the out slot's previous answer is out
+    wait_counter(staged, k + 1, abort);
     uint8_t* pin = e->pin_in[s];
-    std::vector<std::pair<void*, const void*>> ds = {
-        {pin, origins + 3 * s0}, {pin + m * 24, dirs + 3 * s0}, {pin + m * 48, tmaxs + s0}};
-    std::vector<size_t> bytes = {(size_t)m * 24, (size_t)m * 24, (size_t)m * 8};
-    pooled_copy(e->pool, ds, bytes);
     cudaMemcpyAsync(e->org + 3 * s0, pin, (size_t)m * 24, cudaMemcpyHostToDevice, e->copy);
     cudaMemcpyAsync(e->dir + 3 * s0, pin + m * 24, (size_t)m * 24, cudaMemcpyHostToDevice,
                     e->copy);
     cudaMemcpyAsync(e->tms + s0, pin + m * 48, (size_t)m * 8, cudaMemcpyHostToDevice, e->copy);
     cudaEventRecord(e->ev_in[s], e->copy);
+    issued.store(k + 1, std::memory_order_release);
     cudaStreamWaitEvent(e->main, e->ev_in[s], 0);
     rc = run_range(e, s0, s1);
     if (rc != NIF_OK) break;
@@ -433,9 +604,19 @@ extern "C" int nif_engine_occluded_host(nif_engine* e, const double* origins,
     cudaStreamWaitEvent(e->d2h, e->ev_pass[s], 0);
     cudaMemcpyAsync(e->pin_out[s], e->occ + s0, (size_t)m, cudaMemcpyDeviceToHost, e->d2h);
     cudaEventRecord(e->ev_out[s], e->d2h);
+    if (trace) t_issued[k] = us();
   }
+  if (rc != NIF_OK) abort.store(true);
+  e->stager->wait();
   if (rc == NIF_OK)
-    for (int k = std::max(0, nc - kSlots); k < nc; ++k) drain(k);
+    for (int k = std::max(0, nc - e->slots); k < nc; ++k) drain(k);
+  if (trace) {
+    std::fprintf(stderr, "{\"staging_trace_us\": {\"chunks\": %d, \"staged\": [", nc);
+    for (int k = 0; k < nc; ++k) std::fprintf(stderr, "%s%.1f", k ? "," : "", t_staged[k]);
+    std::fprintf(stderr, "], \"issued\": [");
+    for (int k = 0; k < nc; ++k) std::fprintf(stderr, "%s%.1f", k ? "," : "", t_issued[k]);
+    std::fprintf(stderr, "], \"drained\": %.1f}}\n", us());
+  }
   const cudaError_t err = cudaStreamSynchronize(e->main);
   cudaStreamSynchronize(e->copy);
   cudaStreamSynchronize(e->d2h);
@@ -453,7 +634,7 @@ extern "C" int nif_engine_occluded_host(nif_engine* e, const double* origins,
     if ((rc = alloc_queues(e, std::min<int64_t>(e->n_net, want)))) return rc;
     for (int k = 0; k < nc; ++k) {
       if (total(k) <= qcap_run) continue;
-      const int64_t s0 = (int64_t)k * step, s1 = std::min(n, s0 + step);
+      const int64_t s0 = bound[k], s1 = bound[k + 1];
       ++e->overflow_reruns;
       if ((rc = run_range(e, s0, s1))) return rc;
       cudaMemcpyAsync(occ_out + s0, e->occ + s0, (size_t)(s1 - s0), cudaMemcpyDeviceToHost,

@@ -56,6 +56,26 @@ def _oracle_family(model, fam):
         dist=np.stack([g["inner_dist"] for g in grids]) if fam == "inner" else None)
 
 
+def _check_coords(ref, got, fam):
+    """fp32 hot-path coordinates vs the fp64 reference: u (azimuth, wraps)
+    within COORD_TOL on the circle; v = acos(z)/pi checked through z =
+    cos(pi v) -- the quantity the gather computes in fp32 -- since acos
+    amplifies a 1-ulp error of z near the poles (|dv| up to
+    sqrt(2 * 2^-24)/pi ~ 1e-4 at |z| -> 1); r within COORD_TOL."""
+    if len(ref) == 0:
+        return
+    for c in (0, 2):
+        du = np.abs(ref[:, c] - got[:, c])
+        du = np.minimum(du, 1.0 - du)
+        assert du.max() <= COORD_TOL, (fam, c, du.max())
+    for c in (1, 3):
+        dz = np.abs(np.cos(np.pi * ref[:, c]) - np.cos(np.pi * got[:, c]))
+        assert dz.max() <= COORD_TOL, (fam, c, dz.max())
+        assert np.abs(ref[:, c] - got[:, c]).max() <= 2e-4, (fam, c)
+    if ref.shape[1] > 4:
+        assert np.abs(ref[:, 4] - got[:, 4]).max() <= COORD_TOL, (fam, "r")
+
+
 def _hot_path(eng, n):
     """Run the hot path once; return per-ray bits and the queues with the
     tcgen05 per-record logits."""
@@ -107,8 +127,7 @@ def _compare(scene, model, rays, hot, min_agree=0.999):
         assert len(key_ref) == len(key_hot), (fam, len(key_ref), len(key_hot))
         assert np.array_equal(key_ref[o_ref], key_hot[o_hot]), fam
         assert np.unique(key_ref).size == key_ref.size
-        cerr = np.abs(r_coord[o_ref] - h["coord"][o_hot]).max() if len(key_ref) else 0.0
-        assert cerr <= COORD_TOL, (fam, cerr)
+        _check_coords(r_coord[o_ref], h["coord"][o_hot], fam)
         f = _oracle_family(model, fam)
         x = oracle.encode(f["pos"], f["dir"], f["dist"], r_obj, r_coord)
         ref = oracle.dense_forward(f["w"], f["b"], f["dims"], x, sigmoid_head=0)[:, 0]

@@ -57,7 +57,9 @@ def test_infer_occlusion_matches_reference(sharing, gold, cuda):
                            (1, encode_inner_arrays, forward_inner_arrays, 5)):
         sel = kind == k
         prob[sel] = fwd(m, obj[sel], enc(m, obj[sel], coord[sel, :w]))[:, 0]
-    assert np.array_equal(prob, gold[f"prob_{sharing}"])
+    # logits are bit-exact (test_gpu_parity); the sigmoid's exp is CUDA's
+    # (<= 1 ulp from numba's libm), so probabilities agree to a few ulps
+    np.testing.assert_allclose(prob, gold[f"prob_{sharing}"], rtol=4e-16, atol=0)
     # tensor-core path: identical wherever the reference's probability is
     # decided beyond the logit tolerance (|logit| > 2e-2)
     fast = infer_occlusion(m, qs, exact=False)
