@@ -1,21 +1,34 @@
 """NIF shadow-ray visibility benchmark (BASELINE.json metric).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3|c4]
 
-Workload (BASELINE.json configs[1]): synthetic
-multi-object scene, 12 x icosphere(6) + NIF-enabled ground plane =
-983,042 triangles in 13 objects, 1920x1080, 1 spp direct-illumination
+Workload (BASELINE.json configs[1], the default at N=1):
+synthetic multi-object scene, 12 x icosphere(6) + NIF-enabled ground plane
+= 983,042 triangles in 13 objects, 1920x1080, 1 spp direct-illumination
 shadow rays, inference only. One step = one NIF visibility pass over the
 frame's shadow rays: phase-1 gather (top-level culling + fp64 T_outer /
 T_inner) -> fused grid encoding + visibility MLP (tcgen05) -> p < 0.5 ->
 per-ray OR. Rays are generated on the GPU by the sample pass (not timed).
 
-value : shadow rays resolved per second, whole job (sum over ranks),
-        rays resident in HBM, L2 flushed (256 MiB write) between steps.
-e2e   : the same through the public API with pinned host buffers
-        (H2D of origins/dirs/tmaxs + D2H of the per-ray bits every step).
-Multi-GPU: one process per GPU (torchrun), each rank owns its own frame
-(sample index = rank): weak scaling, no collective on the inference path.
+Multi-GPU (torchrun, one process per GPU): ONE frame
+split into N equal row bands (parallel.tile_pixels); rank r generates and
+resolves its own band's shadow rays -- no collective on the data path
+(strong scaling, total work = one frame). Default config under torchrun:
+C4 = the C2 scene at 3840x2160 (5.2M shadow rays), so per-GPU bands stay
+large at 8 GPUs; --config c2 splits the 1080p frame instead.
+
+value : shadow rays of the frame resolved per second (all bands), rays
+        resident in HBM, L2 flushed (256 MiB write) between steps, CUDA
+        events on the launching stream, max over ranks.
+e2e   : the same metric through the drop-in plugin NifBackend.occluded
+        (renderer.py:675-683) on pageable numpy rays -> bool[n]: the native
+        engine's C-ABI, staging through its pinned ring, H2D of the rays and
+        D2H of the answer every step; host clock around each synchronous
+        call, max over ranks.
+--impl reference: the reference CPU path restated in oracle/ (scene build,
+        seeded init, gather + encode + row-sequential MLP + OR) on the same
+        frame, host cores only; the B200 package is never imported.
 """
 
 from __future__ import annotations
@@ -43,7 +56,10 @@ WORKLOADS = {
     "c2": WORKLOAD,
     "c3": ("C3: 24x icosphere(8) + NIF plane, 31,457,282 tris, 25 objects, 1920x1080, "
            "1 spp point-light shadow rays, inference"),
+    "c4": ("C4: C2 scene (12x icosphere(6) + NIF plane, 983,042 tris) at 3840x2160, "
+           "1 spp point-light shadow rays, inference, frame split in row bands across GPUs"),
 }
+RESOLUTION = {"c1": (256, 256), "c2": (1920, 1080), "c3": (1920, 1080), "c4": (3840, 2160)}
 # kernels of one visibility pass (names as ncu reports them) and their
 # algorithmic work: see DESIGN.md section 4
 K_GATHER = "gather_warp_kernel"
@@ -55,9 +71,20 @@ def workload_label(args):
     """The workload string of the configuration actually run (resolution
     overrides included)."""
     base = WORKLOADS[args.config]
-    if args.config != "c1" and (args.width, args.height) != (1920, 1080):
-        base = base.replace("1920x1080", f"{args.width}x{args.height}")
+    w0, h0 = RESOLUTION[args.config]
+    if (args.width, args.height) != (w0, h0):
+        base = base.replace(f"{w0}x{h0}", f"{args.width}x{args.height}")
     return base
+
+
+def config_of(args, ws, n_frame, counts):
+    """The `config` object: identical on both arms for the same run."""
+    return {"workload": workload_label(args), "rays_per_frame": int(n_frame),
+            "outer_records": int(counts[0]), "inner_records": int(counts[1]),
+            "model": f"NifConfig() defaults (R 256/128, seed 0, random init), "
+                     f"sharing={args.sharing}",
+            "trained_epochs": args.train_epochs,
+            "parallelism": f"one frame split in {ws} row band(s), one per GPU"}
 
 
 def parse():
@@ -66,9 +93,10 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
-    p.add_argument("--width", type=int, default=1920)
-    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4"],
+                   help="default: c2 on one GPU, c4 (4K frame in row bands) under torchrun")
+    p.add_argument("--width", type=int, default=None)
+    p.add_argument("--height", type=int, default=None)
     p.add_argument("--train-epochs", type=int, default=0,
                    help="epochs of GPU training on 1 spp before timing (0 = random init)")
     p.add_argument("--sharing", default="shared", choices=["shared", "per_object"],
@@ -77,7 +105,13 @@ def parse():
     p.add_argument("--e2e-chunks", type=int, default=4,
                    help="chunks of the e2e host path (H2D of chunk k+1 overlaps chunk k)")
     p.add_argument("--profile", action="store_true", help="few steps, no clocks / cpu leg")
-    return p.parse_args()
+    args = p.parse_args()
+    if args.config is None:
+        args.config = "c2" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "c4"
+    w0, h0 = RESOLUTION[args.config]
+    args.width = w0 if args.width is None else args.width
+    args.height = h0 if args.height is None else args.height
+    return args
 
 
 def dist_setup(args):
@@ -152,7 +186,7 @@ def build_workload(args, rank, build_device=None):
     # (identical trees) -- the reference arm keeps the host builder
     if args.config == "c3":
         return synthetic.c3(args.width, args.height, build_device=build_device)
-    return synthetic.c2(args.width, args.height, build_device=build_device)
+    return synthetic.c2(args.width, args.height, build_device=build_device)  # c2, c4
 
 
 def cpu_path_step(scene, model, rays_np, n):
@@ -210,55 +244,49 @@ def cpu_baseline_leg(scene, model, rays_np, config, budget_s=20.0):
 
 
 def run_reference(args, rank, ws):
-    """--impl reference: the reference's CPU path (oracle port; the Python
-    reference cannot travel to the GPU box) on the host cores."""
+    """--impl reference: the reference's CPU path on the host cores, built
+    and run from oracle/ alone (oracle.refscene restates the scene build --
+    meshgen, _build_sah, pack -- and the seeded init; nif_oracle.c the
+    gather / encode / dense forward), on this run's whole frame. The Python
+    reference itself cannot travel to the GPU box. Under torchrun rank 0
+    alone runs and prints; the other ranks exit without work."""
     if rank != 0:
         return
-    from oracle import oracle
-    from paper_2306_07191_b200 import synthetic
-    from paper_2306_07191_b200.nif import NifConfig, init_arrays
-    scene = build_workload(args, rank)
-    # shadow rays from the oracle's own sample pass (same rays as ours)
+    from oracle import oracle, refscene
+    if args.config == "c1":
+        scene = refscene.c1(args.width, args.height)
+    elif args.config == "c3":
+        scene = refscene.lattice(24, 8, 0.3, args.width, args.height, cols=6)
+    else:
+        scene = refscene.lattice(12, 6, 0.35, args.width, args.height)
+    if args.sharing != "shared" or args.train_epochs:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "reference arm restates the shared, untrained default model only"}))
+        return
+    rays = scene.shadow_rays(0)
+    n = len(rays[2])
+    o_heads, i_heads, grids = refscene.init_model(scene.n_objects, seed=0)
+    fams = {"outer": refscene.family_arrays(o_heads, grids, "outer"),
+            "inner": refscene.family_arrays(i_heads, grids, "inner")}
     osc = oracle.OracleScene(scene.pack, scene.epsilon_t)
-    cum, kind, data = scene.light_tables()
-    sp = oracle.sample_pass(osc, scene.camera, cum, kind, data, scene.seed, 0)
-    cos = np.einsum("ij,ij->i", sp["normal"], sp["ldir"])
-    cast = sp["hit"] & (cos > 0) & (sp["pdf"] > 0)
-    rays = (sp["point"][cast], sp["ldir"][cast], sp["tmax"][cast])
-
-    class HostModel:
-        def __init__(self):
-            outer, inner, grids, _, _ = init_arrays(NifConfig(seed=0), scene.n_objects)
-            self._l = {"outer": outer[0], "inner": inner[0]}
-            self._g = grids
-
-        def host_layers(self, fam):
-            return [self._l[fam]]
-
-        def host_grids(self):
-            return self._g
-
-    model = HostModel()
-    n = min(len(rays[0]), 20000)
-    step = cpu_path_step(scene, model, rays, n)
+    kind = oracle.gather(osc, *rays, scene.nif_route_mask(None))[0]
+    counts = (int((kind == 0).sum()), int((kind == 1).sum()))
     for _ in range(args.warmup):
-        step()
+        refscene.visibility_pass(scene, fams, rays)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        step()
+        refscene.visibility_pass(scene, fams, rays)
         times.append(time.perf_counter() - t0)
     per = float(np.sum(times)) / args.steps
     value = n / per
     base = {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
-            "sample": f"{n} C2 shadow rays per step (first {n} of the frame), "
-                      "gather + encode + row-sequential MLP, all host threads"}
+            "sample": f"the whole frame per step ({n} shadow rays): gather + encode + "
+                      "row-sequential MLP + per-ray OR, all host threads (OpenMP)"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": WORKLOADS[args.config], "rays_per_frame": int(len(rays[0])),
-                       "sample_rays_per_step": n},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": config_of(args, ws, n, counts),
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -278,7 +306,12 @@ def main():
                                                 shadow_rays_dev)
     dev = torch.device("cuda", torch.cuda.current_device())
     scene = build_workload(args, rank, build_device=dev)
-    data = sample_pass_dev(scene, scene.camera, rank, scene.seed)
+    # this rank's row band of the frame (the whole frame at N=1); the sample
+    # pass keys its RNG by the global pixel index, so the bands' rays are
+    # exactly the single-GPU frame's
+    from paper_2306_07191_b200.parallel import tile_pixels
+    pix0, n_pix = tile_pixels(scene.camera.width, scene.camera.height, rank, ws)
+    data = sample_pass_dev(scene, scene.camera, 0, scene.seed, "importance", pix0, n_pix)
     _, o, d, t = shadow_rays_dev(data, require_emit=False)
     n = int(t.numel())
     model = build_model(NifConfig(seed=0, sharing=args.sharing), scene)
@@ -384,14 +417,14 @@ def main():
     from paper_2306_07191_b200.pipeline import render_dev
     nif_be = NifBackend(model)
     render_ms = {}
-    for name, be in (("nif", nif_be), ("bvh", BvhBackend())):
+    for name, be in ((("nif", nif_be), ("bvh", BvhBackend())) if ws == 1 else ()):
         for _ in range(2):
-            render_dev(scene, be, spp=1, sample_offset=rank)
+            render_dev(scene, be, spp=1)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(5):
-            render_dev(scene, be, spp=1, sample_offset=rank)
+            render_dev(scene, be, spp=1)
         e1.record(stream)
         e1.synchronize()
         render_ms[name] = e0.elapsed_time(e1) / 5
@@ -463,13 +496,20 @@ def main():
     # --- reduce over ranks (max time) ---------------------------------------
     ms, e2e_ms = ms_local, e2e_ms_local
     n_total = n
+    frame_counts = [int(counts[0]), int(counts[1])]
+    band_ms = [ms_local / args.steps]
     if ws > 1:
         tt = torch.tensor([ms_local, e2e_ms_local], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms, e2e_ms = float(tt[0]), float(tt[1])
-        nn = torch.tensor([n], device=dev, dtype=torch.int64)
+        nn = torch.tensor([n, int(counts[0]), int(counts[1])], device=dev, dtype=torch.int64)
         torch.distributed.all_reduce(nn)
-        n_total = int(nn)
+        n_total = int(nn[0])
+        frame_counts = [int(nn[1]), int(nn[2])]
+        per = torch.zeros(ws, device=dev, dtype=torch.float64)
+        per[rank] = ms_local / args.steps
+        torch.distributed.all_reduce(per)
+        band_ms = per.cpu().tolist()
     if rank != 0:
         return
     value = n_total * args.steps / (ms / 1e3)
@@ -521,7 +561,7 @@ def main():
     rooflines = {k: roof_of(k) for k in ("gather", "query_outer", "query_inner")}
 
     cpu = None
-    if not args.no_cpu_baseline and not args.profile:
+    if not args.no_cpu_baseline and not args.profile and ws == 1:
         try:
             rays_np = (rays_host.origins, rays_host.dirs, rays_host.tmaxs)
             cpu = cpu_baseline_leg(scene, model, rays_np, args.config)
@@ -531,16 +571,14 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp16-mma/fp32-acc (fp64 gather)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp16-mma/fp32-acc (fp64 gather)",
         "data": "synthetic",
-        "config": {"workload": workload_label(args), "rays_per_frame_per_gpu": n,
-                   "outer_records": n_outer,
-                   "inner_records": n_inner, "model": f"NifConfig() defaults (R 256/128), sharing={args.sharing}",
-                   "trained_epochs": args.train_epochs, "l2": "flushed (256 MiB write) per step",
-                   "parallelism": f"{ws} independent frames (sample index = rank)"},
+        "config": config_of(args, ws, n_total, frame_counts),
+        "l2": "flushed (256 MiB write) between steps",
         "frame_ms": ms / args.steps,
+        "band_ms_per_rank": band_ms,
         # SURVEY 8(d) metric (i) also asks for (ray, object) records per second
-        "records_per_s": (n_outer + n_inner) * ws * args.steps / (ms / 1e3),
+        "records_per_s": sum(frame_counts) * args.steps / (ms / 1e3),
         "bvh_ms_per_frame": kt["bvh_anyhit"],
         "render_ms_per_frame_1spp": render_ms,
         "kernel_ms": kt,
@@ -548,7 +586,7 @@ def main():
         "rooflines": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": int(n * 56), "d2h_bytes_per_step": int(n),
+                "h2d_bytes_per_step": int(n_total * 56), "d2h_bytes_per_step": int(n_total),
                 "api": "NifBackend.occluded(scene, ShadowRays of numpy f64 arrays) -> bool[n] "
                        "(native engine, C-ABI nif_engine_occluded_host)",
                 "parity_with_device_path": e2e_parity,

@@ -612,3 +612,177 @@ int oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ---- bvh.py:34-303 (_build_sah) ----------------------------------------
+ * Binned SAH, depth-first with an explicit stack, stable partition by bin
+ * index, "halve by current order" when centroids collapse. Outputs sized
+ * for 2n nodes; returns the node count. Single-threaded like the reference
+ * (the order of the node ids is the reference's stack discipline). */
+static int sah_bin(double c, double cmin, double ext, int64_t n_bins) {
+  int64_t b = (int64_t)((double)n_bins * (c - cmin) / ext);
+  if (b >= n_bins) b = n_bins - 1;
+  if (b < 0) b = 0;
+  return (int)b;
+}
+
+int64_t oracle_build_sah(const double* lo, const double* hi, const double* ce, int64_t n,
+                         int64_t max_leaf, int64_t n_bins, double c_trav, double c_isect,
+                         double* node_lo, double* node_hi, int64_t* node_a, int64_t* node_b,
+                         uint8_t* node_leaf, int64_t* order) {
+  int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t* stack = (int64_t*)malloc(sizeof(int64_t) * 3 * (size_t)(2 * n + 8));
+  int64_t* bin_cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_bins);
+  double* bin_lo = (double*)malloc(sizeof(double) * 3 * (size_t)n_bins);
+  double* bin_hi = (double*)malloc(sizeof(double) * 3 * (size_t)n_bins);
+  double* left_sa = (double*)malloc(sizeof(double) * (size_t)n_bins);
+  double* right_sa = (double*)malloc(sizeof(double) * (size_t)n_bins);
+  int64_t* left_n = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_bins);
+  int64_t* right_n = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_bins);
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  for (int64_t i = 0; i < 2 * n; ++i) {
+    node_a[i] = 0;
+    node_b[i] = 0;
+    node_leaf[i] = 0;
+  }
+  stack[0] = 0;
+  stack[1] = 0;
+  stack[2] = n;
+  int64_t sp = 1, n_nodes = 1;
+  while (sp > 0) {
+    --sp;
+    const int64_t idx = stack[3 * sp], start = stack[3 * sp + 1], end = stack[3 * sp + 2];
+    const int64_t count = end - start;
+    double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double cl[3] = {INFINITY, INFINITY, INFINITY}, chh[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = start; i < end; ++i) {
+      const int64_t p = order[i];
+      for (int c = 0; c < 3; ++c) {
+        if (lo[3 * p + c] < bl[c]) bl[c] = lo[3 * p + c];
+        if (hi[3 * p + c] > bh[c]) bh[c] = hi[3 * p + c];
+      }
+      for (int c = 0; c < 3; ++c) {
+        if (ce[3 * p + c] < cl[c]) cl[c] = ce[3 * p + c];
+        if (ce[3 * p + c] > chh[c]) chh[c] = ce[3 * p + c];
+      }
+    }
+    for (int c = 0; c < 3; ++c) {
+      node_lo[3 * idx + c] = bl[c];
+      node_hi[3 * idx + c] = bh[c];
+    }
+    double best_cost = INFINITY;
+    int best_axis = -1;
+    int64_t best_k = -1;
+    if (count > 1) {
+      const double dx = bh[0] - bl[0], dy = bh[1] - bl[1], dz = bh[2] - bl[2];
+      const double sa_node = 2.0 * (dx * dy + dy * dz + dz * dx);
+      if (sa_node > 1e-300) {
+        for (int axis = 0; axis < 3; ++axis) {
+          const double cmin = cl[axis], ext = chh[axis] - cl[axis];
+          if (ext <= 0.0) continue;
+          for (int64_t k = 0; k < n_bins; ++k) {
+            bin_cnt[k] = 0;
+            for (int c = 0; c < 3; ++c) {
+              bin_lo[3 * k + c] = INFINITY;
+              bin_hi[3 * k + c] = -INFINITY;
+            }
+          }
+          for (int64_t i = start; i < end; ++i) {
+            const int64_t p = order[i];
+            const int b = sah_bin(ce[3 * p + axis], cmin, ext, n_bins);
+            bin_cnt[b] += 1;
+            for (int c = 0; c < 3; ++c) {
+              if (lo[3 * p + c] < bin_lo[3 * b + c]) bin_lo[3 * b + c] = lo[3 * p + c];
+              if (hi[3 * p + c] > bin_hi[3 * b + c]) bin_hi[3 * b + c] = hi[3 * p + c];
+            }
+          }
+          for (int dir = 0; dir < 2; ++dir) {  /* left sweep, then right sweep */
+            double a[3] = {INFINITY, INFINITY, INFINITY}, bb[3] = {-INFINITY, -INFINITY, -INFINITY};
+            int64_t cnt = 0;
+            for (int64_t j = 0; j < n_bins; ++j) {
+              const int64_t k = dir == 0 ? j : n_bins - 1 - j;
+              if (bin_cnt[k] > 0)
+                for (int c = 0; c < 3; ++c) {
+                  if (bin_lo[3 * k + c] < a[c]) a[c] = bin_lo[3 * k + c];
+                  if (bin_hi[3 * k + c] > bb[c]) bb[c] = bin_hi[3 * k + c];
+                }
+              cnt += bin_cnt[k];
+              double sa = 0.0;
+              if (cnt > 0) {
+                const double ex = bb[0] - a[0], ey = bb[1] - a[1], ez = bb[2] - a[2];
+                sa = 2.0 * (ex * ey + ey * ez + ez * ex);
+              }
+              if (dir == 0) {
+                left_n[k] = cnt;
+                left_sa[k] = sa;
+              } else {
+                right_n[k] = cnt;
+                right_sa[k] = sa;
+              }
+            }
+          }
+          for (int64_t k = 0; k < n_bins - 1; ++k) {
+            const int64_t nl = left_n[k], nr = right_n[k + 1];
+            if (nl == 0 || nr == 0) continue;
+            const double cost =
+                c_trav + (left_sa[k] * (double)nl + right_sa[k + 1] * (double)nr) * c_isect / sa_node;
+            if (cost < best_cost) {
+              best_cost = cost;
+              best_axis = axis;
+              best_k = k;
+            }
+          }
+        }
+      }
+    }
+    int do_split = 0;
+    int64_t mid = start;
+    if (best_axis >= 0 && (count > max_leaf || best_cost < c_isect * (double)count)) {
+      const double cmin = cl[best_axis], ext = chh[best_axis] - cl[best_axis];
+      int64_t nl = 0;
+      for (int64_t i = start; i < end; ++i) {
+        const int64_t p = order[i];
+        if (sah_bin(ce[3 * p + best_axis], cmin, ext, n_bins) <= best_k) tmp[nl++] = p;
+      }
+      int64_t nr = nl;
+      for (int64_t i = start; i < end; ++i) {
+        const int64_t p = order[i];
+        if (sah_bin(ce[3 * p + best_axis], cmin, ext, n_bins) > best_k) tmp[nr++] = p;
+      }
+      for (int64_t i = 0; i < count; ++i) order[start + i] = tmp[i];
+      mid = start + nl;
+      do_split = 1;
+    } else if (count > max_leaf) {
+      mid = start + count / 2;
+      do_split = 1;
+    }
+    if (do_split) {
+      const int64_t left = n_nodes, right = n_nodes + 1;
+      n_nodes += 2;
+      node_a[idx] = left;
+      node_b[idx] = right;
+      node_leaf[idx] = 0;
+      stack[3 * sp] = right;
+      stack[3 * sp + 1] = mid;
+      stack[3 * sp + 2] = end;
+      ++sp;
+      stack[3 * sp] = left;
+      stack[3 * sp + 1] = start;
+      stack[3 * sp + 2] = mid;
+      ++sp;
+    } else {
+      node_a[idx] = start;
+      node_b[idx] = count;
+      node_leaf[idx] = 1;
+    }
+  }
+  free(tmp);
+  free(stack);
+  free(bin_cnt);
+  free(bin_lo);
+  free(bin_hi);
+  free(left_sa);
+  free(right_sa);
+  free(left_n);
+  free(right_n);
+  return n_nodes;
+}
