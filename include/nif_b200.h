@@ -288,6 +288,42 @@ int nif_adam_units_dev(const nif_family_view* f, const nif_train_view* t, double
                        double beta1, double beta2, double eps, int64_t* cursor, int64_t delta,
                        void* stream);
 
+/* Data-parallel / deterministic form of the fused step (nif.py:682-749):
+ * the same forward / loss / backward over rows idx[(cursor ? *cursor : 0) +
+ * row0 + k*row_step], with the gradients routed to caller buffers:
+ *   mlp_grad  (NULL: t->grad + t->off_w) receives the MLP gradients in the
+ *             family layout [w | pad | b] (off_b - off_w + n_heads*b_stride
+ *             floats), accumulated by fp32 atomics, or
+ *   mlp_part  (non-NULL: deterministic) per-CTA partial sums, reduced in CTA
+ *             order into mlp_grad after the kernel (part_floats >=
+ *             nif_train_part_floats(n_rows));
+ *   dx_out    (non-NULL) the fp32 input gradient of batch row g at
+ *             dx_out[g*IN + k] (IN = dims[0]) instead of the grid scatter,
+ *             which nif_grid_scatter_dev then applies for the whole batch.
+ * A data-parallel rank writes only its own rows of dx_out: zero the buffer,
+ * all-reduce [dx_out | mlp_grad] (one collective), scatter every row.     */
+int nif_train_fwdbwd_ex_dev(const nif_family_view* f, const nif_train_view* t,
+                            const int64_t* obj, const double* coord, const float* label,
+                            const int64_t* idx, const int64_t* cursor, int64_t n_rows,
+                            int64_t row0, int64_t row_step, double* sq_err, float* dx_out,
+                            float* mlp_grad, float* mlp_part, int64_t part_floats, void* stream);
+int64_t nif_train_part_floats(const nif_family_view* f, const nif_train_view* t, int64_t n_rows);
+
+/* Grid-gradient scatter of a whole batch from its input gradients dx
+ * [n_rows][IN] (grids.py:171-202 accumulate_grad_{2d,1d}_batch: corner
+ * contribution (float)(w_fp64 * dx), added into t->grad). deterministic=0:
+ * fp32 atomics, warp-aggregated (lanes hitting one cell are summed in lane
+ * order, one atomic per group and latent). deterministic=1: contributions
+ * sorted by (cell, corner, batch row) -- the reference's np.add.at order --
+ * and summed sequentially per cell, bit-reproducible run to run; needs
+ * ws_bytes >= nif_grid_scatter_ws_bytes(n_rows) of device workspace.      */
+size_t nif_grid_scatter_ws_bytes(const nif_family_view* f, const nif_train_view* t,
+                                 int64_t n_rows);
+int nif_grid_scatter_dev(const nif_family_view* f, const nif_train_view* t, const int64_t* obj,
+                         const double* coord, const int64_t* idx, const int64_t* cursor,
+                         int64_t n_rows, const float* dx, int deterministic, void* ws,
+                         size_t ws_bytes, void* stream);
+
 /* Adam (grids.py:31-45) on every touched object's grids (dense, all
  * cells) and on each touched MLP head; fp64 moments over fp32 storage,
  * numba's integer power for the bias correction; clears the gradients of

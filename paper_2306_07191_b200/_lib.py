@@ -174,6 +174,13 @@ _SIGS = {
     "nif_train_fwdbwd_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
                                        I64, I64, I64, P, P]),
     "nif_adam_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), D, D, D, D, P]),
+    "nif_train_fwdbwd_ex_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P,
+                                          P, P, I64, I64, I64, P, P, P, P, I64, P]),
+    "nif_train_part_floats": (C.c_int64, [C.POINTER(FamilyView), C.POINTER(TrainView), I64]),
+    "nif_grid_scatter_ws_bytes": (C.c_size_t, [C.POINTER(FamilyView), C.POINTER(TrainView),
+                                               I64]),
+    "nif_grid_scatter_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
+                                       I64, P, C.c_int, P, C.c_size_t, P]),
     "nif_sample_pass_dev": (C.c_int, [C.POINTER(SceneView), C.POINTER(Camera),
                                       C.POINTER(LightsView), I64, I64, I32, I64, I64,
                                       C.POINTER(PassOut), P]),
@@ -200,7 +207,7 @@ def declared_symbols():
     import re
     hdr = (_HERE.parent / "include" / "nif_b200.h").read_text()
     hdr += (_HERE.parent / "include" / "nif_b200_debug.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(nif_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(nif_\w+)\s*\(",
                                  hdr, re.M)))
 
 

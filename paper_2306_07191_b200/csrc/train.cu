@@ -15,6 +15,7 @@
 // gradients are fp32 atomics of (fp64 weight * upstream) rounded to fp32,
 // the reference's np.add.at contributions.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cstdlib>
 #include <stdint.h>
 
@@ -85,7 +86,27 @@ struct TrainArgs {
   int64_t n_rows, row0, row_step;
   double* sq_err;
   const int64_t* cursor;  // device row offset added to idx (graph-replayed steps), or NULL
+  // gradient sinks (nif_train_fwdbwd_ex_dev): MLP gradients go to mlp_dst
+  // ([w | pad | b], the family buffer's layout from off_w) by fp32 atomics,
+  // or -- deterministic mode -- as this CTA's partial sums into row
+  // blockIdx.x of mlp_part ([n_cta][n_mlp], reduced in CTA order after the
+  // kernel); with dx_out set, the input gradient of batch row g is stored at
+  // dx_out[g * IN + k] instead of being scattered into the grids
+  float* mlp_dst;
+  float* mlp_part;
+  int64_t n_mlp;
+  float* dx_out;
+  int64_t part_cap;  // floats in mlp_part
 };
+
+thread_local unsigned g_last_ctas = 0;  // CTAs of the last fwd/bwd launch (host)
+
+__device__ __forceinline__ void mlp_put(const TrainArgs& a, float* dst, float s) {
+  if (a.mlp_part != nullptr)
+    a.mlp_part[(size_t)blockIdx.x * a.n_mlp + (size_t)(dst - a.mlp_dst)] = s;
+  else
+    atomicAdd(dst, s);
+}
 
 // idx + *cursor: a CUDA graph of one optimiser step is replayed per batch
 // while the batch start lives on the device
@@ -138,8 +159,8 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
   const int n_uniq = s_nuniq;
   const float* Wt = f.w + (size_t)head * f.w_stride;
   const float* Bt = f.b + (size_t)head * f.b_stride;
-  float* gW0 = a.t.grad + a.t.off_w;
-  float* gB0 = a.t.grad + a.t.off_b;
+  float* gW0 = a.mlp_dst;
+  float* gB0 = a.mlp_dst + (a.t.off_b - a.t.off_w);
   const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
 
   // ---- encode (grids.py:141-191: fp64 weights, fp64 sum, fp32 result) ----
@@ -254,11 +275,11 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
         for (int r = 0; r < RB; ++r)
           if (s_rhead[r] == hh)
             s = fmaf(dh[r * kMaxOut + q], leaky(zs[((size_t)(L - 1) * RB + r) * WP + k]), s);
-        atomicAdd(gW + wo_h + q * W + k, s);
+        mlp_put(a, gW + wo_h + q * W + k, s);
       } else {
         for (int r = 0; r < RB; ++r)
           if (s_rhead[r] == hh) s += dh[r * kMaxOut + q];
-        atomicAdd(gB + bo_h + q, s);
+        mlp_put(a, gB + bo_h + q, s);
       }
     }
   }
@@ -281,11 +302,11 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
             if (s_rhead[r] == hh)
               s = fmaf(dzc[(size_t)r * WP + j], leaky(zs[((size_t)(l - 1) * RB + r) * WP + k]),
                        s);
-          atomicAdd(gW + wo + (size_t)j * W + k, s);
+          mlp_put(a, gW + wo + (size_t)j * W + k, s);
         } else {
           for (int r = 0; r < RB; ++r)
             if (s_rhead[r] == hh) s += dzc[(size_t)r * WP + j];
-          atomicAdd(gB + bo + j, s);
+          mlp_put(a, gB + bo + j, s);
         }
       }
     }
@@ -316,11 +337,11 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
       if (k < IN) {
         for (int r = 0; r < RB; ++r)
           if (s_rhead[r] == hh) s = fmaf(dzc[(size_t)r * WP + j], xs[r * kMaxIn + k], s);
-        atomicAdd(gW + (size_t)j * IN + k, s);
+        mlp_put(a, gW + (size_t)j * IN + k, s);
       } else {
         for (int r = 0; r < RB; ++r)
           if (s_rhead[r] == hh) s += dzc[(size_t)r * WP + j];
-        atomicAdd(gB + j, s);
+        mlp_put(a, gB + j, s);
       }
     }
   }
@@ -332,6 +353,10 @@ __global__ void train_fwdbwd_kernel(TrainArgs a) {
     const float* dc = dzc + (size_t)tid * WP;
     for (int j = 0; j < W; ++j) s = fmaf(dc[j], __ldg(Wt + (size_t)j * IN + k), s);
     dx[k] = s;
+  }
+  if (a.dx_out != nullptr) {  // data-parallel / deterministic: the scatter runs later
+    for (int k = 0; k < IN; ++k) a.dx_out[g * IN + k] = dx[k];
+    return;
   }
   const size_t g2 = (size_t)f.R * f.R * f.N;
   float* gpos = a.t.grad + a.t.off_pos + (size_t)o * g2;
@@ -653,8 +678,8 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
   float* sb = sm + T.sb;    // every layer's biases
   double* rwd = reinterpret_cast<double*>(sm) + T.rwd;
   int* rwi = reinterpret_cast<int*>(sm) + T.rwi;
-  float* gW = a.t.grad + a.t.off_w;
-  float* gB = a.t.grad + a.t.off_b;
+  float* gW = a.mlp_dst;
+  float* gB = a.mlp_dst + (a.t.off_b - a.t.off_w);
   const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
   const int tc = tid & 15, tr = tid >> 4;  // 16 column groups x TT/16 row groups of RPT
 
@@ -834,10 +859,10 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     float s = 0.f;
     if (k < W) {
       for (int r = 0; r < RB; ++r) s = fmaf(dh[r * kMaxOut + q], zl[r * WP + k], s);
-      atomicAdd(gW + wo_h + q * W + k, s);
+      mlp_put(a, gW + wo_h + q * W + k, s);
     } else {
       for (int r = 0; r < RB; ++r) s += dh[r * kMaxOut + q];
-      atomicAdd(gB + bo_h + q, s);
+      mlp_put(a, gB + bo_h + q, s);
     }
   }
   __syncthreads();
@@ -873,11 +898,11 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
       for (int cj = 0; cj < CPT; ++cj)
 #pragma unroll
         for (int ck = 0; ck < CPT; ++ck)
-          atomicAdd(gW + wo + (size_t)(tj + 16 * cj) * W + tk + 16 * ck, g[cj][ck]);
+          mlp_put(a, gW + wo + (size_t)(tj + 16 * cj) * W + tk + 16 * ck, g[cj][ck]);
       if (tid < W) {
         float sbias = 0.f;
         for (int r = 0; r < RB; ++r) sbias += dzc[r * WP + tid];
-        atomicAdd(gB + bo + tid, sbias);
+        mlp_put(a, gB + bo + tid, sbias);
       }
     } else {
       for (int e = tid; e < W * (W + 1); e += TT) {
@@ -885,10 +910,10 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
         float s = 0.f;
         if (k < W) {
           for (int r = 0; r < RB; ++r) s = fmaf(dzc[r * WP + j], zp[r * WP + k], s);
-          atomicAdd(gW + wo + (size_t)j * W + k, s);
+          mlp_put(a, gW + wo + (size_t)j * W + k, s);
         } else {
           for (int r = 0; r < RB; ++r) s += dzc[r * WP + j];
-          atomicAdd(gB + bo + j, s);
+          mlp_put(a, gB + bo + j, s);
         }
       }
     }
@@ -927,10 +952,10 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     float s = 0.f;
     if (k < IN) {
       for (int r = 0; r < RB; ++r) s = fmaf(dzc[r * WP + j], xs[r * kMaxIn + k], s);
-      atomicAdd(gW + (size_t)j * IN + k, s);
+      mlp_put(a, gW + (size_t)j * IN + k, s);
     } else {
       for (int r = 0; r < RB; ++r) s += dzc[r * WP + j];
-      atomicAdd(gB + j, s);
+      mlp_put(a, gB + j, s);
     }
   }
   // dx = dZ_0 W_0, one (row, input) per thread -> grid scatter
@@ -943,6 +968,11 @@ __global__ void __launch_bounds__(TT) train_fwdbwd_tiled_kernel(TrainArgs a) {
     float s = 0.f;
     const float* dc = dzc + (size_t)r * WP;
     for (int j = 0; j < W; ++j) s = fmaf(dc[j], sw[j * INP + k], s);
+    if (a.dx_out != nullptr) {  // data-parallel / deterministic: the scatter runs later
+      const int64_t g = a.row0 + ((int64_t)blockIdx.x * RB + r) * a.row_step;
+      a.dx_out[g * IN + k] = s;
+      continue;
+    }
     const double dx = (double)s;
     if (k < 2 * f.N) {
       const bool is_pos = k < f.N;
@@ -976,6 +1006,9 @@ int launch_fwdbwd_tiled_rb(const TrainArgs& a, cudaStream_t st) {
   const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
   if (my_rows <= 0) return NIF_OK;
   const unsigned grid = (unsigned)((my_rows + RB - 1) / RB);
+  if (a.mlp_part != nullptr && (int64_t)grid * a.n_mlp > a.part_cap)
+    return fail(NIF_ERR_VALUE, "MLP partials buffer too small (%lld CTAs)", (long long)grid);
+  g_last_ctas = grid;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(TT);
@@ -1016,11 +1049,22 @@ int launch_fwdbwd(const TrainArgs& a, cudaStream_t st) {
   const int64_t my_rows = (a.n_rows - a.row0 + a.row_step - 1) / a.row_step;
   if (my_rows <= 0) return NIF_OK;
   const unsigned grid = (unsigned)((my_rows + rb - 1) / rb);
+  if (a.mlp_part != nullptr && (int64_t)grid * a.n_mlp > a.part_cap)
+    return fail(NIF_ERR_VALUE, "MLP partials buffer too small (%lld CTAs)", (long long)grid);
+  if (a.mlp_part != nullptr)  // per-head partials: a CTA writes only its own heads' rows
+    cudaMemsetAsync(a.mlp_part, 0, (size_t)grid * a.n_mlp * sizeof(float), st);
+  g_last_ctas = grid;
   kern<<<grid, rb, smem, st>>>(a);
   return check_launch("nif_train_fwdbwd_dev");
 }
 
 }  // namespace
+}  // namespace nif
+
+namespace nif {
+namespace {
+int launch_fwdbwd_any(const TrainArgs& a, cudaStream_t st);
+}
 }  // namespace nif
 
 using namespace nif;
@@ -1064,15 +1108,23 @@ extern "C" int nif_train_fwdbwd_cur_dev(const nif_family_view* f, const nif_trai
                                         const float* label, const int64_t* idx,
                                         const int64_t* cursor, int64_t n_rows, int64_t row0,
                                         int64_t row_step, double* sq_err, void* stream) {
-  if (n_rows <= 0) return NIF_OK;
+  TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err, cursor,
+              t->grad + t->off_w, nullptr, 0, nullptr, 0};
+  return launch_fwdbwd_any(a, (cudaStream_t)stream);
+}
+
+namespace nif {
+namespace {
+int launch_fwdbwd_any(const TrainArgs& a, cudaStream_t st) {
+  const nif_family_view* f = &a.f;
+  g_last_ctas = 0;
+  if (a.n_rows <= 0) return NIF_OK;
   if (f->n_layers < 2) return fail(NIF_ERR_UNSUPPORTED, "training needs at least one hidden layer");
   if (f->dims[0] > kMaxIn) return fail(NIF_ERR_UNSUPPORTED, "input width above %d", kMaxIn);
   if (f->dims[f->n_layers] > kMaxOut) return fail(NIF_ERR_UNSUPPORTED, "head wider than %d", kMaxOut);
   for (int i = 2; i < f->n_layers; ++i)
     if (f->dims[i] != f->dims[1]) return fail(NIF_ERR_UNSUPPORTED, "hidden widths must match");
-  if (row_step < 1 || row0 < 0) return fail(NIF_ERR_VALUE, "bad row partition");
-  TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err, cursor};
-  cudaStream_t st = (cudaStream_t)stream;
+  if (a.row_step < 1 || a.row0 < 0) return fail(NIF_ERR_VALUE, "bad row partition");
   if (g_train_variant != 1 && f->n_heads == 1) {
     switch (f->dims[1]) {
       case 16: return launch_fwdbwd_tiled<16>(a, st);
@@ -1095,6 +1147,8 @@ extern "C" int nif_train_fwdbwd_cur_dev(const nif_family_view* f, const nif_trai
     default: return fail(NIF_ERR_UNSUPPORTED, "hidden width %d not instantiated", f->dims[1]);
   }
 }
+}  // namespace
+}  // namespace nif
 
 extern "C" int nif_debug_set_train_variant(int v) {
   g_train_variant = v;
@@ -1187,4 +1241,249 @@ extern "C" int nif_adam_units_dev(const nif_family_view* f, const nif_train_view
                                   int64_t delta, void* stream) {
   launch_adam_units(f, t, lr, beta1, beta2, eps, cursor, delta, (cudaStream_t)stream);
   return check_launch("nif_adam_units_dev");
+}
+
+// ---------------------------------------------------------------------------
+// Gradient sinks for data-parallel and deterministic training
+// ---------------------------------------------------------------------------
+namespace nif {
+namespace {
+
+// dst[i] += sum_c part[c][i], CTAs in order (deterministic MLP gradients);
+// the [w | pad | b] padding is skipped
+__global__ void mlp_reduce_kernel(const float* __restrict__ part, int n_cta, int64_t n_mlp,
+                                  int64_t w_end, int64_t b_begin, float* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_mlp || (i >= w_end && i < b_begin)) return;
+  float s = 0.f;
+  for (int c = 0; c < n_cta; ++c) s += part[(size_t)c * n_mlp + i];
+  dst[i] += s;
+}
+
+struct ScatterArgs {
+  nif_family_view f;
+  nif_train_view t;
+  const int64_t* obj;
+  const double* coord;
+  const int64_t* idx;
+  const int64_t* cursor;
+  int64_t n_rows;
+  const float* dx;  // [n_rows][IN]
+  int slots;        // 8 (outer: 4 pos + 4 dir corners) or 10 (+ 2 dist)
+  int gbits;        // bits of the batch position in a sort key
+};
+
+// One contribution slot of batch row g: the grid cell (element offset of its
+// first latent in the family buffer), the latent count, the fp64 corner
+// weight and the offset of the matching inputs in dx -- grids.py:125-150
+// corner order 00, 01, 10, 11 (2-D), i0, i1 (1-D)
+struct Contrib {
+  int64_t elem;
+  int n, kbase;
+  double w;
+};
+
+__device__ __forceinline__ Contrib contrib(const ScatterArgs& a, int64_t g, int slot) {
+  const nif_family_view& f = a.f;
+  const int64_t* bidx = batch_idx(a.idx, a.cursor);
+  const int64_t row = bidx ? bidx[g] : g;
+  const int o = (int)a.obj[row];
+  const int cw = f.family == NIF_FAMILY_OUTER ? 4 : 5;
+  const double* c = a.coord + row * cw;
+  Contrib r;
+  if (slot < 8) {
+    const bool pos = slot < 4;
+    const Bil64 b = pos ? bil64(c[0], c[1], f.R) : bil64(c[2], c[3], f.R);
+    const int q = slot & 3;
+    r.elem = (pos ? a.t.off_pos : a.t.off_dir) + ((int64_t)o * f.R * f.R + b.c[q]) * f.N;
+    r.n = f.N;
+    r.kbase = pos ? 0 : f.N;
+    r.w = b.w[q];
+  } else {
+    const Axis ax = axis_indices(c[4], f.Rd, false);
+    const bool hi = slot == 9;
+    r.elem = a.t.off_dist + ((int64_t)o * f.Rd + (hi ? ax.i1 : ax.i0)) * f.Nd;
+    r.n = f.Nd;
+    r.kbase = 2 * f.N;
+    r.w = hi ? ax.w : 1.0 - ax.w;
+  }
+  return r;
+}
+
+// Atomic scatter, warp-aggregated: a warp takes 32 consecutive batch rows
+// of one slot; lanes that hit the same cell are combined (lane order) with
+// __match_any_sync and the group's leader issues one fp32 atomic per latent.
+__global__ void __launch_bounds__(256) scatter_atomic_kernel(ScatterArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = t >> 5;
+  const int slot = (int)(wid % a.slots);
+  const int64_t g = (wid / a.slots) * 32 + lane;
+  const bool valid = g < a.n_rows;
+  const int IN = a.f.dims[0];
+  Contrib c{};
+  if (valid) c = contrib(a, g, slot);
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const unsigned peers = __match_any_sync(act, c.elem);
+  const int leader = __ffs(peers) - 1;
+  float* dst = a.t.grad + c.elem;
+  for (int k = 0; k < c.n; ++k) {
+    // grids.py:175: (w * up).astype(f32), then added into the fp32 grad
+    float v = (float)(c.w * (double)a.dx[g * IN + c.kbase + k]);
+    // leader accumulates its peers in ascending lane order
+    unsigned rest = peers & ~(1u << lane);
+    float sum = v;
+    while (__any_sync(act, rest != 0u)) {
+      const int src = rest ? __ffs(rest) - 1 : lane;
+      const float pv = __shfl_sync(act, v, src);
+      if (rest) {
+        sum += pv;
+        rest &= rest - 1;
+      }
+    }
+    if (lane == leader) atomicAdd(dst + k, sum);
+  }
+}
+
+__device__ __forceinline__ int slot_group(const ScatterArgs& a, int64_t elem) {
+  return elem >= a.t.off_dist && a.f.family == NIF_FAMILY_INNER ? 2
+       : (elem >= a.t.off_dir ? 1 : 0);
+}
+
+// Deterministic scatter, pass 1: one sort key per contribution,
+// (cell element, corner, batch position) -- np.add.at's order for that cell
+__global__ void scatter_keys_kernel(ScatterArgs a, uint64_t* __restrict__ keys) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.n_rows * a.slots) return;
+  const int64_t g = t / a.slots;
+  const int slot = (int)(t - g * a.slots);
+  const Contrib c = contrib(a, g, slot);
+  const int corner = slot < 8 ? (slot & 3) : slot - 8;
+  keys[t] = ((uint64_t)c.elem << (a.gbits + 2)) | ((uint64_t)corner << a.gbits) | (uint64_t)g;
+}
+
+// pass 2: the first key of each cell walks the cell's run in sorted order,
+// adding every contribution into fp32 accumulators seeded with the grad
+__global__ void scatter_segments_kernel(ScatterArgs a, const uint64_t* __restrict__ keys,
+                                        int64_t n_keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_keys) return;
+  const int sh = a.gbits + 2;
+  const uint64_t elem = keys[i] >> sh;
+  if (i > 0 && (keys[i - 1] >> sh) == elem) return;
+  const int IN = a.f.dims[0];
+  const int grp = slot_group(a, (int64_t)elem);
+  const int n = grp == 2 ? a.f.Nd : a.f.N;
+  float acc[kMaxIn];
+  float* dst = a.t.grad + elem;
+  for (int k = 0; k < n; ++k) acc[k] = dst[k];
+  const uint64_t gmask = (1ull << a.gbits) - 1;
+  for (int64_t j = i; j < n_keys && (keys[j] >> sh) == elem; ++j) {
+    const int64_t g = (int64_t)(keys[j] & gmask);
+    const int corner = (int)((keys[j] >> a.gbits) & 3);
+    const int slot = grp == 2 ? 8 + corner : grp * 4 + corner;
+    const Contrib c = contrib(a, g, slot);
+    for (int k = 0; k < n; ++k) acc[k] += (float)(c.w * (double)a.dx[g * IN + c.kbase + k]);
+  }
+  for (int k = 0; k < n; ++k) dst[k] = acc[k];
+}
+
+int bits_for(uint64_t v) {
+  int b = 0;
+  while (b < 64 && (v >> b) != 0) ++b;
+  return b;
+}
+
+struct ScatterWs {
+  uint64_t* keys_in;
+  uint64_t* keys_out;
+  void* temp;
+  size_t temp_bytes, total;
+};
+
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+ScatterWs scatter_ws(int64_t n_keys, int end_bit, void* base) {
+  ScatterWs w{};
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                 (int)(n_keys > 0 ? n_keys : 1), 0, end_bit);
+  const size_t kb = al256((size_t)(n_keys > 0 ? n_keys : 1) * 8);
+  uint8_t* p = (uint8_t*)base;
+  w.keys_in = (uint64_t*)p;
+  w.keys_out = (uint64_t*)(p + kb);
+  w.temp = p + 2 * kb;
+  w.temp_bytes = temp;
+  w.total = 2 * kb + al256(temp);
+  return w;
+}
+
+int scatter_slots(const nif_family_view* f) { return f->family == NIF_FAMILY_INNER ? 10 : 8; }
+
+}  // namespace
+}  // namespace nif
+
+extern "C" int nif_train_fwdbwd_ex_dev(const nif_family_view* f, const nif_train_view* t,
+                                       const int64_t* obj, const double* coord,
+                                       const float* label, const int64_t* idx,
+                                       const int64_t* cursor, int64_t n_rows, int64_t row0,
+                                       int64_t row_step, double* sq_err, float* dx_out,
+                                       float* mlp_grad, float* mlp_part, int64_t part_floats,
+                                       void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n_mlp = t->off_b - t->off_w + (int64_t)f->n_heads * f->b_stride;
+  float* dst = mlp_grad ? mlp_grad : t->grad + t->off_w;
+  TrainArgs a{*f, *t, obj, coord, label, idx, n_rows, row0, row_step, sq_err, cursor,
+              dst, mlp_part, n_mlp, dx_out, part_floats};
+  int rc = launch_fwdbwd_any(a, st);
+  if (rc != NIF_OK || mlp_part == nullptr || g_last_ctas == 0) return rc;
+  const int64_t w_end = (int64_t)f->n_heads * f->w_stride, b_begin = t->off_b - t->off_w;
+  mlp_reduce_kernel<<<(unsigned)((n_mlp + 255) / 256), 256, 0, st>>>(
+      mlp_part, (int)g_last_ctas, n_mlp, w_end, b_begin, dst);
+  return check_launch("nif_train_fwdbwd_ex_dev(reduce)");
+}
+
+extern "C" int64_t nif_train_part_floats(const nif_family_view* f, const nif_train_view* t,
+                                         int64_t n_rows) {
+  // worst case over the kernels: 16 rows per CTA (tiled), 32 (per-row floor)
+  const int64_t n_mlp = t->off_b - t->off_w + (int64_t)f->n_heads * f->b_stride;
+  return ((n_rows + 15) / 16) * n_mlp;
+}
+
+extern "C" size_t nif_grid_scatter_ws_bytes(const nif_family_view* f, const nif_train_view* t,
+                                            int64_t n_rows) {
+  const int gbits = bits_for((uint64_t)(n_rows > 1 ? n_rows - 1 : 1));
+  const int end_bit = bits_for((uint64_t)t->numel) + 2 + gbits;
+  return scatter_ws(n_rows * scatter_slots(f), end_bit, nullptr).total;
+}
+
+extern "C" int nif_grid_scatter_dev(const nif_family_view* f, const nif_train_view* t,
+                                    const int64_t* obj, const double* coord, const int64_t* idx,
+                                    const int64_t* cursor, int64_t n_rows, const float* dx,
+                                    int deterministic, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_rows <= 0) return NIF_OK;
+  if (f->N > kMaxIn || f->Nd > kMaxIn) return fail(NIF_ERR_UNSUPPORTED, "too many latents");
+  const int gbits = bits_for((uint64_t)(n_rows > 1 ? n_rows - 1 : 1));
+  const int end_bit = bits_for((uint64_t)t->numel) + 2 + gbits;
+  if (end_bit > 64) return fail(NIF_ERR_UNSUPPORTED, "sort key wider than 64 bits");
+  ScatterArgs a{*f, *t, obj, coord, idx, cursor, n_rows, dx, scatter_slots(f), gbits};
+  const int64_t n_keys = n_rows * a.slots;
+  if (!deterministic) {
+    const int64_t threads = ((n_rows + 31) / 32) * 32 * a.slots;
+    scatter_atomic_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
+    return check_launch("nif_grid_scatter_dev(atomic)");
+  }
+  ScatterWs w = scatter_ws(n_keys, end_bit, ws);
+  if (ws == nullptr || ws_bytes < w.total)
+    return fail(NIF_ERR_VALUE, "scatter workspace needs %zu bytes", w.total);
+  scatter_keys_kernel<<<(unsigned)((n_keys + 255) / 256), 256, 0, st>>>(a, w.keys_in);
+  size_t tb = w.temp_bytes;
+  if (cub::DeviceRadixSort::SortKeys(w.temp, tb, w.keys_in, w.keys_out, (int)n_keys, 0, end_bit,
+                                     st) != cudaSuccess)
+    return check_launch("nif_grid_scatter_dev(sort)");
+  scatter_segments_kernel<<<(unsigned)((n_keys + 255) / 256), 256, 0, st>>>(a, w.keys_out,
+                                                                          n_keys);
+  return check_launch("nif_grid_scatter_dev(deterministic)");
 }

@@ -4,18 +4,21 @@ Inference shards by image tile with no data-path collective: rank r owns
 a contiguous band of pixel rows, generates its own primary/shadow rays
 (the sample pass takes a pixel offset, the RNG is keyed by the global
 pixel index, so the union of the bands is exactly the single-GPU frame)
-and resolves their visibility locally. The only exchange is the final
-gather of the tile images to rank 0.
+and resolves their visibility on its own device (sample pass ->
+visibility -> shading stay in HBM). The only exchange is the final gather
+of the tile images to rank 0.
 
-Training is data parallel: see train.train (global permutation, rows
-interleaved across ranks, one all-reduce of the flat gradient buffer per
-optimiser step, identical Adam on every replica).
+Training is data parallel (reference nif.py:606-647 and
+752-795): each rank collects the samples of its own band, one ordered
+all-gather rebuilds the reference's global sample order (spp-major, then
+ray-major across the bands), every rank draws the same global permutation,
+and each optimiser step exchanges one buffer [input gradients of the batch
+rows | MLP gradients] with a single all-reduce (see train.py).
 """
 
 from __future__ import annotations
 
-import math
-from typing import Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -36,46 +39,116 @@ def tile_pixels(width: int, height: int, rank: int, world: int) -> Tuple[int, in
     return y0 * width, (y1 - y0) * width
 
 
-def render_sharded(scene, backend, spp: int, seed=None, group=None):
-    """Progressive direct-lighting render, image split in row bands across
-    ranks; returns the full linear image on rank 0 (None elsewhere)."""
+def world_rank(group=None) -> Tuple[int, int]:
+    """(world, rank) of `group` (1, 0 without torch.distributed)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def allgather_ordered(parts: Sequence, group=None) -> List:
+    """Ordered concatenation across ranks of per-segment local tensors.
+
+    ``parts[s]`` is this rank's tensor for segment s (all ranks pass the same
+    number of segments and the same trailing shape / dtype). Returns, on every
+    rank, ``[cat over ranks r of parts_r[s] for s]`` -- segment-major, rank
+    order inside a segment: the reference's spp-major, band-ordered sample
+    order when the segments are sample indices and the ranks own pixel bands
+    in order. Two collectives: the per-segment row counts, then the rows
+    (padded to the largest rank). Device-agnostic (NCCL or gloo).
+    """
     import torch
     import torch.distributed as dist
+    world, rank = world_rank(group)
+    if world == 1:
+        return list(parts)
+    ref = parts[0]
+    dev = ref.device
+    if dist.get_backend(group) == "gloo" and dev.type != "cpu":
+        # gloo gathers host tensors: stage through the host and come back
+        return [t.to(dev) for t in allgather_ordered([p.cpu() for p in parts], group)]
+    n_seg = len(parts)
+    counts = torch.tensor([int(p.shape[0]) for p in parts], dtype=torch.int64, device=dev)
+    all_counts = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(all_counts, counts, group=group)
+    cnt = torch.stack(all_counts).cpu().numpy()  # [world, n_seg]
+    tail = tuple(ref.shape[1:])
+    local = torch.cat(list(parts)) if n_seg else ref.new_zeros((0,) + tail)
+    mx = int(cnt.sum(axis=1).max())
+    pad = local.new_zeros((mx,) + tail)
+    pad[:local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    offs = np.concatenate([np.zeros((world, 1), np.int64), np.cumsum(cnt, axis=1)], axis=1)
+    out = []
+    for s in range(n_seg):
+        out.append(torch.cat([bufs[r][offs[r, s]:offs[r, s + 1]] for r in range(world)]))
+    return out
 
+
+def render_band(scene, backend, spp: int, pix0: int, n_pix: int, seed=None, camera=None,
+                sample_offset: int = 0):
+    """renderer.py:808-861 for pixels [pix0, pix0 + n_pix): the fp64 HDR sum
+    of `spp` progressive samples as a device tensor (n_pix, 3). Sample pass,
+    cast filter, visibility (``backend.occluded_dev`` when the backend has
+    it) and shading all stay on the device."""
+    import torch
+
+    from . import _lib
     from .pipeline import ShadowRays, sample_pass_dev, shadow_rays_dev
-
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    cam = scene.camera
-    pix0, n_pix = tile_pixels(cam.width, cam.height, rank, world)
+    camera = camera or scene.camera
     seed = scene.seed if seed is None else seed
     ds = scene.device()
     dev = ds.device
     buf = torch.zeros((n_pix, 3), dtype=torch.float64, device=dev)
-    inv_pi = 1.0 / math.pi
-    for s in range(spp):
-        data = sample_pass_dev(scene, cam, s, seed, "importance", pix0, n_pix)
-        cos = (data["normal"] * data["ldir"]).sum(dim=1)
+    L = _lib.lib()
+    on_device = hasattr(backend, "occluded_dev")
+    for s in range(sample_offset, sample_offset + spp):
+        data = sample_pass_dev(scene, camera, s, seed, "importance", pix0, n_pix)
         cast, o, d, t = shadow_rays_dev(data)
-        if int(cast.sum()) == 0:
+        idx = cast.nonzero().squeeze(1)
+        n_cast = int(idx.numel())
+        if n_cast == 0:
             continue
-        occ = backend.occluded(scene, ShadowRays(o.cpu().numpy(), d.cpu().numpy(),
-                                                 t.cpu().numpy()))
-        vis = torch.zeros(n_pix, dtype=torch.float64, device=dev)
-        vis[cast] = torch.from_numpy(~occ).to(dev).double()
-        obj = data["obj"].long().clamp(min=0)
-        scale = torch.where(cast, vis * cos / torch.where(cast, data["pdf"], 1.0), 0.0)
-        contrib = ds.albedo[obj] * inv_pi * data["emit"] * scale[:, None]
-        buf += torch.where(cast[:, None], contrib, 0.0)
+        if on_device:
+            occ = backend.occluded_dev(scene, o, d, t)
+        else:
+            rays = ShadowRays(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+            occ = torch.from_numpy(backend.occluded(scene, rays, 1).astype(np.uint8)).to(dev)
+        po = _lib.PassOut(**{k: _lib.ptr(v) for k, v in data.items()})
+        L.nif_shade_accumulate_dev(po, _lib.ptr(ds.albedo), _lib.ptr(idx), _lib.ptr(occ),
+                                   n_cast, _lib.ptr(buf), _lib.stream_ptr())
+    return buf
+
+
+def render_sharded(scene, backend, spp: int, seed=None, group=None, camera=None,
+                   sample_offset: int = 0) -> Optional[np.ndarray]:
+    """Progressive direct-lighting render, image split in row bands across
+    ranks; returns the full linear image (mean of the samples) on rank 0
+    and None elsewhere."""
+    camera = camera or scene.camera
+    world, rank = world_rank(group)
+    pix0, n_pix = tile_pixels(camera.width, camera.height, rank, world)
+    buf = render_band(scene, backend, spp, pix0, n_pix, seed, camera, sample_offset)
     if world == 1:
-        return (buf / spp).view(cam.height, cam.width, 3).cpu().numpy()
-    sizes = [tile_pixels(cam.width, cam.height, r, world)[1] for r in range(world)]
-    mx = max(sizes)
-    pad = torch.zeros((mx, 3), dtype=torch.float64, device=dev)
-    pad[:n_pix] = buf
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)
+        return (buf / spp).view(camera.height, camera.width, 3).cpu().numpy()
+    full = allgather_ordered([buf], group)[0]
     if rank != 0:
         return None
-    full = torch.cat([p[:sz] for p, sz in zip(parts, sizes)])
-    return (full / spp).view(cam.height, cam.width, 3).cpu().numpy()
+    return (full / spp).view(camera.height, camera.width, 3).cpu().numpy()
+
+
+def split_rows(n_rows: int, rank: int, world: int) -> Tuple[int, int]:
+    """(row0, row_step) of `rank` inside one global batch: interleaved rows
+    r, r + W, r + 2W, ... (every rank gets a share of every object group)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    return rank, world
+
+
+def rows_of(n_rows: int, rank: int, world: int) -> np.ndarray:
+    """Batch positions a rank processes (host-side mirror of split_rows)."""
+    r0, st = split_rows(n_rows, rank, world)
+    return np.arange(r0, n_rows, st, dtype=np.int64)
+

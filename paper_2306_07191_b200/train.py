@@ -10,13 +10,15 @@ fused forward/backward + grid scatter, dense Adam over touched grids + MLP)
 with no host synchronisation until the losses are read back after the last
 epoch; the host draws the next permutation while the GPU replays.
 
-Data parallel (torch.distributed over NCCL): every rank holds the same
-sample set and the same global permutation; rank r processes rows
-r, r+W, r+2W, ... of each global batch (per-object normalisation uses the
-global batch counts), the flat fp32 gradient buffer of the family plus the
-squared-error accumulator are summed with one all-reduce, and every rank
-applies the identical Adam update, so replicas stay identical without a
-broadcast.
+Data parallel (torch.distributed over NCCL): samples are collected per
+rank on its own band of pixel rows and all-gathered into the reference's
+global order, so every rank holds the same sample set and draws the same
+global permutation; rank r processes rows r, r+W, r+2W, ... of each global
+batch (per-object normalisation uses the global batch counts), one
+all-reduce per step sums the exchange buffer [input gradients of the batch
+rows | MLP gradients] (see _Sink), every rank scatters the whole batch
+into its grids and applies the identical Adam update, so replicas stay
+identical without a broadcast.
 """
 
 from __future__ import annotations
@@ -80,14 +82,21 @@ class SampleSet:
 
 def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "importance",
                     labeler=None, seed: Optional[int] = None,
-                    threads: Optional[int] = None) -> SampleSet:
+                    threads: Optional[int] = None, group=None) -> SampleSet:
     """nif.py:569-674 on the device: per sample index, the primary pass,
     every hit pixel's shadow ray (no cosine filter), the gather in the
     reference's record order and per-object BVH labels (1 = visible).
     labeler="geometry" follows the primary rays instead (uniform sampler,
     camera origin, infinite t_max) and labels each record with the closest
-    hit in its own object (unit normal, t / diagonal), keeping hit rows."""
+    hit in its own object (unit normal, t / diagonal), keeping hit rows.
+
+    Under torch.distributed (or with `group`), rank r traces only its own
+    band of pixel rows (parallel.tile_pixels) and one ordered all-gather
+    per array rebuilds the reference's global order -- sample-major, then
+    ray-major across the bands in rank order (nif.py:606-647) -- so every
+    rank ends with the single-process SampleSet."""
     torch = _torch()
+    from .parallel import allgather_ordered, tile_pixels, world_rank
     from .pipeline import gather_sized, sample_pass_dev
     camera = camera or scene.camera
     if camera is None:
@@ -103,16 +112,31 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
     ds = scene.device()
     dev = ds.device
     route = scene.nif_enabled.copy()
-    n_pix = camera.width * camera.height
-    acc = {k: [] for k in ("oo", "oc", "ol", "or_", "io", "ic", "il", "ir")}
-    n_rays = shadow_rays = degenerate = 0
+    n_pix_all = camera.width * camera.height
+    world, rank = world_rank(group)
+    pix0, n_pix = tile_pixels(camera.width, camera.height, rank, world)
+    keys = ("oo", "oc", "ol", "or_", "io", "ic", "il", "ir")
+    lt = () if head == "occlusion" else (4,)
+    tails = {"oo": ((), torch.int64), "oc": ((4,), torch.float64), "ol": (lt, torch.float32),
+             "or_": ((), torch.int64), "io": ((), torch.int64), "ic": ((5,), torch.float64),
+             "il": (lt, torch.float32), "ir": ((), torch.int64)}
+    # one (possibly empty) tensor per sample index and array: the segments of
+    # the ordered all-gather
+    acc = {k: [] for k in keys}
+    stat = torch.zeros(3, dtype=torch.int64)  # rays, shadow rays, degenerate queries
     L = _lib.lib()
     cam_pos = torch.from_numpy(np.ascontiguousarray(
         np.broadcast_to(np.asarray(camera.position, np.float64), (n_pix, 3)))).to(dev)
     inf_tmax = torch.full((n_pix,), math.inf, dtype=torch.float64, device=dev)
+
+    def empty(k):
+        tail, dt = tails[k]
+        return torch.zeros((0,) + tail, dtype=dt, device=dev)
+
     for s in range(spp):
+        got = {}
         data = sample_pass_dev(scene, camera, s, seed,
-                               "uniform" if head == "geometry" else sampler)
+                               "uniform" if head == "geometry" else sampler, pix0, n_pix)
         if head == "geometry":
             idx = torch.arange(n_pix, device=dev)
             n = n_pix
@@ -121,61 +145,64 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
             mask = data["hit"] != 0
             idx = mask.nonzero().squeeze(1)
             n = int(idx.numel())
-            if n == 0:
-                continue
             o = data["point"][idx].contiguous()
             d = data["ldir"][idx].contiguous()
             t = data["tmax"][idx].contiguous()
-        buf, counts = gather_sized(ds, ds.route(route), o, d, t, n, int(route.sum()), dev)
-        m = int(counts[2])
-        shadow_rays += n
-        degenerate += int(counts[3])
-        if m == 0:
-            continue
-        rec_obj = buf.rec_obj[:m]
-        rec_ray = buf.rec_ray[:m]
-        if head == "geometry":
-            lab = torch.empty((m, 4), dtype=torch.float32, device=dev)
-            keep = torch.empty(m, dtype=torch.uint8, device=dev)
-            L.nif_label_geometry_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m,
-                                     _lib.ptr(o), _lib.ptr(d), float(scene.diagonal),
-                                     _lib.ptr(lab), _lib.ptr(keep), _lib.stream_ptr())
-            keep = keep != 0
-        else:
-            vis = torch.empty(m, dtype=torch.uint8, device=dev)
-            L.nif_label_visible_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m,
-                                    _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), _lib.ptr(vis),
-                                    _lib.stream_ptr())
-            lab, keep = vis.float(), None
-        kind = buf.rec_kind[:m]
-        coord = buf.rec_coord[:m * 5].view(m, 5)
-        ray_ids = s * n_pix + idx
-        for k, (ko, kc, kl, kr), width in ((0, ("oo", "oc", "ol", "or_"), 4),
-                                           (1, ("io", "ic", "il", "ir"), 5)):
-            selm = kind == k
-            if keep is not None:
-                selm &= keep
-            sel = selm.nonzero().squeeze(1)
-            if sel.numel() == 0:
-                continue
-            acc[ko].append(rec_obj[sel].long())
-            acc[kc].append(coord[sel, :width].contiguous())
-            acc[kl].append(lab[sel])
-            acc[kr].append(ray_ids[rec_ray[sel].long()])
-        n_rays += n
+        m = 0
+        if n:
+            buf, counts = gather_sized(ds, ds.route(route), o, d, t, n, int(route.sum()), dev)
+            m = int(counts[2])
+            stat[1] += n
+            stat[2] += int(counts[3])
+        if m:
+            stat[0] += n
+            rec_obj = buf.rec_obj[:m]
+            rec_ray = buf.rec_ray[:m]
+            if head == "geometry":
+                lab = torch.empty((m, 4), dtype=torch.float32, device=dev)
+                keep = torch.empty(m, dtype=torch.uint8, device=dev)
+                L.nif_label_geometry_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m,
+                                         _lib.ptr(o), _lib.ptr(d), float(scene.diagonal),
+                                         _lib.ptr(lab), _lib.ptr(keep), _lib.stream_ptr())
+                keep = keep != 0
+            else:
+                vis = torch.empty(m, dtype=torch.uint8, device=dev)
+                L.nif_label_visible_dev(ds.view, _lib.ptr(rec_obj), _lib.ptr(rec_ray), m,
+                                        _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), _lib.ptr(vis),
+                                        _lib.stream_ptr())
+                lab, keep = vis.float(), None
+            kind = buf.rec_kind[:m]
+            coord = buf.rec_coord[:m * 5].view(m, 5)
+            # global ray id: sample-major over the whole image (nif.py:640)
+            ray_ids = s * n_pix_all + pix0 + idx
+            for k, (ko, kc, kl, kr), width in ((0, ("oo", "oc", "ol", "or_"), 4),
+                                               (1, ("io", "ic", "il", "ir"), 5)):
+                selm = kind == k
+                if keep is not None:
+                    selm &= keep
+                sel = selm.nonzero().squeeze(1)
+                got[ko] = rec_obj[sel].long()
+                got[kc] = coord[sel, :width].contiguous()
+                got[kl] = lab[sel]
+                got[kr] = ray_ids[rec_ray[sel].long()]
+        for k in keys:
+            acc[k].append(got.get(k, empty(k)))
 
-    def cat(key, tail, dt):
-        if acc[key]:
-            return torch.cat(acc[key]).contiguous()
-        return torch.zeros((0,) + tail, dtype=dt, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        st = stat.to(dev)
+        dist.all_reduce(st, group=group)
+        stat = st.cpu()
+        for k in keys:
+            acc[k] = allgather_ordered(acc[k], group)
 
-    lt = () if head == "occlusion" else (4,)
-    out = SampleSet(head, cat("oo", (), torch.int64), cat("oc", (4,), torch.float64),
-                    cat("ol", lt, torch.float32), cat("or_", (), torch.int64),
-                    cat("io", (), torch.int64), cat("ic", (5,), torch.float64),
-                    cat("il", lt, torch.float32), cat("ir", (), torch.int64), n_rays=n_rays)
-    out.stats = {"pixel_samples": spp * n_pix, "shadow_rays": shadow_rays,
-                 "degenerate_queries": degenerate,
+    def cat(k):
+        parts = [a for a in acc[k] if a.shape[0]]
+        return torch.cat(parts).contiguous() if parts else empty(k)
+
+    out = SampleSet(head, *(cat(k) for k in keys), n_rays=int(stat[0]))
+    out.stats = {"pixel_samples": spp * n_pix_all, "shadow_rays": int(stat[1]),
+                 "degenerate_queries": int(stat[2]),
                  "outer_per_object": np.bincount(out.outer_obj.cpu().numpy(),
                                                  minlength=scene.n_objects),
                  "inner_per_object": np.bincount(out.inner_obj.cpu().numpy(),
@@ -198,35 +225,91 @@ class _Step:
         self.fv = self.fam.view()
         self.tv = self.fam.train_view()
 
-    def run(self, obj, coord, label, idx, n_rows, rank=0, world=1, group=None, stream=None,
-            idx_ptr=None):
+    def run(self, obj, coord, label, idx, n_rows, stream=None, idx_ptr=None):
         """One optimiser step over rows idx[0:n_rows] (device tensors; or a raw
         device pointer idx_ptr into an int64 row list); leaves this batch's
-        squared-error sum added into self.sq."""
-        torch = _torch()
+        squared-error sum added into self.sq. (Data-parallel steps go
+        through _Sink.)"""
         L = _lib.lib()
         fam, model = self.fam, self.model
         sp = _lib.stream_ptr(stream)
         fv, tv = self.fv, self.tv
         p = _lib.ptr
-        if idx_ptr is not None:
-            idx = None
         ip = idx_ptr if idx_ptr is not None else p(idx)
         L.nif_batch_counts_dev(p(obj), ip, n_rows, fam.n_obj, p(fam.counts), sp)
-        if world > 1:
-            sq_local = torch.zeros(1, dtype=torch.float64, device=model.device)
-            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), ip, n_rows, rank,
-                                   world, p(sq_local), sp)
-            import torch.distributed as dist
-            dist.all_reduce(fam.grad, group=group)
-            dist.all_reduce(sq_local, group=group)
-            self.sq += sq_local
-        else:
-            L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), ip, n_rows, 0, 1,
-                                   p(self.sq), sp)
+        L.nif_train_fwdbwd_dev(fv, tv, p(obj), p(coord), p(label), ip, n_rows, 0, 1,
+                               p(self.sq), sp)
         a = model.config.adam
         L.nif_adam_dev(fv, tv, model.learning_rate, a.beta1, a.beta2, a.epsilon, sp)
         fam.dirty = True
+
+
+class _Sink:
+    """Gradient routing of one family's step when the grid scatter is not
+    fused into the forward/backward kernel: data parallel and / or
+    deterministic.
+
+    One flat fp32 exchange buffer per family, ``comm = [dx | mlp]``:
+    ``dx[g, k]`` is the input gradient of global batch row g (written only by
+    the rank that owns row g, zero elsewhere) and ``mlp`` the MLP gradients
+    in the family's [w | pad | b] layout. Per optimiser step: zero comm,
+    fused forward/backward of this rank's rows into it, ONE all-reduce
+    (sum) of comm, then on every rank the grid scatter of *all* batch rows
+    from dx (grids.py:171-202; identical on every rank, deterministic mode
+    sums each cell in np.add.at's order) and the MLP gradients copied into
+    the family buffer, then the same dense Adam everywhere -- replicas stay
+    identical without a broadcast. Exchanged per step: bs x IN + n_mlp
+    floats (outer 2^11 x 6 + 4,673; inner 2^12 x 13 + 5,425), independent
+    of how many objects the batch touches, against 1.6 MB / 0.7 MB per
+    touched object for a dense grid-gradient all-reduce."""
+
+    def __init__(self, step: "_Step", bs: int, world: int, rank: int, group, deterministic: bool):
+        torch = _torch()
+        L = _lib.lib()
+        fam = step.fam
+        dev = step.model.device
+        self.step, self.bs, self.world, self.rank, self.group = step, bs, world, rank, group
+        self.det = bool(deterministic)
+        # Every rank scatters the whole batch into its own replica: the sorted
+        # (order-fixed) scatter keeps the replicas bit-identical, where fp32
+        # atomics would let them drift apart in the last bits
+        self.det_scatter = self.det or group is not None
+        self.IN = int(fam.dims[0])
+        self.dx_len = (bs * self.IN + 63) // 64 * 64
+        off_w = fam.offsets["w"][0]
+        off_b, size_b = fam.offsets["b"]
+        self.n_mlp = off_b - off_w + size_b
+        self.comm = torch.zeros(self.dx_len + self.n_mlp, dtype=torch.float32, device=dev)
+        self.dx = self.comm[:self.dx_len]
+        self.mlp = self.comm[self.dx_len:]
+        self.grad_mlp = fam.grad[off_w:off_w + self.n_mlp]
+        self.part = self.ws = None
+        self.part_n = 0
+        if self.det_scatter:
+            nb = int(L.nif_grid_scatter_ws_bytes(step.fv, step.tv, bs))
+            self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        if self.det:
+            self.part_n = int(L.nif_train_part_floats(step.fv, step.tv, bs))
+            self.part = torch.empty(max(self.part_n, 1), dtype=torch.float32, device=dev)
+
+    def enqueue(self, obj, coord, label, idx_ptr, cursor_ptr, n_rows, sq_ptr, sp):
+        """Everything from the batch counts to the gradients, stream-ordered
+        on the current stream (capturable: no host synchronisation)."""
+        L = _lib.lib()
+        st = self.step
+        p = _lib.ptr
+        self.comm.zero_()
+        L.nif_train_prologue_cur_dev(st.fv, st.tv, p(obj), idx_ptr, cursor_ptr, n_rows, sp)
+        L.nif_train_fwdbwd_ex_dev(st.fv, st.tv, p(obj), p(coord), p(label), idx_ptr, cursor_ptr,
+                                  n_rows, self.rank, self.world, sq_ptr, p(self.dx),
+                                  p(self.mlp), p(self.part), self.part_n, sp)
+        if self.group is not None:  # one collective per step
+            import torch.distributed as dist
+            dist.all_reduce(self.comm, group=self.group)
+        L.nif_grid_scatter_dev(st.fv, st.tv, p(obj), p(coord), idx_ptr, cursor_ptr, n_rows,
+                               p(self.dx), int(self.det_scatter), p(self.ws),
+                               0 if self.ws is None else int(self.ws.numel()), sp)
+        self.grad_mlp.copy_(self.mlp)
 
 
 class _GraphStep:
@@ -236,11 +319,19 @@ class _GraphStep:
     itself), so an epoch is one async H2D copy of the permutation (from a
     pinned staging buffer) plus one graph launch per batch -- no per-step
     host work and no host synchronisation: the host is free to draw the
-    next permutation while the GPU replays this one."""
+    next permutation while the GPU replays this one.
 
-    def __init__(self, step: "_Step", obj, coord, label, n: int, bs: int):
+    With a _Sink (data parallel / deterministic) the captured step also
+    holds the exchange buffer's all-reduce (NCCL collectives are capturable;
+    each family has its own communicator so the two families' graphs can
+    replay concurrently). capture=False runs the same launches eagerly per
+    batch (gloo, which cannot be captured)."""
+
+    def __init__(self, step: "_Step", obj, coord, label, n: int, bs: int, sink=None,
+                 capture: bool = True):
         torch = _torch()
         self.step, self.bs = step, bs
+        self.sink, self.capture = sink, capture
         dev = step.model.device
         self.perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         self.cursor = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -257,13 +348,17 @@ class _GraphStep:
         st, fam, model = self.step, self.step.fam, self.step.model
         p = _lib.ptr
         sp = _lib.stream_ptr()
-        # three launches: counts + step counters, fused fwd/bwd, dense Adam
-        # (which also moves the cursor on)
-        L.nif_train_prologue_cur_dev(st.fv, st.tv, p(self.obj), p(self.perm), p(self.cursor),
-                                     n_rows, sp)
-        L.nif_train_fwdbwd_cur_dev(st.fv, st.tv, p(self.obj), p(self.coord), p(self.label),
-                                   p(self.perm), p(self.cursor), n_rows, 0, 1, p(st.sq), sp)
         a = model.config.adam
+        if self.sink is not None:
+            self.sink.enqueue(self.obj, self.coord, self.label, p(self.perm), p(self.cursor),
+                              n_rows, p(st.sq), sp)
+        else:
+            # three launches: counts + step counters, fused fwd/bwd, dense Adam
+            # (which also moves the cursor on)
+            L.nif_train_prologue_cur_dev(st.fv, st.tv, p(self.obj), p(self.perm),
+                                         p(self.cursor), n_rows, sp)
+            L.nif_train_fwdbwd_cur_dev(st.fv, st.tv, p(self.obj), p(self.coord), p(self.label),
+                                       p(self.perm), p(self.cursor), n_rows, 0, 1, p(st.sq), sp)
         L.nif_adam_units_dev(st.fv, st.tv, model.learning_rate, a.beta1, a.beta2, a.epsilon,
                              p(self.cursor) if advance else None, n_rows, sp)
 
@@ -283,7 +378,7 @@ class _GraphStep:
         self.copied[k] = ev
         self.cursor.zero_()
         n_full = n // self.bs
-        if n_full and self.graph is None:
+        if n_full and self.capture and self.graph is None:
             s = torch.cuda.Stream(device=self.perm.device)
             s.wait_stream(torch.cuda.current_stream())
             g = torch.cuda.CUDAGraph()
@@ -296,7 +391,10 @@ class _GraphStep:
             torch.cuda.current_stream().wait_stream(s)
             self.graph = g
         for _ in range(n_full):
-            self.graph.replay()
+            if self.capture:
+                self.graph.replay()
+            else:
+                self._enqueue(self.bs, True)
         if n - n_full * self.bs:
             self._enqueue(n - n_full * self.bs, False)
         # the prologue overwrites counts; leave them zero for the
@@ -330,11 +428,18 @@ _train_batch = train_batch
 
 
 def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional[int] = None,
-          group=None) -> np.ndarray:
+          group=None, deterministic: bool = False) -> np.ndarray:
     """nif.py:752-795: shuffled mini-batch epochs over both families; loss
     curve (epochs, 3) = outer, inner, combined (NaN for an empty family).
-    With torch.distributed initialised (or `group` given) the batches are
-    split across ranks and gradients all-reduced once per step."""
+
+    With torch.distributed initialised (or `group` given) every rank holds
+    the same samples and draws the same global permutation; rank r takes
+    rows r, r+W, ... of each global batch (per-object loss scale from the
+    global batch counts) and the step exchanges one buffer [batch input
+    gradients | MLP gradients] with a single all-reduce (_Sink), captured
+    in the step's CUDA graph under NCCL. deterministic=True makes the
+    gradients bit-reproducible run to run: grid cells summed in np.add.at's
+    order after a sort, MLP gradients reduced over CTAs in order."""
     torch = _torch()
     if isinstance(samples, dict):
         samples = SampleSet.from_host(samples, device=model.device)
@@ -348,16 +453,26 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     curve = np.zeros((epochs, 3))
     if epochs == 0:
         return curve
-    world, rank = 1, 0
+    from .parallel import world_rank
+    world, rank = world_rank(group)
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized():
-        world, rank = dist.get_world_size(group), dist.get_rank(group)
     epoch_ss = np.random.SeedSequence([seed, 0x7472]).spawn(epochs)
     bo = model.config.outer.batch_size
     bi = model.config.inner.batch_size
     steps = {"outer": _Step(model, "outer"), "inner": _Step(model, "inner")}
-    # single GPU: every full batch is a replay of one captured step
-    use_graph = world == 1 and model.device.type == "cuda"
+    on_gpu = model.device.type == "cuda"
+    # every full batch is a replay of one captured step: always on one GPU,
+    # under NCCL with the all-reduce inside the graph; gloo runs eagerly
+    capture = on_gpu and (world == 1 or (dist.get_backend(group) == "nccl"
+                                         and os.environ.get("NIF_DP_GRAPH", "1") != "0"))
+    use_sink = world > 1 or deterministic
+    fam_groups = {}
+    if world > 1:
+        # one communicator per family: the two families' steps (and their
+        # collectives) run on separate streams, concurrently
+        ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
+        for which in ("outer", "inner"):
+            fam_groups[which] = dist.new_group(ranks, backend=dist.get_backend(group))
     gsteps = {}
     fams = ((0, bo, "outer", samples.outer_obj, samples.outer_coord, samples.outer_label),
             (1, bi, "inner", samples.inner_obj, samples.inner_coord, samples.inner_label))
@@ -392,12 +507,11 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     pool = ThreadPoolExecutor(max_workers=depth)
     ahead = deque(pool.submit(epoch_perms, k) for k in range(min(depth, epochs)))
     # The two families are independent optimisers (disjoint parameters,
-    # counts and step counters), so on one GPU each runs its own sequence of
-    # steps -- in the reference's order within the family -- on its own
-    # stream, and the latency-bound steps of one overlap the other's.
-    import contextlib
+    # counts and step counters), so each runs its own sequence of steps --
+    # in the reference's order within the family -- on its own stream, and
+    # the latency-bound steps of one overlap the other's.
     fam_streams = {}
-    if use_graph:
+    if on_gpu:
         cur = torch.cuda.current_stream(model.device)
         for which in ("outer", "inner"):
             fam_streams[which] = torch.cuda.Stream(device=model.device)
@@ -410,22 +524,19 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
             n = int(obj.shape[0])
             if n == 0:
                 continue
-            perm_np = perms[fam]
             st = steps[which]
-            ctx = torch.cuda.stream(fam_streams[which]) if use_graph else contextlib.nullcontext()
-            with ctx:
+            with torch.cuda.stream(fam_streams[which]):
                 st.sq.zero_()
-                if use_graph:
-                    if which not in gsteps:
-                        gsteps[which] = _GraphStep(st, obj, coord, label, n, bs)
-                    gsteps[which].epoch(perm_np)
-                else:
-                    perm = torch.from_numpy(perm_np).to(model.device)
-                    base = perm.data_ptr()
-                    for k in range(0, n, bs):
-                        m = min(bs, n - k)
-                        st.run(obj, coord, label, None, m, rank, world, group,
-                               idx_ptr=base + 8 * k)
+                if which not in gsteps:
+                    sink = None
+                    if use_sink:
+                        sink = _Sink(st, bs, world, rank, fam_groups.get(which), deterministic)
+                        if world > 1:  # communicator set up outside any capture
+                            dist.all_reduce(sink.comm, group=fam_groups[which])
+                    gsteps[which] = _GraphStep(st, obj, coord, label, n, bs, sink, capture)
+                gsteps[which].epoch(perms[fam])
+                if world > 1:  # each rank summed the squared errors of its own rows
+                    dist.all_reduce(st.sq, group=fam_groups[which])
                 # the reference's per-batch loss is the mean over rows x outputs
                 width = int(label.shape[1]) if label.dim() > 1 else 1
                 sq[e, fam].copy_(st.sq[0] / width)

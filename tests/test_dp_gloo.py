@@ -123,3 +123,48 @@ def test_dp_gradient_allreduce_equals_full_batch(which, golden, scenes):
         assert p.exitcode == 0
     scale = np.abs(ref).max()
     np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-6 * scale)
+
+
+def _gather_worker(rank, world, port, q):
+    from paper_2306_07191_b200.parallel import allgather_ordered
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # segment s of rank r: (s, r, j) rows; rank 1 has an empty segment 1,
+    # segment lengths differ per rank
+    parts = []
+    for s in range(3):
+        n = 0 if (rank == 1 and s == 1) else 2 + s + 3 * rank
+        parts.append(torch.tensor([[s, rank, j] for j in range(n)], dtype=torch.int64)
+                     .reshape(n, 3))
+    out = allgather_ordered(parts)
+    q.put((rank, [o.numpy() for o in out]))
+    dist.destroy_process_group()
+
+
+def test_allgather_ordered_is_segment_major_rank_ordered():
+    """parallel.allgather_ordered (the package's sample-merging collective):
+    every rank receives segment-major, rank-ordered rows -- the reference's
+    spp-major, band-ordered sample order (nif.py:606-647)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = []
+    for s in range(3):
+        rows = []
+        for r in range(world):
+            n = 0 if (r == 1 and s == 1) else 2 + s + 3 * r
+            rows += [[s, r, j] for j in range(n)]
+        expect.append(np.array(rows, np.int64).reshape(-1, 3))
+    for _, out in got:
+        assert len(out) == 3
+        for a, b in zip(out, expect):
+            np.testing.assert_array_equal(a, b)

@@ -1,0 +1,323 @@
+"""Data-parallel training, deterministic gradients and tile-sharded
+rendering on the device (reference nif.py:606-647,
+682-795, grids.py:171-202, renderer.py:808-861).
+
+* The split step (fwd/bwd into the exchange buffer, then the batch-wide
+  grid scatter) gives the fused step's gradients; rows split over two
+  "ranks" (row0 = r, row_step = 2) into one buffer give the full batch's.
+* Deterministic mode: grid gradients equal the oracle's np.add.at
+  restatement fed the kernel's own input gradients BIT FOR BIT, and two
+  runs are bit-identical (MLP gradients too).
+* Two processes (gloo, both on cuda:0) run the package's own
+  collect_samples / train under torch.distributed: the band-sharded
+  samples equal the single-process samples bit for bit, both replicas end
+  bit-identical, and the loss curve / parameters match the single-process
+  run within the training tolerances of test_gpu_train.py.
+* The union of rendered row bands is the single-GPU frame bit for bit.
+* A world-size-1 NCCL group exercises the all-reduce captured inside the
+  step's CUDA graph.
+"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _model(name, scenes, seed=0):
+    from golden_cfg import small_config
+    from paper_2306_07191_b200 import build_model
+    return build_model(small_config(seed), scenes(name))
+
+
+def _batch(golden, name, which, n_max):
+    import torch
+    g = golden(name)
+    obj = g[f"samples_{which}_obj"][:n_max].astype(np.int64)
+    coord = g[f"samples_{which}_coord"][:n_max]
+    label = g[f"samples_{which}_label"][:n_max].astype(np.float32)
+    dev = torch.device("cuda", 0)
+    return (obj, coord, label, torch.from_numpy(obj).to(dev),
+            torch.from_numpy(np.ascontiguousarray(coord)).to(dev),
+            torch.from_numpy(label).to(dev))
+
+
+def _grad(model, which):
+    return model.family(which).grad.detach().cpu().numpy().copy()
+
+
+def _fused_grad(model, which, t_obj, t_coord, t_lab):
+    import torch
+    from paper_2306_07191_b200 import _lib
+    fam = model.family(which)
+    L, p, sp = _lib.lib(), _lib.ptr, _lib.stream_ptr()
+    n = int(t_obj.numel())
+    fam.grad.zero_()
+    fam.counts.zero_()
+    sq = torch.zeros(1, dtype=torch.float64, device=model.device)
+    L.nif_batch_counts_dev(p(t_obj), None, n, fam.n_obj, p(fam.counts), sp)
+    L.nif_train_fwdbwd_dev(fam.view(), fam.train_view(), p(t_obj), p(t_coord), p(t_lab), None,
+                           n, 0, 1, p(sq), sp)
+    return _grad(model, which), float(sq.item())
+
+
+def _split_grad(model, which, t_obj, t_coord, t_lab, world=1, det=False):
+    """The _Sink route by hand: every "rank" writes its rows of dx and adds
+    its MLP partial sums into one exchange buffer (what the all-reduce
+    would produce), then the whole batch is scattered."""
+    import torch
+    from paper_2306_07191_b200 import _lib
+    fam = model.family(which)
+    fv, tv = fam.view(), fam.train_view()
+    L, p, sp = _lib.lib(), _lib.ptr, _lib.stream_ptr()
+    n = int(t_obj.numel())
+    IN = fam.dims[0]
+    fam.grad.zero_()
+    fam.counts.zero_()
+    L.nif_batch_counts_dev(p(t_obj), None, n, fam.n_obj, p(fam.counts), sp)
+    off_w = fam.offsets["w"][0]
+    off_b, size_b = fam.offsets["b"]
+    n_mlp = off_b - off_w + size_b
+    dx = torch.zeros(n * IN, dtype=torch.float32, device=model.device)
+    mlp = torch.zeros(n_mlp, dtype=torch.float32, device=model.device)
+    sq = torch.zeros(1, dtype=torch.float64, device=model.device)
+    part_n = int(L.nif_train_part_floats(fv, tv, n)) if det else 0
+    part = torch.empty(max(part_n, 1), dtype=torch.float32, device=model.device) if det else None
+    for r in range(world):
+        L.nif_train_fwdbwd_ex_dev(fv, tv, p(t_obj), p(t_coord), p(t_lab), None, None, n, r, world,
+                                  p(sq), p(dx), p(mlp), p(part), part_n, sp)
+    nb = int(L.nif_grid_scatter_ws_bytes(fv, tv, n))
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=model.device)
+    L.nif_grid_scatter_dev(fv, tv, p(t_obj), p(t_coord), None, None, n, p(dx), int(det), p(ws),
+                           nb, sp)
+    fam.grad[off_w:off_w + n_mlp].copy_(mlp)
+    return _grad(model, which), float(sq.item()), dx.view(n, IN).cpu().numpy()
+
+
+def _assert_close(got, ref, rel=1e-5):
+    scale = max(float(np.abs(ref).max()), 1e-30)
+    np.testing.assert_allclose(got, ref, rtol=rel, atol=rel * scale)
+
+
+@pytest.mark.parametrize("name", ["c1s", "overlap"])
+@pytest.mark.parametrize("which", ["outer", "inner"])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_split_step_matches_fused(name, which, world, cuda, golden, scenes):
+    n_max = 256 if which == "outer" else 512
+    _, _, _, t_obj, t_coord, t_lab = _batch(golden, name, which, n_max)
+    m = _model(name, scenes)
+    ref, ref_sq = _fused_grad(m, which, t_obj, t_coord, t_lab)
+    got, sq, _ = _split_grad(m, which, t_obj, t_coord, t_lab, world=world)
+    assert sq == pytest.approx(ref_sq, rel=1e-12)
+    _assert_close(got, ref)
+
+
+@pytest.mark.parametrize("name", ["c1s", "overlap"])
+@pytest.mark.parametrize("which", ["outer", "inner"])
+def test_deterministic_scatter_is_np_add_at(name, which, cuda, golden, scenes):
+    """The sorted scatter adds each cell's contributions in np.add.at's
+    order (object groups of the stable argsort, corners 00/01/10/11 or
+    i0/i1, rows in batch order): fed the kernel's own input gradients, the
+    oracle's grids.py restatement gives identical bits."""
+    from oracle import oracle
+    n_max = 256 if which == "outer" else 512
+    obj, coord, _, t_obj, t_coord, t_lab = _batch(golden, name, which, n_max)
+    m = _model(name, scenes)
+    got, _, dx = _split_grad(m, which, t_obj, t_coord, t_lab, det=True)
+    fam = m.family(which)
+    R, N = fam.R, fam.N
+    order = np.argsort(obj, kind="stable")
+    bounds = np.flatnonzero(np.diff(obj[order])) + 1
+    ref = np.zeros_like(got)
+    for grp in np.split(order, bounds):
+        if len(grp) == 0:
+            continue
+        o = int(obj[grp[0]])
+        gp = oracle.OGrid(np.zeros((R, R, N), np.float32))
+        gd = oracle.OGrid(np.zeros((R, R, N), np.float32))
+        oracle.grad_2d(gp, coord[grp, 0:2], dx[grp, :N])
+        oracle.grad_2d(gd, coord[grp, 2:4], dx[grp, N:2 * N])
+        for key, gg in (("pos", gp), ("dir", gd)):
+            off = fam.offsets[key][0] + o * R * R * N
+            ref[off:off + R * R * N] = gg.grad.reshape(-1)
+        if which == "inner":
+            Rd, Nd = fam.Rd, fam.Nd
+            gr = oracle.OGrid(np.zeros((Rd, Nd), np.float32), wrap_u=False)
+            oracle.grad_1d(gr, coord[grp, 4], dx[grp, 2 * N:])
+            off = fam.offsets["dist"][0] + o * Rd * Nd
+            ref[off:off + Rd * Nd] = gr.grad.reshape(-1)
+    grid_end = fam.offsets["w"][0]
+    assert np.array_equal(got[:grid_end].view(np.uint32), ref[:grid_end].view(np.uint32))
+
+
+@pytest.mark.parametrize("which", ["outer", "inner"])
+def test_deterministic_mode_is_bit_reproducible(which, cuda, golden, scenes):
+    n_max = 256 if which == "outer" else 512
+    _, _, _, t_obj, t_coord, t_lab = _batch(golden, "overlap", which, n_max)
+    m = _model("overlap", scenes)
+    a, _, _ = _split_grad(m, which, t_obj, t_coord, t_lab, world=2, det=True)
+    b, _, _ = _split_grad(m, which, t_obj, t_coord, t_lab, world=2, det=True)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    ref, _ = _fused_grad(m, which, t_obj, t_coord, t_lab)
+    _assert_close(a, ref)
+
+
+def test_warp_aggregated_scatter_hot_cells(cuda, scenes):
+    """Many rows on few cells (the aggregation path: whole warps on one
+    cell) against the float64 sum."""
+    import torch
+    from paper_2306_07191_b200 import _lib
+    m = _model("c1s", scenes)
+    fam = m.family("outer")
+    fv, tv = fam.view(), fam.train_view()
+    L, p, sp = _lib.lib(), _lib.ptr, _lib.stream_ptr()
+    rng = np.random.default_rng(3)
+    n = 4096
+    obj = np.zeros(n, np.int64)
+    coord = np.repeat(rng.random((4, 4)), n // 4, axis=0)  # 4 distinct coordinates
+    dx = rng.standard_normal((n, fam.dims[0])).astype(np.float32)
+    dev = m.device
+    t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+         for k, v in (("obj", obj), ("coord", coord), ("dx", dx))}
+    fam.grad.zero_()
+    L.nif_grid_scatter_dev(fv, tv, p(t["obj"]), p(t["coord"]), None, None, n, p(t["dx"]), 0,
+                           None, 0, sp)
+    got = _grad(m, "outer")
+    fam.grad.zero_()
+    nb = int(L.nif_grid_scatter_ws_bytes(fv, tv, n))
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    L.nif_grid_scatter_dev(fv, tv, p(t["obj"]), p(t["coord"]), None, None, n, p(t["dx"]), 1,
+                           p(ws), nb, sp)
+    det = _grad(m, "outer")
+    _assert_close(got, det, rel=1e-4)
+    assert np.count_nonzero(det) > 0
+
+
+def test_render_bands_union_is_single_gpu_frame(cuda, scenes):
+    import torch
+    from paper_2306_07191_b200 import BvhBackend, NifBackend
+    from paper_2306_07191_b200.parallel import render_band, tile_pixels
+    from paper_2306_07191_b200.pipeline import render_dev
+    s = scenes("overlap")
+    cam = s.camera
+    for backend in (BvhBackend(), NifBackend(_model("overlap", scenes))):
+        full = render_dev(s, backend, spp=2).reshape(-1, 3)
+        for world in (2, 3):
+            parts = []
+            for r in range(world):
+                pix0, n_pix = tile_pixels(cam.width, cam.height, r, world)
+                parts.append(render_band(s, backend, 2, pix0, n_pix))
+            got = torch.cat(parts)
+            assert torch.equal(got, full), (type(backend).__name__, world)
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _dp_worker(rank, world, port, out, det):
+    import torch
+    import torch.distributed as dist
+    from golden_cfg import small_config
+    from scenes import RECIPES, build_scene
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.train import collect_samples, train
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = build_scene(RECIPES["overlap"])
+        smp = collect_samples(s, spp=2, seed=s.seed)
+        m = build_model(small_config(), s)
+        curve = train(m, smp, epochs=2, deterministic=det)
+        arrays = {f"a{i:03d}": a for i, a in enumerate(m.model_arrays())}
+        np.savez(os.path.join(out, f"rank{rank}.npz"), curve=curve,
+                 **{"s_" + k: v for k, v in smp.host().items()}, **arrays)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("det", [False, True])
+def test_dp_two_ranks_gloo_package_code(det, cuda, golden, scenes):
+    import torch.multiprocessing as mp
+    from paper_2306_07191_b200.train import collect_samples, train
+    world = 2
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_dp_worker, args=(world, _free_port(), out, det), nprocs=world,
+                           join=True, start_method="spawn")
+        res = [dict(np.load(os.path.join(out, f"rank{r}.npz"))) for r in range(world)]
+    s = scenes("overlap")
+    smp = collect_samples(s, spp=2, seed=s.seed)
+    ref_s = smp.host()
+    g = golden("overlap")
+    for k, v in ref_s.items():  # band-sharded collection == single process == reference
+        for r in range(world):
+            np.testing.assert_array_equal(res[r]["s_" + k], v, err_msg=k)
+        if k.endswith(("obj", "label", "ray")):
+            np.testing.assert_array_equal(v, g["samples_" + k], err_msg=k)
+    arrays = [k for k in res[0] if k.startswith("a")]
+    for k in arrays:  # replicas identical without a broadcast
+        assert np.array_equal(res[0][k], res[1][k]), k
+    m = _model("overlap", scenes)
+    curve = train(m, smp, epochs=2, deterministic=det)
+    np.testing.assert_allclose(res[0]["curve"], curve, rtol=1e-4)
+    ref_arrays = m.model_arrays()
+    close = total = 0
+    for i, ref in enumerate(ref_arrays):
+        got = res[0][f"a{i:03d}"]
+        close += int(np.sum(np.abs(got - ref) <= 1e-5))
+        total += ref.size
+    assert close / total >= 0.995, close / total
+
+
+def _nccl_worker(rank, port, out):
+    import torch
+    import torch.distributed as dist
+    from golden_cfg import small_config
+    from scenes import RECIPES, build_scene
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.train import _GraphStep, _Sink, _Step, collect_samples
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        s = build_scene(RECIPES["c1s"])
+        smp = collect_samples(s, spp=2, seed=s.seed)
+        res = {}
+        for mode in ("graph", "eager"):
+            m = build_model(small_config(), s)
+            st = _Step(m, "inner")
+            grp = dist.new_group([0])
+            sink = _Sink(st, 512, 1, 0, grp, deterministic=True)
+            dist.all_reduce(sink.comm, group=grp)
+            gs = _GraphStep(st, smp.inner_obj, smp.inner_coord, smp.inner_label, smp.n_inner, 512,
+                            sink, capture=mode == "graph")
+            perm = np.random.default_rng(5).permutation(smp.n_inner)
+            gs.epoch(perm)
+            gs.epoch(perm[::-1].copy())
+            torch.cuda.synchronize()
+            res[mode] = m.family("inner").params.cpu().numpy()
+            res[mode + "_sq"] = st.sq.cpu().numpy()
+        np.savez(os.path.join(out, "nccl.npz"), **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_all_reduce_captured_in_step_graph(cuda):
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_nccl_worker, args=(_free_port(), out), nprocs=1, join=True,
+                           start_method="spawn")
+        r = dict(np.load(os.path.join(out, "nccl.npz")))
+    # deterministic step: the replayed graph and the eager launches agree bit for bit
+    assert np.array_equal(r["graph"].view(np.uint32), r["eager"].view(np.uint32))
+    # (the loss sum is an fp64 atomic accumulation: equal to rounding)
+    np.testing.assert_allclose(r["graph_sq"], r["eager_sq"], rtol=1e-12)
