@@ -311,14 +311,21 @@ int64_t nif_train_part_floats(const nif_family_view* f, const nif_train_view* t,
 
 /* Grid-gradient scatter of a whole batch from its input gradients dx
  * [n_rows][IN] (grids.py:171-202 accumulate_grad_{2d,1d}_batch: corner
- * contribution (float)(w_fp64 * dx), added into t->grad). deterministic=0:
- * fp32 atomics, warp-aggregated (lanes hitting one cell are summed in lane
- * order, one atomic per group and latent). deterministic=1: contributions
- * sorted by (cell, corner, batch row) -- the reference's np.add.at order --
- * and summed sequentially per cell, bit-reproducible run to run; needs
- * ws_bytes >= nif_grid_scatter_ws_bytes(n_rows) of device workspace.      */
+ * contribution (float)(w_fp64 * dx), added into t->grad).
+ *   deterministic=0: fp32 atomics, warp-aggregated (lanes hitting one cell
+ *     are summed in lane order, one atomic per group and latent);
+ *   deterministic=1: contributions stably sorted by (cell, corner) in batch
+ *     row order -- the reference's np.add.at order -- and summed
+ *     sequentially per cell: bit-identical to the reference's scatter;
+ *   deterministic=2: order-independent fixed point (int64 atomics at a
+ *     per-batch power-of-two scale, one fp32 rounding per cell):
+ *     bit-reproducible on every run and every data-parallel rank at the
+ *     cost of the atomic scatter.
+ * Modes 1 and 2 need ws_bytes >= nif_grid_scatter_ws_bytes(...,
+ * deterministic) of device workspace (mode 2: zeroed once before its first
+ * use; the scatter leaves it ready for the next call).                     */
 size_t nif_grid_scatter_ws_bytes(const nif_family_view* f, const nif_train_view* t,
-                                 int64_t n_rows);
+                                 int64_t n_rows, int deterministic);
 int nif_grid_scatter_dev(const nif_family_view* f, const nif_train_view* t, const int64_t* obj,
                          const double* coord, const int64_t* idx, const int64_t* cursor,
                          int64_t n_rows, const float* dx, int deterministic, void* ws,

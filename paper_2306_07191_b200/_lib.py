@@ -178,7 +178,7 @@ _SIGS = {
                                           P, P, I64, I64, I64, P, P, P, P, I64, P]),
     "nif_train_part_floats": (C.c_int64, [C.POINTER(FamilyView), C.POINTER(TrainView), I64]),
     "nif_grid_scatter_ws_bytes": (C.c_size_t, [C.POINTER(FamilyView), C.POINTER(TrainView),
-                                               I64]),
+                                               I64, C.c_int]),
     "nif_grid_scatter_dev": (C.c_int, [C.POINTER(FamilyView), C.POINTER(TrainView), P, P, P, P,
                                        I64, P, C.c_int, P, C.c_size_t, P]),
     "nif_sample_pass_dev": (C.c_int, [C.POINTER(SceneView), C.POINTER(Camera),

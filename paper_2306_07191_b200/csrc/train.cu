@@ -1270,7 +1270,6 @@ struct ScatterArgs {
   int64_t n_rows;
   const float* dx;  // [n_rows][IN]
   int slots;        // 8 (outer: 4 pos + 4 dir corners) or 10 (+ 2 dist)
-  int gbits;        // bits of the batch position in a sort key
 };
 
 // One contribution slot of batch row g: the grid cell (element offset of its
@@ -1346,47 +1345,213 @@ __global__ void __launch_bounds__(256) scatter_atomic_kernel(ScatterArgs a) {
   }
 }
 
-__device__ __forceinline__ int slot_group(const ScatterArgs& a, int64_t elem) {
-  return elem >= a.t.off_dist && a.f.family == NIF_FAMILY_INNER ? 2
-       : (elem >= a.t.off_dir ? 1 : 0);
+// ---- deterministic=2: order-independent fixed-point scatter ---------------
+// Every contribution (float)(w * dx) is scaled by 2^S (exact in fp64) and
+// rounded to an int64; int64 atomic sums are associative, so the result is
+// bit-identical whatever the atomics' order -- on every run and on every
+// data-parallel rank -- at about the atomic scatter's cost. S is chosen per
+// batch from max |dx| so no cell can overflow: |sum| <= 4 * n_rows * max|dx|
+// < 2^62. The first contribution to a cell claims it (a per-cell tag) and
+// lists it; each listed cell is then rounded once to fp32 (__ll2float_rn,
+// then an exact power-of-two scale) and added into the grad, and its
+// accumulator and tag cleared. Workspace: int64 per family element, uint32
+// tag per element, the cell list, {max |dx| bits, list length, blocks done}
+// -- zeroed once before first use; every call leaves it zeroed again.
+struct FxWs {
+  unsigned long long* acc;
+  uint32_t* tag;
+  uint32_t* list;
+  uint32_t* state;  // [0] max |dx| (fp32 bits), [1] listed cells, [2] convert blocks done
+};
+
+__device__ __forceinline__ int fx_shift(const uint32_t* state, int64_t n_rows) {
+  const float m = __uint_as_float(state[0]);
+  int e = 0;
+  const double bound = 4.0 * (double)n_rows * (double)m;  // bound < 2^e
+  if (bound > 0.0) frexp(bound, &e);
+  const int S = 62 - e;
+  return S < 0 ? 0 : (S > 100 ? 100 : S);
 }
 
-// Deterministic scatter, pass 1: one sort key per contribution,
-// (cell element, corner, batch position) -- np.add.at's order for that cell
-__global__ void scatter_keys_kernel(ScatterArgs a, uint64_t* __restrict__ keys) {
+__global__ void __launch_bounds__(256) fx_max_kernel(const float* __restrict__ dx, int64_t n,
+                                                     uint32_t* state) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(dx[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(state, __float_as_uint(m));  // m >= 0
+}
+
+__device__ __forceinline__ long long fx_q(float v, int S) {
+  return __double2ll_rn(ldexp((double)v, S));
+}
+
+// pass 2: warp-aggregated int64 atomics (exact sums, any order); the first
+// contribution to each cell lists it
+__global__ void __launch_bounds__(256) scatter_fx_add_kernel(ScatterArgs a, FxWs w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = t >> 5;
+  const int slot = (int)(wid % a.slots);
+  const int64_t g = (wid / a.slots) * 32 + lane;
+  const bool valid = g < a.n_rows;
+  const int IN = a.f.dims[0];
+  const int S = fx_shift(w.state, a.n_rows);
+  Contrib c{};
+  if (valid) c = contrib(a, g, slot);
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const unsigned peers = __match_any_sync(act, c.elem);
+  const int leader = __ffs(peers) - 1;
+  for (int k = 0; k < c.n; ++k) {
+    const long long q = fx_q((float)(c.w * (double)a.dx[g * IN + c.kbase + k]), S);
+    unsigned rest = peers & ~(1u << lane);
+    long long sum = q;
+    while (__any_sync(act, rest != 0u)) {
+      const int src = rest ? __ffs(rest) - 1 : lane;
+      const long long pv = __shfl_sync(act, q, src);
+      if (rest) {
+        sum += pv;
+        rest &= rest - 1;
+      }
+    }
+    if (lane == leader) atomicAdd(w.acc + c.elem + k, (unsigned long long)sum);
+  }
+  if (lane == leader && atomicExch(w.tag + c.elem, 1u) == 0u)
+    w.list[atomicAdd(w.state + 1, 1u)] = (uint32_t)c.elem;
+}
+
+// pass 3: each listed cell, int64 -> fp32 once; the last block re-zeroes the state
+template <int NL>
+__device__ __forceinline__ void fx_convert_cell(unsigned long long* __restrict__ acc,
+                                                float* __restrict__ grad, float inv) {
+  long long q[NL];
+  float g[NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {  // every load in flight before the first store
+    q[k] = (long long)acc[k];
+    g[k] = grad[k];
+  }
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    acc[k] = 0ull;
+    grad[k] = g[k] + __fmul_rn(__ll2float_rn(q[k]), inv);
+  }
+}
+
+__global__ void __launch_bounds__(256) scatter_fx_convert_kernel(ScatterArgs a, FxWs w) {
+  const int S = fx_shift(w.state, a.n_rows);
+  const float inv = __int_as_float((127 - S) << 23);  // 2^-S, exact (0 <= S <= 100)
+  const uint32_t n_cells = w.state[1];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cells;
+       i += gridDim.x * blockDim.x) {
+    const int64_t elem = w.list[i];
+    const bool dist = a.f.family == NIF_FAMILY_INNER && elem >= a.t.off_dist;
+    const int n = dist ? a.f.Nd : a.f.N;
+    unsigned long long* acc = w.acc + elem;
+    float* grad = a.t.grad + elem;
+    switch (n) {
+      case 1: fx_convert_cell<1>(acc, grad, inv); break;
+      case 2: fx_convert_cell<2>(acc, grad, inv); break;
+      case 3: fx_convert_cell<3>(acc, grad, inv); break;
+      case 4: fx_convert_cell<4>(acc, grad, inv); break;
+      case 5: fx_convert_cell<5>(acc, grad, inv); break;
+      case 6: fx_convert_cell<6>(acc, grad, inv); break;
+      case 7: fx_convert_cell<7>(acc, grad, inv); break;
+      default: fx_convert_cell<8>(acc, grad, inv); break;
+    }
+    w.tag[elem] = 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(w.state + 2, 1u) == gridDim.x - 1) {  // every block has read the state
+      w.state[0] = 0u;
+      w.state[1] = 0u;
+      w.state[2] = 0u;
+    }
+  }
+}
+
+constexpr int kLatStride = 8;  // floats per precomputed contribution (N, Nd <= 8)
+
+// Deterministic scatter, pass 1: per contribution t = g * slots + slot, its
+// fp32 values (float)(w * dx) per latent and a 32-bit sort key (cell
+// element << 2 | corner). The keys are written in t order, i.e. batch-row
+// major, and the radix sort is stable, so equal keys stay in batch order:
+// sorted by (cell, corner, row) -- np.add.at's order for that cell.
+__global__ void scatter_keys_kernel(ScatterArgs a, uint32_t* __restrict__ keys,
+                                    uint32_t* __restrict__ ids, float* __restrict__ vals) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.n_rows * a.slots) return;
   const int64_t g = t / a.slots;
   const int slot = (int)(t - g * a.slots);
   const Contrib c = contrib(a, g, slot);
   const int corner = slot < 8 ? (slot & 3) : slot - 8;
-  keys[t] = ((uint64_t)c.elem << (a.gbits + 2)) | ((uint64_t)corner << a.gbits) | (uint64_t)g;
+  keys[t] = ((uint32_t)c.elem << 2) | (uint32_t)corner;
+  ids[t] = (uint32_t)t;
+  const int IN = a.f.dims[0];
+  float* v = vals + t * kLatStride;
+  for (int k = 0; k < c.n; ++k) v[k] = (float)(c.w * (double)a.dx[g * IN + c.kbase + k]);
 }
 
-// pass 2: the first key of each cell walks the cell's run in sorted order,
-// adding every contribution into fp32 accumulators seeded with the grad
-__global__ void scatter_segments_kernel(ScatterArgs a, const uint64_t* __restrict__ keys,
-                                        int64_t n_keys) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_keys) return;
-  const int sh = a.gbits + 2;
-  const uint64_t elem = keys[i] >> sh;
-  if (i > 0 && (keys[i - 1] >> sh) == elem) return;
-  const int IN = a.f.dims[0];
-  const int grp = slot_group(a, (int64_t)elem);
-  const int n = grp == 2 ? a.f.Nd : a.f.N;
-  float acc[kMaxIn];
-  float* dst = a.t.grad + elem;
-  for (int k = 0; k < n; ++k) acc[k] = dst[k];
-  const uint64_t gmask = (1ull << a.gbits) - 1;
-  for (int64_t j = i; j < n_keys && (keys[j] >> sh) == elem; ++j) {
-    const int64_t g = (int64_t)(keys[j] & gmask);
-    const int corner = (int)((keys[j] >> a.gbits) & 3);
-    const int slot = grp == 2 ? 8 + corner : grp * 4 + corner;
-    const Contrib c = contrib(a, g, slot);
-    for (int k = 0; k < n; ++k) acc[k] += (float)(c.w * (double)a.dx[g * IN + c.kbase + k]);
+// pass 2: one warp per sorted position; the warp whose position starts a
+// cell's run walks the run 32 contributions at a time (lanes load in
+// parallel, coalesced) and adds them in sorted order into fp32
+// accumulators seeded with the grad: one sequential fp32 sum per latent,
+// exactly np.add.at's. (Runs can be hundreds long -- e.g. the outer
+// direction grid, where one light makes most shadow rays of an object hit
+// the same few cells -- so a thread-serial walk would be latency-bound.)
+template <int NL>
+__device__ __forceinline__ void seg_sum_warp(float* dst, const uint32_t* keys,
+                                             const uint32_t* ids, const float* vals, int64_t i,
+                                             int64_t n_keys, uint32_t cell, int lane) {
+  float acc[NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) acc[k] = dst[k];
+  for (int64_t j0 = i;; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const bool in = j < n_keys && (keys[j] >> 2) == cell;
+    const unsigned m = __ballot_sync(0xffffffffu, in);  // a prefix of the lanes (sorted)
+    float v[NL];
+    if (in) {
+      const float* src = vals + (size_t)ids[j] * kLatStride;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) v[k] = src[k];
+    }
+    const int cnt = __popc(m);
+    for (int q = 0; q < cnt; ++q)
+#pragma unroll
+      for (int k = 0; k < NL; ++k) acc[k] += __shfl_sync(0xffffffffu, v[k], q);
+    if (cnt < 32) break;
   }
-  for (int k = 0; k < n; ++k) dst[k] = acc[k];
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NL; ++k) dst[k] = acc[k];
+}
+
+__global__ void __launch_bounds__(256) scatter_segments_kernel(
+    ScatterArgs a, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ids,
+    const float* __restrict__ vals, int64_t n_keys) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n_keys) return;
+  const uint32_t cell = keys[i] >> 2;
+  if (i > 0 && (keys[i - 1] >> 2) == cell) return;  // warp-uniform
+  const bool dist = a.f.family == NIF_FAMILY_INNER && (int64_t)cell >= a.t.off_dist;
+  const int n = dist ? a.f.Nd : a.f.N;
+  float* dst = a.t.grad + cell;
+  switch (n) {
+    case 1: seg_sum_warp<1>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    case 2: seg_sum_warp<2>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    case 3: seg_sum_warp<3>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    case 4: seg_sum_warp<4>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    case 5: seg_sum_warp<5>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    case 6: seg_sum_warp<6>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    case 7: seg_sum_warp<7>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+    default: seg_sum_warp<8>(dst, keys, ids, vals, i, n_keys, cell, lane); break;
+  }
 }
 
 int bits_for(uint64_t v) {
@@ -1396,8 +1561,8 @@ int bits_for(uint64_t v) {
 }
 
 struct ScatterWs {
-  uint64_t* keys_in;
-  uint64_t* keys_out;
+  uint32_t *keys_in, *keys_out, *ids_in, *ids_out;
+  float* vals;
   void* temp;
   size_t temp_bytes, total;
 };
@@ -1407,15 +1572,20 @@ size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 ScatterWs scatter_ws(int64_t n_keys, int end_bit, void* base) {
   ScatterWs w{};
   size_t temp = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                 (int)(n_keys > 0 ? n_keys : 1), 0, end_bit);
-  const size_t kb = al256((size_t)(n_keys > 0 ? n_keys : 1) * 8);
+  const int nk = (int)(n_keys > 0 ? n_keys : 1);
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, nk, 0, end_bit);
+  const size_t kb = al256((size_t)nk * 4);
   uint8_t* p = (uint8_t*)base;
-  w.keys_in = (uint64_t*)p;
-  w.keys_out = (uint64_t*)(p + kb);
-  w.temp = p + 2 * kb;
+  w.keys_in = (uint32_t*)p;
+  w.keys_out = (uint32_t*)(p + kb);
+  w.ids_in = (uint32_t*)(p + 2 * kb);
+  w.ids_out = (uint32_t*)(p + 3 * kb);
+  w.vals = (float*)(p + 4 * kb);
+  const size_t vb = al256((size_t)nk * kLatStride * 4);
+  w.temp = p + 4 * kb + vb;
   w.temp_bytes = temp;
-  w.total = 2 * kb + al256(temp);
+  w.total = 4 * kb + vb + al256(temp);
   return w;
 }
 
@@ -1452,10 +1622,13 @@ extern "C" int64_t nif_train_part_floats(const nif_family_view* f, const nif_tra
 }
 
 extern "C" size_t nif_grid_scatter_ws_bytes(const nif_family_view* f, const nif_train_view* t,
-                                            int64_t n_rows) {
-  const int gbits = bits_for((uint64_t)(n_rows > 1 ? n_rows - 1 : 1));
-  const int end_bit = bits_for((uint64_t)t->numel) + 2 + gbits;
-  return scatter_ws(n_rows * scatter_slots(f), end_bit, nullptr).total;
+                                            int64_t n_rows, int deterministic) {
+  if (deterministic == 2)  // acc, tag, list, state
+    return al256((size_t)t->numel * 8) + al256((size_t)t->numel * 4) +
+           al256((size_t)(n_rows * scatter_slots(f)) * 4) + 256;
+  if (deterministic == 1)
+    return scatter_ws(n_rows * scatter_slots(f), bits_for((uint64_t)t->numel) + 2, nullptr).total;
+  return 0;
 }
 
 extern "C" int nif_grid_scatter_dev(const nif_family_view* f, const nif_train_view* t,
@@ -1464,26 +1637,51 @@ extern "C" int nif_grid_scatter_dev(const nif_family_view* f, const nif_train_vi
                                     int deterministic, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_rows <= 0) return NIF_OK;
-  if (f->N > kMaxIn || f->Nd > kMaxIn) return fail(NIF_ERR_UNSUPPORTED, "too many latents");
-  const int gbits = bits_for((uint64_t)(n_rows > 1 ? n_rows - 1 : 1));
-  const int end_bit = bits_for((uint64_t)t->numel) + 2 + gbits;
-  if (end_bit > 64) return fail(NIF_ERR_UNSUPPORTED, "sort key wider than 64 bits");
-  ScatterArgs a{*f, *t, obj, coord, idx, cursor, n_rows, dx, scatter_slots(f), gbits};
+  if (f->N > kLatStride || f->Nd > kLatStride)
+    return fail(NIF_ERR_UNSUPPORTED, "more than %d latents per cell", kLatStride);
+  ScatterArgs a{*f, *t, obj, coord, idx, cursor, n_rows, dx, scatter_slots(f)};
   const int64_t n_keys = n_rows * a.slots;
   if (!deterministic) {
     const int64_t threads = ((n_rows + 31) / 32) * 32 * a.slots;
     scatter_atomic_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
     return check_launch("nif_grid_scatter_dev(atomic)");
   }
+  if (deterministic == 2) {
+    const size_t need = nif_grid_scatter_ws_bytes(f, t, n_rows, 2);
+    if (ws == nullptr || ws_bytes < need)
+      return fail(NIF_ERR_VALUE, "scatter workspace needs %zu bytes", need);
+    // [state | acc | tag | list]: the list last, so calls with fewer rows
+    // than the workspace was sized for see the same state / accumulators
+    uint8_t* p = (uint8_t*)ws;
+    const size_t o1 = 256, o2 = o1 + al256((size_t)t->numel * 8);
+    const size_t o3 = o2 + al256((size_t)t->numel * 4);
+    FxWs w{(unsigned long long*)(p + o1), (uint32_t*)(p + o2), (uint32_t*)(p + o3),
+           (uint32_t*)p};
+    const int64_t n_dx = n_rows * f->dims[0];
+    int64_t mb = (n_dx + 1023) / 1024;
+    if (mb > sm_count()) mb = sm_count();
+    fx_max_kernel<<<(unsigned)(mb > 0 ? mb : 1), 256, 0, st>>>(dx, n_dx, w.state);
+    const int64_t threads = ((n_rows + 31) / 32) * 32 * a.slots;
+    scatter_fx_add_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a, w);
+    int64_t cb = (n_keys + 255) / 256;
+    if (cb > 2 * sm_count()) cb = 2 * sm_count();
+    scatter_fx_convert_kernel<<<(unsigned)cb, 256, 0, st>>>(a, w);
+    return check_launch("nif_grid_scatter_dev(fixed point)");
+  }
+  const int end_bit = bits_for((uint64_t)t->numel) + 2;
+  if (end_bit > 32 || n_keys > INT32_MAX)
+    return fail(NIF_ERR_UNSUPPORTED, "deterministic scatter: family buffer above 2^30 floats");
   ScatterWs w = scatter_ws(n_keys, end_bit, ws);
   if (ws == nullptr || ws_bytes < w.total)
     return fail(NIF_ERR_VALUE, "scatter workspace needs %zu bytes", w.total);
-  scatter_keys_kernel<<<(unsigned)((n_keys + 255) / 256), 256, 0, st>>>(a, w.keys_in);
+  const unsigned blocks = (unsigned)((n_keys + 255) / 256);
+  scatter_keys_kernel<<<blocks, 256, 0, st>>>(a, w.keys_in, w.ids_in, w.vals);
   size_t tb = w.temp_bytes;
-  if (cub::DeviceRadixSort::SortKeys(w.temp, tb, w.keys_in, w.keys_out, (int)n_keys, 0, end_bit,
-                                     st) != cudaSuccess)
+  // stable: equal (cell, corner) keys keep batch-row order
+  if (cub::DeviceRadixSort::SortPairs(w.temp, tb, w.keys_in, w.keys_out, w.ids_in, w.ids_out,
+                                      (int)n_keys, 0, end_bit, st) != cudaSuccess)
     return check_launch("nif_grid_scatter_dev(sort)");
-  scatter_segments_kernel<<<(unsigned)((n_keys + 255) / 256), 256, 0, st>>>(a, w.keys_out,
-                                                                          n_keys);
+  scatter_segments_kernel<<<(unsigned)((n_keys + 7) / 8), 256, 0, st>>>(a, w.keys_out, w.ids_out,
+                                                                       w.vals, n_keys);
   return check_launch("nif_grid_scatter_dev(deterministic)");
 }

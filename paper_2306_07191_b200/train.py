@@ -263,17 +263,22 @@ class _Sink:
     of how many objects the batch touches, against 1.6 MB / 0.7 MB per
     touched object for a dense grid-gradient all-reduce."""
 
-    def __init__(self, step: "_Step", bs: int, world: int, rank: int, group, deterministic: bool):
+    def __init__(self, step: "_Step", bs: int, world: int, rank: int, group, deterministic: bool,
+                 scatter_mode: Optional[int] = None):
         torch = _torch()
         L = _lib.lib()
         fam = step.fam
         dev = step.model.device
         self.step, self.bs, self.world, self.rank, self.group = step, bs, world, rank, group
         self.det = bool(deterministic)
-        # Every rank scatters the whole batch into its own replica: the sorted
-        # (order-fixed) scatter keeps the replicas bit-identical, where fp32
-        # atomics would let them drift apart in the last bits
-        self.det_scatter = self.det or group is not None
+        # Every rank scatters the whole batch into its own replica, so the
+        # scatter must not depend on the atomics' order or the replicas would
+        # drift apart in the last bits: deterministic=True uses the sorted
+        # scatter (np.add.at's order), data parallel otherwise the
+        # order-independent fixed-point one (about the atomic scatter's cost)
+        self.scatter_mode = 1 if self.det else (2 if group is not None else 0)
+        if scatter_mode is not None:
+            self.scatter_mode = scatter_mode
         self.IN = int(fam.dims[0])
         self.dx_len = (bs * self.IN + 63) // 64 * 64
         off_w = fam.offsets["w"][0]
@@ -285,9 +290,9 @@ class _Sink:
         self.grad_mlp = fam.grad[off_w:off_w + self.n_mlp]
         self.part = self.ws = None
         self.part_n = 0
-        if self.det_scatter:
-            nb = int(L.nif_grid_scatter_ws_bytes(step.fv, step.tv, bs))
-            self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        if self.scatter_mode:
+            nb = int(L.nif_grid_scatter_ws_bytes(step.fv, step.tv, bs, self.scatter_mode))
+            self.ws = torch.zeros(max(nb, 1), dtype=torch.uint8, device=dev)
         if self.det:
             self.part_n = int(L.nif_train_part_floats(step.fv, step.tv, bs))
             self.part = torch.empty(max(self.part_n, 1), dtype=torch.float32, device=dev)
@@ -307,7 +312,7 @@ class _Sink:
             import torch.distributed as dist
             dist.all_reduce(self.comm, group=self.group)
         L.nif_grid_scatter_dev(st.fv, st.tv, p(obj), p(coord), idx_ptr, cursor_ptr, n_rows,
-                               p(self.dx), int(self.det_scatter), p(self.ws),
+                               p(self.dx), self.scatter_mode, p(self.ws),
                                0 if self.ws is None else int(self.ws.numel()), sp)
         self.grad_mlp.copy_(self.mlp)
 
