@@ -21,6 +21,9 @@ int nif_debug_set_prof_gather(void* buf);
  * with look-back (reference order), 2 persistent TMA-pipelined look-back
  * (reference order). All produce the same records.                     */
 int nif_debug_set_gather_variant(int v);
+/* CTAs per SM of the hot-path gather / fused query grids (0: default) */
+int nif_debug_set_gather_grid(int ctas_per_sm);
+int nif_debug_set_query_grid(int ctas_per_sm);
 /* Culling statistics of the hot-path gather since the last call (rays,
  * bundle survivors, prefilter survivors, classified hits); only in a
  * library built with -DNIF_GATHER_STATS (tools/gather_stats.py).       */

@@ -160,6 +160,8 @@ _SIGS = {
     "nif_debug_set_prof": (C.c_int, [P]),
     "nif_debug_set_prof_gather": (C.c_int, [P]),
     "nif_debug_set_gather_variant": (C.c_int, [C.c_int]),
+    "nif_debug_set_gather_grid": (C.c_int, [C.c_int]),
+    "nif_debug_set_query_grid": (C.c_int, [C.c_int]),
     "nif_debug_set_query_variant": (C.c_int, [C.c_int]),
     "nif_debug_set_train_variant": (C.c_int, [C.c_int]),
     "nif_batch_counts_dev": (C.c_int, [P, P, I64, I32, P, P]),

@@ -1189,6 +1189,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
 }
 
 long long* g_gprof = nullptr;  // diagnostic phase stamps (nif_debug_set_prof_gather)
+int g_gather_cpsm = 0;     // CTAs per SM of the hot-path gather grid (0: NIF_GATHER_MINB_U)
 int g_gather_variant = 0;  // 0 unordered warp chunks, 1 one tile per CTA, 2 persistent ordered
 
 size_t fused_ws(int64_t n) {
@@ -1237,7 +1238,7 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
         *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
   else if (g_gather_variant == 0) {
     const int64_t chunks = (n + 31) / 32;
-    int64_t grid = (int64_t)sm_count() * NIF_GATHER_MINB_U;
+    int64_t grid = (int64_t)sm_count() * (g_gather_cpsm > 0 ? g_gather_cpsm : NIF_GATHER_MINB_U);
     if (grid * (kThreads / 32) > chunks) grid = (chunks + kThreads / 32 - 1) / (kThreads / 32);
     gather_warp_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
         *s, route, origins, dirs, tmaxs, n, *out, (unsigned long long*)ctr,
@@ -1274,6 +1275,11 @@ extern "C" int nif_debug_gather_stats(unsigned long long* out) {
   (void)out;
   return fail(NIF_ERR_UNSUPPORTED, "built without NIF_GATHER_STATS");
 #endif
+}
+
+extern "C" int nif_debug_set_gather_grid(int ctas_per_sm) {
+  g_gather_cpsm = ctas_per_sm;
+  return NIF_OK;
 }
 
 extern "C" int nif_debug_set_gather_variant(int v) {

@@ -344,6 +344,7 @@ struct TcArgs {
 
 long long* g_prof = nullptr;
 int g_query_variant = 0;  // nif_debug_set_query_variant
+int g_query_cpsm = 0;     // CTAs per SM cap of the fused query grids (0: TMEM/occupancy bound)
 
 __device__ __forceinline__ void store_chunk(uint8_t* base, int row, int chunk, int kp,
                                             uint4 v) {
@@ -1558,6 +1559,7 @@ int launch_ts(const TcArgs& a, cudaStream_t st) {
     return check_launch("query_ts: smem attribute");
   const int per_sm_tmem = 512 / C::COLS;
   int per_sm = per_sm_tmem < TPS / G ? per_sm_tmem : TPS / G;
+  if (g_query_cpsm > 0 && per_sm > g_query_cpsm) per_sm = g_query_cpsm;
   if (per_sm < 1) per_sm = 1;
   const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
   int64_t grid = (int64_t)sm_count() * per_sm;
@@ -2096,6 +2098,11 @@ extern "C" int nif_occ_init_dev(const uint8_t* bvh_occ, int64_t n, uint8_t* occ_
   occ_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(bvh_occ, n,
                                                                                   occ_ray);
   return check_launch("nif_occ_init_dev");
+}
+
+extern "C" int nif_debug_set_query_grid(int ctas_per_sm) {
+  g_query_cpsm = ctas_per_sm;
+  return NIF_OK;
 }
 
 extern "C" int nif_debug_set_query_variant(int v) {
