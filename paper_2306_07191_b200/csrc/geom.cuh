@@ -15,7 +15,7 @@ namespace nif {
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 2.0 * 3.141592653589793;
 constexpr double kDegenerateRadius = 1e-9;  // geometry.py:22
-constexpr int kStack = 64;                  // device traversal stack
+constexpr int kStack = 120;  // device traversal stack: bvh.py:26 MAX_DEPTH
 
 struct Hit3 {
   bool hit;

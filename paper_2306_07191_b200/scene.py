@@ -25,7 +25,7 @@ N_BINS = 16           # bvh.py:22
 COST_TRAVERSAL = 1.0  # bvh.py:23
 COST_INTERSECT = 1.5  # bvh.py:24
 MAX_DEPTH = 120       # bvh.py:26 (reference stack budget)
-DEVICE_STACK = 64     # traversal stack of the CUDA kernels
+DEVICE_STACK = 120    # traversal stack of the CUDA kernels (bvh.py:26 MAX_DEPTH)
 EPSILON_SCALE = 1e-4  # renderer.py:43
 CONTAINMENT_TOL = 1e-6  # geometry.py:20
 
