@@ -102,6 +102,8 @@ def parse():
     p.add_argument("--sharing", default="shared", choices=["shared", "per_object"],
                    help="NifConfig.sharing (per_object: one MLP per object, bucketed query)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-train-leg", action="store_true",
+                   help="skip the online-training epoch measured after the visibility pass")
     p.add_argument("--e2e-chunks", type=int, default=4,
                    help="chunks of the e2e host path (H2D of chunk k+1 overlaps chunk k)")
     p.add_argument("--profile", action="store_true", help="few steps, no clocks / cpu leg")
@@ -493,6 +495,37 @@ def main():
         h2d_gbs = max(h2d_gbs, n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9)
     del h2d_src, h2d_dst
 
+    # --- online training: one spp of samples collected
+    # band-sharded across the ranks (ordered all-gather into the reference's
+    # global order), then one epoch of the reference schedule; under torchrun
+    # every optimiser step is the data-parallel step -- one all-reduce of
+    # [batch input gradients | MLP gradients], captured in the step's CUDA
+    # graph. Host clock around the synchronous train() call, max over ranks.
+    train_leg = None
+    if not args.no_train_leg and not args.profile:
+        from paper_2306_07191_b200 import train as tr
+        smp = tr.collect_samples(scene, spp=1, seed=scene.seed)
+        tm = build_model(NifConfig(seed=0, sharing=args.sharing), scene)
+        tr.train(tm, smp, epochs=1)  # warm: graph capture, communicators
+        barrier()
+        t0 = time.perf_counter()
+        curve = tr.train(tm, smp, epochs=1)
+        barrier()
+        ep_s = time.perf_counter() - t0
+        if ws > 1:
+            te = torch.tensor([ep_s], device=dev)
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+            ep_s = float(te[0])
+        cfgt = tm.config
+        n_steps = -(-smp.n_outer // cfgt.outer.batch_size) - (-smp.n_inner // cfgt.inner.batch_size)
+        train_leg = {"epoch_ms": ep_s * 1e3, "optimizer_steps": int(n_steps),
+                     "steps_per_s": n_steps / ep_s, "samples": smp.n_outer + smp.n_inner,
+                     "spp": 1, "loss": float(curve[-1, 2]),
+                     "mode": (f"data parallel over {ws} GPUs: one NCCL all-reduce per step "
+                              "inside the step graph, fixed-point grid scatter")
+                     if ws > 1 else "single GPU: captured 3-launch step per batch"}
+        del tm, smp
+
     # --- reduce over ranks (max time) ---------------------------------------
     ms, e2e_ms = ms_local, e2e_ms_local
     n_total = n
@@ -599,6 +632,7 @@ def main():
         # per step: gather_fused, query_tc outer (side stream), query_tc inner
         # (plus two memset nodes for the gather's counters / scan state)
         "gpu_launches": args.steps * 3,
+        "train": train_leg,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line))
