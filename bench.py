@@ -63,8 +63,8 @@ RESOLUTION = {"c1": (256, 256), "c2": (1920, 1080), "c3": (1920, 1080), "c4": (3
 # kernels of one visibility pass (names as ncu reports them) and their
 # algorithmic work: see DESIGN.md section 4
 K_GATHER = "gather_warp_kernel"
-K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4, 0>"
-K_INNER = "query_ts_kernel<5, 3, 48, 3, 3, 6, 0>"
+K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4, 0, 1, 0>"
+K_INNER = "query_ts_kernel<5, 3, 48, 3, 1, 4, 0, 1, 1>"
 
 
 def workload_label(args):

@@ -1396,10 +1396,10 @@ __global__ void __launch_bounds__(128 * G, TPS / G) mlp_tiles_kernel(MlpArgs a) 
 // tiles (nif_query_bucketed_dev); each warpgroup walks a contiguous range of
 // tiles and keeps its own copy of the current object's weights, reloading
 // it only when the object changes.
-#ifndef NIF_ENC_ISSUE
-#define NIF_ENC_ISSUE 0  // 0: under the last hidden MMA; k: under the k-th (k=1 spills, slower)
-#endif
-template <int N, int ND, int W, int L, int G, int TPS, bool PO = false, int HD = 1>
+// EI: where the next tile's record loads and corner gathers are issued --
+// 0 under the last hidden layer's MMA, k >= 1 under the k-th, -1 right after
+// the first layer's MMA (the earliest; needs the registers of G = 1 CTAs)
+template <int N, int ND, int W, int L, int G, int TPS, bool PO = false, int HD = 1, int EI = 0>
 __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   using C = MlpCfg<W, L, G, HD>;
   constexpr bool INNER = ND > 0;
@@ -1507,6 +1507,10 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
       tc::mma_f16_ts(acc, a_op, tc::smem_desc(opaque_u32(sWa), 128, kK1 * 16), idW, 0);
       tc::mma_commit(bar);
     }
+    if constexpr (EI < 0) {  // next tile's gathers in flight under the whole MLP chain
+      issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
+      rb = fetch(t + 2 * stride);
+    }
     tc::mbar_wait_sleep(bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
@@ -1523,7 +1527,7 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
           tc::mma_f16_ts(acc, a_op + s * 8, tc::smem_desc(wb + s * 256, 128, Kp * 16), idW, s > 0);
         tc::mma_commit(bar);
       }
-      if (layer == (NIF_ENC_ISSUE > 0 && NIF_ENC_ISSUE < L ? NIF_ENC_ISSUE : L - 1)) {
+      if (EI >= 0 && layer == (EI > 0 && EI < L ? EI : L - 1)) {
         // next tile's gathers in flight under the remaining MMAs + head
         issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
         rb = fetch(t + 2 * stride);
@@ -1549,10 +1553,10 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
 }
 
-template <int N, int ND, int W, int L, int G, int TPS, bool PO = false, int HD = 1>
+template <int N, int ND, int W, int L, int G, int TPS, bool PO = false, int HD = 1, int EI = 0>
 int launch_ts(const TcArgs& a, cudaStream_t st) {
   using C = MlpCfg<W, L, G, HD>;
-  auto kern = query_ts_kernel<N, ND, W, L, G, TPS, PO, HD>;
+  auto kern = query_ts_kernel<N, ND, W, L, G, TPS, PO, HD, EI>;
   const size_t smem = C::SMEM + (PO ? (size_t)(G - 1) * C::W_AL : 0);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
@@ -1590,7 +1594,7 @@ int launch_ts_po(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int
     return 0;
   }
   if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
-    *rc = launch_ts<5, 3, 48, 3, 3, 6, true>(a, st);
+    *rc = launch_ts<5, 3, 48, 3, 1, 4, true, 1, 1>(a, st);
     return 0;
   }
   return 1;
@@ -1605,7 +1609,7 @@ int launch_ts_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, in
       return 0;
     }
     if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
-      *rc = launch_ts<5, 3, 48, 3, 3, 6, false, 4>(a, st);
+      *rc = launch_ts<5, 3, 48, 3, 1, 4, false, 4, 1>(a, st);
       return 0;
     }
     return 1;
@@ -1621,8 +1625,19 @@ int launch_ts_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, in
     NIF_TS(3, 0, 64, 2, 1, 4)
     NIF_TS(5, 3, 48, 3, 1, 6)
   }
+  if (g_query_variant == 12) {  // round-1 inner configuration: 2 CTAs x 3 warpgroups per SM
+    NIF_TS(5, 3, 48, 3, 3, 6)
+  }
   NIF_TS(3, 0, 64, 2, 2, 4)
-  NIF_TS(5, 3, 48, 3, 3, 6)
+  // inner default: one warpgroup per CTA, 4 CTAs per SM (TMEM: 80 columns
+  // per tile, allocated as 128), 128 registers per thread -- no spills --
+  // and the next tile's gathers issued under the first hidden layer's MMA.
+  // C2: 51.9 us vs 57.1 us for 2 CTAs x 3 warpgroups (6 tiles per SM at the
+  // 80-register cap, spilling; variant 12)
+  if (f.N == 5 && f.family == NIF_FAMILY_INNER && f.Nd == 3 && W == 48 && L == 3) {
+    *rc = launch_ts<5, 3, 48, 3, 1, 4, false, 1, 1>(a, st);
+    return 0;
+  }
   // C5 sweep shapes (TMEM: W=48 -> 80 columns per tile, 64 -> 112, 128 -> 208)
   NIF_TS(3, 0, 64, 3, 2, 4)
   NIF_TS(3, 0, 64, 4, 2, 4)

@@ -1,8 +1,9 @@
 #!/bin/bash
 # Build an alternative libnif_b200.so with extra nvcc defines for one unit:
-#   tools/build_variant.sh <tag> <unit.cu> <nvcc flags...>  -> build/libnif_<tag>.so
-# (select at run time with NIF_B200_LIB=build/libnif_<tag>.so)
+#   tools/build_variant.sh <tag> <unit.cu> <nvcc flags...>  -> variants/libnif_<tag>.so
+# (select at run time with NIF_B200_LIB=variants/libnif_<tag>.so; variants/ travels to the GPU box)
 set -e
+mkdir -p "$(dirname "$0")/../variants"
 cd "$(dirname "$0")/.."
 tag=$1; unit=$2; shift 2
 ARCH="-gencode arch=compute_100a,code=sm_100a"
@@ -16,5 +17,5 @@ done
 mad=""
 case $unit in trace.cu|exact.cu|gather.cu|train.cu) mad="-fmad=false";; esac
 nvcc $ARCH $COMMON $mad "$@" -c paper_2306_07191_b200/csrc/$unit -o build/var_$tag.o
-nvcc $ARCH -shared -cudart static -o build/libnif_$tag.so $objs build/var_$tag.o -Xlinker --no-undefined -lpthread -ldl -lrt
-echo build/libnif_$tag.so
+nvcc $ARCH -shared -cudart static -o variants/libnif_$tag.so $objs build/var_$tag.o -Xlinker --no-undefined -lpthread -ldl -lrt
+echo variants/libnif_$tag.so
