@@ -734,77 +734,12 @@ __global__ void __launch_bounds__(128 * kTpc) query_tc_kernel(TcArgs a) {
   if (warp == 0) tc::tmem_dealloc(tbase, l.tmem_cols);
 }
 
-// ---------------------------------------------------------------------------
-// Specialised tcgen05 query kernel (shapes known at compile time)
-//
-// G independent tile pipelines per CTA (one warpgroup = 128 records each,
-// own mbarrier, own named barrier, own W-column TMEM accumulator) share one
-// resident copy of the weights, so 8 tiles are in flight per SM without
-// replicating weights 8 times. Per tile only one activation tile of
-// 128 x Kp fp16 is kept: the layer-1 input (K = 16) lives in K-chunks 0-1 of
-// that same tile (descriptor SBO = Kp*16), so the constant tail (bias
-// column = 1, zero padding) is written once and never overwritten.
-// Waiting is a suspending try_wait; TMEM reads issue every column chunk of
-// a layer before one wait. The next tile's latent-corner gathers are issued
-// under the head MMA, whose round trip hides most of their L2 latency.
-// ---------------------------------------------------------------------------
-
-template <int N, int ND, int W, int L, int G>
-struct Tc2 {
-  static constexpr int IN = 2 * N + ND;
-  static constexpr int Kp = ((W + 1) + 15) / 16 * 16;
-  static constexpr int Wc = (W + 31) / 32 * 32;
-  static constexpr int COLS_RAW = G * Wc;
-  static constexpr int COLS = COLS_RAW <= 32 ? 32 : COLS_RAW <= 64 ? 64 : COLS_RAW <= 128 ? 128
-                              : COLS_RAW <= 256 ? 256 : 512;
-  static constexpr size_t OFF_HEADF =
-      (size_t)W * kK1 * 2 + (size_t)(L - 1) * W * Kp * 2 + (size_t)16 * Kp * 2;
-  static constexpr size_t W_BYTES = OFF_HEADF + ((size_t)(W + 1) * 4 + 15) / 16 * 16;
-  static constexpr size_t W_AL = (W_BYTES + 255) / 256 * 256;
-  static constexpr size_t A_BYTES = (size_t)kTileRows * Kp * 2;
-  static constexpr size_t SMEM = W_AL + G * A_BYTES + 64;
-  static_assert(W % 16 == 0 && IN + 1 <= kK1 && L >= 2, "shape");
-  static_assert(COLS_RAW <= 512, "TMEM");
-};
-
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   uint32_t y;
   asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
   return y;
 }
 
-template <int W>
-__device__ __forceinline__ void epilogue_act(uint32_t taddr, uint8_t* sA, int trow, int Kp,
-                                             __half2 slope2) {
-  // W fp32 accumulator columns of this row -> leaky ReLU -> fp16 chunks,
-  // in groups of up to 32 columns (two loads in flight, one wait) to bound
-  // the live registers.
-  uint8_t* rowp = sA + (size_t)(trow >> 3) * (Kp * 16) + (trow & 7) * 16;
-#pragma unroll
-  for (int g0 = 0; g0 < W; g0 += 32) {
-    constexpr int GMAX = 32;
-    uint32_t r[GMAX];
-    const int gw = (W - g0) < GMAX ? (W - g0) : GMAX;  // 16 or 32, compile-time after unroll
-    tc::tmem_ld16_nw(taddr + g0, r);
-    if (gw > 16) tc::tmem_ld16_nw(taddr + g0 + 16, r + 16);
-    tc::tmem_ld_fence<GMAX>(r);
-#pragma unroll
-    for (int c = 0; c < GMAX / 8; ++c) {
-      if (c * 8 >= gw) break;
-      uint32_t h[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        __half2 q = __floats2half2_rn(__uint_as_float(r[8 * c + 2 * i]),
-                                      __uint_as_float(r[8 * c + 2 * i + 1]));
-        q = __hmax2(q, __hmul2(q, slope2));
-        h[i] = h2u(q);
-      }
-      *reinterpret_cast<uint4*>(rowp + (g0 / 8 + c) * 128) = make_uint4(h[0], h[1], h[2], h[3]);
-    }
-  }
-}
-
-// f32x2 helpers (FFMA2 / FMUL2 on sm_100)
 __device__ __forceinline__ unsigned long long f2pack(float a, float b) {
   unsigned long long r;
   asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
@@ -902,183 +837,6 @@ __device__ __forceinline__ void head_simt_n(uint32_t taddr, const float* __restr
     out[j] = s.x + s.y;
   }
 }
-
-template <int N, int ND, int W, int L, int G, int TPS>
-__global__ void __launch_bounds__(128 * G, TPS / G) query_tc2_kernel(TcArgs a) {
-  using C = Tc2<N, ND, W, L, G>;
-  constexpr bool INNER = ND > 0;
-  constexpr int Kp = C::Kp;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const FastLayout& l = a.l;
-  const int tid = threadIdx.x;
-  const int wg = tid >> 7;
-  const int trow = tid & (kTileRows - 1);
-  const int quad = (tid >> 5) & 3;
-  const bool leader = trow == 0;
-  uint8_t* sW = smem;
-  uint8_t* sA = smem + C::W_AL + (size_t)wg * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::W_AL + G * C::A_BYTES);
-  uint64_t* bar = bars + wg;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + G);
-
-  const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
-  const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
-  const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
-  const int64_t n = min(*a.count, a.cap);
-  const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
-  const int64_t stride = (int64_t)gridDim.x * G;
-  const int64_t first = (int64_t)blockIdx.x * G + wg;
-
-  // corner gathers of tile k+1 in flight under tile k's head MMA, record
-  // words of tile k+2 one stage earlier
-  EncIn<N, ND> ea;
-  issue_enc<N, ND>(ea, load_rec(a, first, trow, n, INNER), tpos, tdir, tdist, l.R, l.Rd);
-  RecIn rb = load_rec(a, first + stride, trow, n, INNER);
-
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a.blob);
-    uint4* dst = reinterpret_cast<uint4*>(sW);
-    for (int i = tid; i < (int)(C::W_BYTES / 16); i += blockDim.x) dst[i] = __ldg(src + i);
-  }
-  // constant tail of this warpgroup's activation tile: column W = 1, rest 0
-#pragma unroll
-  for (int c = W / 8; c < Kp / 8; ++c) {
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (c == W / 8) v.x = h2u(__halves2half2(__float2half_rn(1.f), __float2half_rn(0.f)));
-    store_chunk(sA, trow, c, Kp, v);
-  }
-  if (tid == 0) {
-    for (int g = 0; g < G; ++g) tc::mbar_init(bars + g, 1);
-    tc::fence_barrier_init();
-  }
-  if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
-  tc::fence_async_smem();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t acc = *tslot + (uint32_t)(wg * C::Wc);
-  const uint32_t lane_acc = acc + ((uint32_t)(quad * 32) << 16);
-
-  const uint32_t sAa = tc::smem_u32(sA), sWa = tc::smem_u32(sW);
-  constexpr uint32_t off_hidden = (uint32_t)W * kK1 * 2;
-  constexpr uint32_t off_head = off_hidden + (uint32_t)(L - 1) * W * Kp * 2;
-  const uint32_t idW = tc::idesc_f16(W), id16 = tc::idesc_f16(16);
-  const __half2 slope2 = __float2half2_rn(kSlope);
-  const uint32_t bar_id = 1 + wg;
-
-  uint32_t phase = 0;
-  for (int64_t t = first; t < n_tiles; t += stride) {
-    const int64_t row = t * kTileRows + trow;
-    const bool valid = ea.valid;
-    const int my_ray = ea.ray;
-    {
-      float x[16];
-      finish_enc<N, ND>(ea, x);
-      uint4 v0, v1;
-      v0.x = h2u(__floats2half2_rn(x[0], x[1]));
-      v0.y = h2u(__floats2half2_rn(x[2], x[3]));
-      v0.z = h2u(__floats2half2_rn(x[4], x[5]));
-      v0.w = h2u(__floats2half2_rn(x[6], x[7]));
-      v1.x = h2u(__floats2half2_rn(x[8], x[9]));
-      v1.y = h2u(__floats2half2_rn(x[10], x[11]));
-      v1.z = h2u(__floats2half2_rn(x[12], x[13]));
-      v1.w = h2u(__floats2half2_rn(x[14], x[15]));
-      store_chunk(sA, trow, 0, Kp, v0);
-      store_chunk(sA, trow, 1, Kp, v1);
-    }
-    tc::fence_async_smem();
-    tc::fence_before_sync();
-    tc::named_sync(bar_id, 128);
-    if (leader) {
-      tc::fence_after_sync();
-      tc::mma_f16(acc, tc::smem_desc(opaque_u32(sAa), 128, Kp * 16),
-                  tc::smem_desc(opaque_u32(sWa), 128, kK1 * 16), idW, 0);
-      tc::mma_commit(bar);
-    }
-    tc::mbar_wait_sleep(bar, phase);
-    phase ^= 1;
-    tc::fence_after_sync();
-
-#pragma unroll
-    for (int layer = 1; layer <= L; ++layer) {
-      epilogue_act<W>(lane_acc, sA, trow, Kp, slope2);
-      tc::fence_async_smem();
-      tc::fence_before_sync();
-      tc::named_sync(bar_id, 128);
-      if (leader) {
-        tc::fence_after_sync();
-        const bool hid = layer < L;
-        // opaque copies keep the descriptors from being hoisted (and held in
-        // registers by every thread) across the tile loop
-        const uint32_t ab = opaque_u32(sAa);
-        const uint32_t wb = opaque_u32(hid ? sWa + off_hidden + (uint32_t)((layer - 1) * W * Kp * 2)
-                                           : sWa + off_head);
-#pragma unroll
-        for (int s = 0; s < Kp / 16; ++s)
-          tc::mma_f16(acc, tc::smem_desc(ab + s * 256, 128, Kp * 16),
-                      tc::smem_desc(wb + s * 256, 128, Kp * 16), hid ? idW : id16, s > 0);
-        tc::mma_commit(bar);
-      }
-      if (layer == L) {
-        // next tile's inputs go in flight under the head MMA of this tile
-        issue_enc<N, ND>(ea, rb, tpos, tdir, tdist, l.R, l.Rd);
-        rb = load_rec(a, t + 2 * stride, trow, n, INNER);
-      }
-      tc::mbar_wait_sleep(bar, phase);
-      phase ^= 1;
-      tc::fence_after_sync();
-    }
-    const float logit = tc::tmem_ld1(lane_acc);
-    if (valid) {
-      if (a.logits) a.logits[row] = logit;
-      if (a.occ && logit < 0.f) a.occ[my_ray] = 1;
-    }
-    tc::fence_before_sync();
-  }
-  __syncthreads();
-  if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
-}
-
-// TPS = tiles in flight per SM the register budget is sized for
-// (8: 64 registers/thread; 6: 80).
-template <int N, int ND, int W, int L, int G, int TPS>
-int launch_tc2(const TcArgs& a, cudaStream_t st) {
-  using C = Tc2<N, ND, W, L, G>;
-  auto kern = query_tc2_kernel<N, ND, W, L, G, TPS>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
-      cudaSuccess)
-    return check_launch("query_tc2: smem attribute");
-  const int per_sm_tmem = 512 / C::COLS;
-  const int per_sm_smem = (int)((228 * 1024) / (C::SMEM + 1024));
-  int per_sm = per_sm_tmem < per_sm_smem ? per_sm_tmem : per_sm_smem;
-  if (per_sm > TPS / G) per_sm = TPS / G;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t max_tiles = (a.cap + kTileRows - 1) / kTileRows;
-  int64_t grid = (int64_t)sm_count() * per_sm;
-  const int64_t need = (max_tiles + G - 1) / G;
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, 128 * G, C::SMEM, st>>>(a);
-  return check_launch("nif_query_dev(tcgen05 specialised)");
-}
-
-// Shared-memory-operand specialisations of the default shapes, kept as
-// measured alternatives (nif_debug_set_query_variant 1 / 9) and checked
-// against the oracle by tests/test_gpu_query_variants.py.
-int launch_tc2_any(const TcArgs& a, const nif_family_view& f, cudaStream_t st, int* rc) {
-  const int W = a.l.W, L = a.l.L;
-  const int tps = g_query_variant == 9 ? 4 : 6;
-  if (f.family == NIF_FAMILY_OUTER && f.N == 3 && W == 64 && L == 2) {
-    *rc = tps == 4 ? launch_tc2<3, 0, 64, 2, 2, 4>(a, st) : launch_tc2<3, 0, 64, 2, 2, 6>(a, st);
-    return 0;
-  }
-  if (f.family == NIF_FAMILY_INNER && f.N == 5 && f.Nd == 3 && W == 48 && L == 3) {
-    *rc = tps == 4 ? launch_tc2<5, 3, 48, 3, 2, 4>(a, st) : launch_tc2<5, 3, 48, 3, 2, 6>(a, st);
-    return 0;
-  }
-  return 1;
-}
-
 
 // ---------------------------------------------------------------------------
 // Split path: standalone grid encoding -> tcgen05 MLP
@@ -2009,11 +1767,7 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
     }
     if (impl != NIF_IMPL_TCGEN05_GENERIC && g_prof == nullptr && g_query_variant != 2) {
       int rc = NIF_OK;
-      if (g_query_variant == 1 || g_query_variant == 9) {
-        if (launch_tc2_any(a, *f, st, &rc) == 0) return rc;
-      } else if (launch_ts_any(a, *f, st, &rc) == 0) {
-        return rc;
-      }
+      if (launch_ts_any(a, *f, st, &rc) == 0) return rc;
     }
     if (f->family == NIF_FAMILY_OUTER && f->N == 3) return launch_tc<3, 0>(a, st);
     if (f->family == NIF_FAMILY_INNER && f->N == 5 && f->Nd == 3) return launch_tc<5, 3>(a, st);

@@ -3,8 +3,8 @@
     python tools/bench_query.py [--train-epochs 0]
 
 Variants (nif_debug_set_query_variant): 0 production (A operand in TMEM);
-1 / 9 shared-memory-operand specialisations (6 / 4 tiles per SM); 2
-runtime-shape generic kernel; 11 TMEM operand, one tile per CTA; "S0" the
+2 runtime-shape generic kernel; 11 TMEM operand, one tile per CTA (6 per
+SM); 12 the round-1 inner configuration (2 CTAs x 3 warpgroups per SM); "S0" the
 split path (encoding kernel + MLP kernel); "P" the fp32 SIMT kernel. Logits of every variant are
 compared with the generic kernel on the same records.
 """
@@ -44,7 +44,7 @@ fams = (("outer", vo, b.outer_obj, b.outer_ray, b.outer_coord, None, b.counts.da
         ("inner", vi, b.inner_obj, b.inner_ray, b.inner_coord, b.inner_r, b.counts.data_ptr() + 8,
          counts[1]))
 ref = {}
-VARIANTS = [(v if v[0] in "SP" else int(v)) for v in sys.argv[1].split(',')] if len(sys.argv) > 1 else [2, 0, 1]
+VARIANTS = [(v if v[0] in "SP" else int(v)) for v in sys.argv[1].split(',')] if len(sys.argv) > 1 else [2, 0, 12]
 if 2 not in VARIANTS:
     VARIANTS = [2] + VARIANTS
 REPS = int(sys.argv[2]) if len(sys.argv) > 2 else 30
