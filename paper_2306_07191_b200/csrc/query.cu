@@ -505,31 +505,58 @@ __device__ __forceinline__ void issue_enc(EncIn<N, ND>& e, const RecIn& r, const
   (void)NP;
 }
 
-__device__ __forceinline__ void acc_h2(uint32_t u, float w, float& a0, float& a1) {
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// one corner's latent pair (fp16x2) times its fp32 weight, accumulated in
+// fp32x2 with one FFMA2 (the same fp32 fma per element as two FFMAs)
+__device__ __forceinline__ void acc_h2(uint32_t u, unsigned long long w2, unsigned long long& a) {
   const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u));
-  a0 = fmaf(w, f.x, a0);
-  a1 = fmaf(w, f.y, a1);
+  a = ffma2(f2pack(f.x, f.y), w2, a);
 }
 
 // corner c of a packed entry: NP=4 -> words (2c, 2c+1) of the entry's 8,
-// NP=8 -> the four words of uint4 c
+// NP=8 -> the four words of uint4 c; acc holds NP/2 packed latent pairs
 template <int NP, int NQ>
-__device__ __forceinline__ void acc_entry(const uint4 (&q)[NQ], const float (&w)[4], float* acc) {
+__device__ __forceinline__ void acc_entry(const uint4 (&q)[NQ], const float (&w)[4],
+                                          unsigned long long* acc) {
   if constexpr (NP == 4) {
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
-      acc_h2(q[i].x, w[2 * i], acc[0], acc[1]);
-      acc_h2(q[i].y, w[2 * i], acc[2], acc[3]);
-      acc_h2(q[i].z, w[2 * i + 1], acc[0], acc[1]);
-      acc_h2(q[i].w, w[2 * i + 1], acc[2], acc[3]);
+      const unsigned long long w0 = f2pack(w[2 * i], w[2 * i]);
+      const unsigned long long w1 = f2pack(w[2 * i + 1], w[2 * i + 1]);
+      acc_h2(q[i].x, w0, acc[0]);
+      acc_h2(q[i].y, w0, acc[1]);
+      acc_h2(q[i].z, w1, acc[0]);
+      acc_h2(q[i].w, w1, acc[1]);
     }
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      acc_h2(q[c].x, w[c], acc[0], acc[1]);
-      acc_h2(q[c].y, w[c], acc[2], acc[3]);
-      acc_h2(q[c].z, w[c], acc[4], acc[5]);
-      acc_h2(q[c].w, w[c], acc[6], acc[7]);
+      const unsigned long long wc = f2pack(w[c], w[c]);
+      acc_h2(q[c].x, wc, acc[0]);
+      acc_h2(q[c].y, wc, acc[1]);
+      acc_h2(q[c].z, wc, acc[2]);
+      acc_h2(q[c].w, wc, acc[3]);
     }
   }
 }
@@ -540,25 +567,29 @@ __device__ __forceinline__ void finish_enc(const EncIn<N, ND>& e, float (&x)[16]
 #pragma unroll
   for (int i = 0; i < 16; ++i) x[i] = 0.f;
   if (e.valid) {
-    float ap[NP], ad[NP];
+    unsigned long long ap[NP / 2], ad[NP / 2];
 #pragma unroll
-    for (int i = 0; i < NP; ++i) ap[i] = ad[i] = 0.f;
+    for (int i = 0; i < NP / 2; ++i) ap[i] = ad[i] = 0ull;  // (+0, +0)
     acc_entry<NP, NQ>(e.qp, e.wp, ap);
     acc_entry<NP, NQ>(e.qd, e.wd, ad);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      x[i] = ap[i];
-      x[N + i] = ad[i];
+      const float2 p2 = f2unpack(ap[i >> 1]), d2 = f2unpack(ad[i >> 1]);
+      x[i] = (i & 1) ? p2.y : p2.x;
+      x[N + i] = (i & 1) ? d2.y : d2.x;
     }
     if constexpr (ND > 0) {
-      float ar[4] = {0.f, 0.f, 0.f, 0.f};
-      const float w0 = 1.f - e.wr, w1 = e.wr;
-      acc_h2(e.qr.x, w0, ar[0], ar[1]);
-      acc_h2(e.qr.y, w0, ar[2], ar[3]);
-      acc_h2(e.qr.z, w1, ar[0], ar[1]);
-      acc_h2(e.qr.w, w1, ar[2], ar[3]);
+      unsigned long long ar[2] = {0ull, 0ull};
+      const unsigned long long w0 = f2pack(1.f - e.wr, 1.f - e.wr), w1 = f2pack(e.wr, e.wr);
+      acc_h2(e.qr.x, w0, ar[0]);
+      acc_h2(e.qr.y, w0, ar[1]);
+      acc_h2(e.qr.z, w1, ar[0]);
+      acc_h2(e.qr.w, w1, ar[1]);
 #pragma unroll
-      for (int i = 0; i < ND; ++i) x[2 * N + i] = ar[i];
+      for (int i = 0; i < ND; ++i) {
+        const float2 r2 = f2unpack(ar[i >> 1]);
+        x[2 * N + i] = (i & 1) ? r2.y : r2.x;
+      }
     }
   }
   x[2 * N + ND] = 1.f;
@@ -740,27 +771,6 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   return y;
 }
 
-__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 f2unpack(unsigned long long r) {
-  float2 v;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-  return v;
-}
-__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
-  unsigned long long r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
-                                                    unsigned long long c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
 
 // Last hidden layer + N=1 head on the CUDA cores: logit = b + sum_k
 // w_k * lrelu(z_k) with z read straight from TMEM (fp32 activations, fp32
