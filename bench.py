@@ -124,8 +124,11 @@ def dist_setup(args):
     if ws > 1:
         import torch.distributed as dist
         backend = "nccl" if args.impl == "ours" else "gloo"
+        # NIF_BENCH_BACKEND=gloo + NIF_BENCH_ONE_GPU=1: every rank on cuda:0 (a
+        # smoke test of the N>1 code path on a one-GPU box; not a measurement)
+        backend = os.environ.get("NIF_BENCH_BACKEND", backend)
         if args.impl == "ours":
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(0 if os.environ.get("NIF_BENCH_ONE_GPU") else local)
         dist.init_process_group(backend)
     elif args.impl == "ours":
         torch.cuda.set_device(0)
@@ -254,7 +257,10 @@ def run_reference(args, rank, ws):
     alone runs and prints; the other ranks exit without work."""
     if rank != 0:
         return
+    # every host thread: torchrun starts its workers with OMP_NUM_THREADS=1,
+    # which the OpenMP runtime has already read
     from oracle import oracle, refscene
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     if args.config == "c1":
         scene = refscene.c1(args.width, args.height)
     elif args.config == "c3":
@@ -521,8 +527,10 @@ def main():
         train_leg = {"epoch_ms": ep_s * 1e3, "optimizer_steps": int(n_steps),
                      "steps_per_s": n_steps / ep_s, "samples": smp.n_outer + smp.n_inner,
                      "spp": 1, "loss": float(curve[-1, 2]),
-                     "mode": (f"data parallel over {ws} GPUs: one NCCL all-reduce per step "
-                              "inside the step graph, fixed-point grid scatter")
+                     "mode": (f"data parallel over {ws} GPUs: one "
+                              f"{torch.distributed.get_backend()} all-reduce per step "
+                              + ("inside the step graph" if torch.distributed.get_backend() == "nccl"
+                                 else "(eager)") + ", fixed-point grid scatter")
                      if ws > 1 else "single GPU: captured 3-launch step per batch"}
         del tm, smp
 

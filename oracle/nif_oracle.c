@@ -786,3 +786,14 @@ int64_t oracle_build_sah(const double* lo, const double* hi, const double* ce, i
   free(right_n);
   return n_nodes;
 }
+
+/* thread count of the following parallel regions (the bench's reference arm
+   runs under torchrun, which starts its workers with OMP_NUM_THREADS=1) */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}

@@ -165,6 +165,11 @@ def max_threads() -> int:
     return int(lib().oracle_max_threads())
 
 
+def set_threads(n: int) -> None:
+    """OpenMP threads of the following oracle calls."""
+    lib().oracle_set_threads(int(n))
+
+
 # ---------------------------------------------------------------------------
 # numpy restatement of the training step
 # ---------------------------------------------------------------------------
