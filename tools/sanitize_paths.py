@@ -1,8 +1,10 @@
 """Small end-to-end exercise of every device path for compute-sanitizer
 (tools/gpu_sanitize.sh): ordered + unordered gather, labels, sample
 collection, one training epoch (tiled fwd/bwd, per-head per-row kernel,
-unit-major Adam), fused / split / bucketed (per_object) queries, the native
-engine, device shading and the GPU SAH build (all three segment classes)."""
+unit-major Adam), the split data-parallel / deterministic training steps
+(exchange buffer, all three grid-scatter modes, ordered MLP reduction),
+fused / split / bucketed (per_object) queries, the native engine, device
+shading and the GPU SAH build (all three segment classes)."""
 import sys
 from pathlib import Path
 
@@ -42,6 +44,25 @@ for sharing in ("shared", "per_object"):
         query_family(model, fam, o, c[:, :w])
         if sharing == "shared":
             query_family(model, fam, o, c[:, :w], split=True)
+# split steps: the sink with the warp-aggregated, fixed-point and sorted
+# scatters (+ ordered MLP partials), eager and graph-replayed
+from paper_2306_07191_b200.train import _GraphStep, _Sink, _Step  # noqa: E402
+cfg = NifConfig(seed=0)
+cfg.outer.grid_resolution = 32
+cfg.inner.grid_resolution = 16
+cfg.outer.batch_size = 256
+cfg.inner.batch_size = 512
+model = build_model(cfg, scene)
+smp = collect_samples(scene, spp=1, seed=scene.seed)
+for which, bs in (("outer", 256), ("inner", 512)):
+    n = getattr(smp, f"n_{which}")
+    for mode, det in ((0, False), (2, False), (1, True)):
+        st = _Step(model, which)
+        sink = _Sink(st, bs, 1, 0, None, deterministic=det, scatter_mode=mode)
+        for cap in (False, True):
+            gs = _GraphStep(st, getattr(smp, f"{which}_obj"), getattr(smp, f"{which}_coord"),
+                            getattr(smp, f"{which}_label"), n, bs, sink, capture=cap)
+            gs.epoch(np.random.default_rng(mode).permutation(n))
 render(c1(32, 24, subdiv=2), config=RenderConfig(spp=1), backend=BvhBackend())
 from paper_2306_07191_b200 import meshgen  # noqa: E402
 from paper_2306_07191_b200.scene import build_bottoms  # noqa: E402
