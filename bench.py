@@ -501,6 +501,40 @@ def main():
         h2d_gbs = max(h2d_gbs, n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9)
     del h2d_src, h2d_dst
 
+    # --- the C4 frame (3840x2160, the same scene) on this one GPU: the N=1
+    # point of the multi-GPU curve, whose N>1 runs split this frame in bands
+    c4_single = None
+    if ws == 1 and args.config == "c2" and not args.profile:
+        import dataclasses
+        cam4 = dataclasses.replace(scene.camera, width=3840, height=2160)
+        d4 = sample_pass_dev(scene, cam4, 0, scene.seed)
+        _, o4, dd4, t4 = shadow_rays_dev(d4, require_emit=False)
+        n4 = int(t4.numel())
+        del d4
+        eng4 = VisibilityEngine(scene, model, n4)
+        eng4.origins[:n4].copy_(o4)
+        eng4.dirs[:n4].copy_(dd4)
+        eng4.tmaxs[:n4].copy_(t4)
+        g4 = eng4.capture(n4)
+        for _ in range(args.warmup):
+            g4.replay()
+        torch.cuda.synchronize()
+        ev4 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for e0, e1 in ev4:
+            flush.fill_(1.0)
+            e0.record(stream)
+            g4.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms4 = float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev4]))
+        c4_single = {"workload": WORKLOADS["c4"].replace(", frame split in row bands across GPUs",
+                                                         ", one GPU"),
+                     "rays_per_frame": n4, "frame_ms": ms4, "value": n4 / (ms4 / 1e3),
+                     "unit": UNIT, "note": "N=1 point of the C4 curve (bench.py under torchrun "
+                                           "splits this frame in N row bands)"}
+        del eng4, g4, o4, dd4, t4
+
     # --- online training: one spp of samples collected
     # band-sharded across the ranks (ordered all-gather into the reference's
     # global order), then one epoch of the reference schedule; under torchrun
@@ -641,6 +675,7 @@ def main():
         # (plus two memset nodes for the gather's counters / scan state)
         "gpu_launches": args.steps * 3,
         "train": train_leg,
+        "c4_single_gpu": c4_single,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line))
