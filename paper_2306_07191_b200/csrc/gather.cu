@@ -250,17 +250,19 @@ __device__ __forceinline__ uint32_t warp_bundle_mask(const RayF& q, bool use_pf,
   const unsigned full = 0xffffffffu;
   const uint32_t vmask = __ballot_sync(full, valid);
   if (n_obj <= 1 || vmask == 0 || !__all_sync(full, use_pf || !valid)) return all_obj;
-  // invalid lanes borrow the first valid lane's ray (neutral for min/max)
-  const int src = __ffs(vmask) - 1;
-  float ox = __shfl_sync(full, q.ox, src), oy = __shfl_sync(full, q.oy, src),
-        oz = __shfl_sync(full, q.oz, src);
-  float ix = __shfl_sync(full, q.ix, src), iy = __shfl_sync(full, q.iy, src),
-        iz = __shfl_sync(full, q.iz, src);
-  float tm = __shfl_sync(full, q.tmax_ru, src);
-  if (valid) {
-    ox = q.ox; oy = q.oy; oz = q.oz;
-    ix = q.ix; iy = q.iy; iz = q.iz;
-    tm = q.tmax_ru;
+  float ox = q.ox, oy = q.oy, oz = q.oz, ix = q.ix, iy = q.iy, iz = q.iz, tm = q.tmax_ru;
+  if (vmask != full) {  // (the last chunk only) invalid lanes borrow the first
+                        // valid lane's ray: neutral for the min/max below
+    const int src = __ffs(vmask) - 1;
+    const float sox = __shfl_sync(full, ox, src), soy = __shfl_sync(full, oy, src),
+                soz = __shfl_sync(full, oz, src), six = __shfl_sync(full, ix, src),
+                siy = __shfl_sync(full, iy, src), siz = __shfl_sync(full, iz, src),
+                stm = __shfl_sync(full, tm, src);
+    if (!valid) {
+      ox = sox; oy = soy; oz = soz;
+      ix = six; iy = siy; iz = siz;
+      tm = stm;
+    }
   }
   const float oxl = wmin(ox), oxh = wmax(ox), oyl = wmin(oy), oyh = wmax(oy);
   const float ozl = wmin(oz), ozh = wmax(oz);
@@ -1024,8 +1026,8 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     }
     const int64_t i = c * 32 + lane;
     const bool valid = i < n;
-    RayX r{};
-    RayF q{};
+    RayX r;  // written for valid lanes; invalid lanes never read their ray
+    RayF q;
     bool use_pf = false;
     if (valid) {
       r.ox = __ldg(org + i * 3 + 0);
