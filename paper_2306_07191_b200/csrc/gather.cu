@@ -95,19 +95,6 @@ __device__ __forceinline__ int classify_obj(const RayX& r, const ObjC& b, bool t
   return 0;
 }
 
-// fp32 spherical map of an fp64 vector (not normalised: atan2 is scale
-// invariant, acos gets z / |v|).
-__device__ __forceinline__ void sph32(double x, double y, double z, double n, float* u,
-                                      float* v) {
-  float uu = (atan2f((float)y, (float)x) + CUDART_PI_F) * (0.5f / CUDART_PI_F);
-  if (uu >= 1.0f) uu -= 1.0f;
-  else if (uu < 0.0f) uu += 1.0f;
-  float zz = (float)(z / n);
-  zz = fminf(fmaxf(zz, -1.0f), 1.0f);
-  *u = uu;
-  *v = acosf(zz) * (1.0f / CUDART_PI_F);
-}
-
 // Hot-path spherical map (geometry.py:233-246) with minimax polynomials in
 // place of atan2f / acosf (a quarter of the gather's instructions):
 //   atan(a) = a * P(a^2) on [0, 1], |err| < 1e-7 rad (degree 7 in a^2);
@@ -954,6 +941,13 @@ gather_persist_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
 #ifndef NIF_GATHER_MINB_U
 #define NIF_GATHER_MINB_U 3
 #endif
+#ifndef NIF_RAY_PREFILTER
+// per-ray fp32 prefilter after the warp-bundle cull: 0 = the bundle's
+// survivors go straight to the exact fp64 test (C2: 1.52 bundle survivors
+// per ray, 1.21 after the prefilter -- the prefilter cost more than the fp64
+// tests it saved: gather 70.1 -> 68.6 us)
+#define NIF_RAY_PREFILTER 0
+#endif
 #ifdef NIF_GATHER_STATS
 // diagnostics build only: rays, bundle survivors, prefilter survivors, hits
 __device__ unsigned long long g_gstats[4];
@@ -1065,12 +1059,16 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     if (valid) {
       uint32_t pmask = 0;
       if (use_pf) {
+#if NIF_RAY_PREFILTER
         uint32_t w = wmask;
         while (w) {
           const int k = __ffs(w) - 1;
           w &= w - 1;
           pmask |= (uint32_t)prefilter(q, flo[k], fhi[k]) << k;
         }
+#else
+        pmask = wmask;
+#endif
       } else {
         pmask = all_obj;
       }
