@@ -21,6 +21,8 @@ from .pipeline import (
     VisibilityEngine, gather_queries, label_visible, oracle_predictor, psnr, psnr_dev, render,
     render_dev, sample_pass, sample_pass_dev, shade_pass_nif, tonemap_srgb8,
 )
+from .parallel import render_band, render_sharded, tile_pixels
+from .train import SampleSet, collect_samples, train, train_batch, train_online
 from .scene import (
     Aabb, AreaLight, BottomLevelBvh, Camera, InnerQuery, OuterQuery, PointLight, QueryRecords,
     Scene, SceneObject, ShadowRays, SphericalCoord, TopLevelBvh, build_bottom, build_top,

@@ -82,7 +82,8 @@ class SampleSet:
 
 def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "importance",
                     labeler=None, seed: Optional[int] = None,
-                    threads: Optional[int] = None, group=None) -> SampleSet:
+                    threads: Optional[int] = None, group=None,
+                    sample_offset: int = 0) -> SampleSet:
     """nif.py:569-674 on the device: per sample index, the primary pass,
     every hit pixel's shadow ray (no cosine filter), the gather in the
     reference's record order and per-object BVH labels (1 = visible).
@@ -94,7 +95,8 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
     band of pixel rows (parallel.tile_pixels) and one ordered all-gather
     per array rebuilds the reference's global order -- sample-major, then
     ray-major across the bands in rank order (nif.py:606-647) -- so every
-    rank ends with the single-process SampleSet."""
+    rank ends with the single-process SampleSet. sample_offset shifts the
+    sample indices (and the ray ids) -- one pass of an online schedule."""
     torch = _torch()
     from .parallel import allgather_ordered, tile_pixels, world_rank
     from .pipeline import gather_sized, sample_pass_dev
@@ -133,7 +135,7 @@ def collect_samples(scene: Scene, camera=None, spp: int = 4, sampler: str = "imp
         tail, dt = tails[k]
         return torch.zeros((0,) + tail, dtype=dt, device=dev)
 
-    for s in range(spp):
+    for s in range(sample_offset, sample_offset + spp):
         got = {}
         data = sample_pass_dev(scene, camera, s, seed,
                                "uniform" if head == "geometry" else sampler, pix0, n_pix)
@@ -433,7 +435,7 @@ _train_batch = train_batch
 
 
 def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional[int] = None,
-          group=None, deterministic: bool = False) -> np.ndarray:
+          group=None, deterministic: bool = False, dp_mode: str = "parity") -> np.ndarray:
     """nif.py:752-795: shuffled mini-batch epochs over both families; loss
     curve (epochs, 3) = outer, inner, combined (NaN for an empty family).
 
@@ -444,7 +446,13 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     gradients | MLP gradients] with a single all-reduce (_Sink), captured
     in the step's CUDA graph under NCCL. deterministic=True makes the
     gradients bit-reproducible run to run: grid cells summed in np.add.at's
-    order after a sort, MLP gradients reduced over CTAs in order."""
+    order after a sort, MLP gradients reduced over CTAs in order.
+
+    dp_mode="parity" (default) keeps the reference's global batch sizes, so
+    W ranks split each batch (the same schedule as one process);
+    dp_mode="throughput" gives every rank a full reference
+    batch -- the global batch is W times the configured size, W times fewer
+    optimiser steps per epoch -- so an epoch's work per GPU shrinks W-fold."""
     torch = _torch()
     if isinstance(samples, dict):
         samples = SampleSet.from_host(samples, device=model.device)
@@ -462,8 +470,11 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     world, rank = world_rank(group)
     import torch.distributed as dist
     epoch_ss = np.random.SeedSequence([seed, 0x7472]).spawn(epochs)
-    bo = model.config.outer.batch_size
-    bi = model.config.inner.batch_size
+    if dp_mode not in ("parity", "throughput"):
+        raise ValueError(f"unknown dp_mode {dp_mode!r}")
+    scale = world if dp_mode == "throughput" else 1
+    bo = model.config.outer.batch_size * scale
+    bi = model.config.inner.batch_size * scale
     steps = {"outer": _Step(model, "outer"), "inner": _Step(model, "inner")}
     on_gpu = model.device.type == "cuda"
     # every full batch is a replay of one captured step: always on one GPU,
@@ -556,3 +567,29 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
         im = sums[1] / counts[1] if counts[1] else math.nan
         curve[e] = (om, im, sums.sum() / counts.sum())
     return curve
+
+
+def train_online(model: NifModel, scene: Scene, spp: int, epochs_per_pass: int = 1,
+                 camera=None, seed: Optional[int] = None, group=None,
+                 deterministic: bool = False, dp_mode: str = "parity"):
+    """Online schedule (north_star "online train step"): for
+    each progressive sample index s, collect that pass's samples on the
+    device (collect_samples(spp=1, sample_offset=s)) and train
+    `epochs_per_pass` epochs on them before the next pass, so the model
+    improves while the frame accumulates. The reference trains after
+    collecting all passes (collect_samples + train, nif.py:569-795); this
+    composes the same two steps per pass. The epochs of pass s draw their
+    permutations from SeedSequence([seed, s]). Returns the per-pass loss
+    curves (spp, epochs_per_pass, 3)."""
+    seed = model.config.seed if seed is None else seed
+    curves = []
+    for s in range(spp):
+        smp = collect_samples(scene, camera, spp=1, seed=scene.seed, group=group,
+                              sample_offset=s)
+        if smp.n_outer == 0 and smp.n_inner == 0:
+            curves.append(np.full((epochs_per_pass, 3), math.nan))
+            continue
+        pass_seed = int(np.random.SeedSequence([seed, s]).generate_state(1)[0])
+        curves.append(train(model, smp, epochs=epochs_per_pass, seed=pass_seed, group=group,
+                            deterministic=deterministic, dp_mode=dp_mode))
+    return np.stack(curves) if curves else np.zeros((0, epochs_per_pass, 3))

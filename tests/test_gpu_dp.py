@@ -229,7 +229,7 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _dp_worker(rank, world, port, out, det):
+def _dp_worker(rank, world, port, out, det, dp_mode="parity"):
     import torch
     import torch.distributed as dist
     from golden_cfg import small_config
@@ -244,7 +244,7 @@ def _dp_worker(rank, world, port, out, det):
         s = build_scene(RECIPES["overlap"])
         smp = collect_samples(s, spp=2, seed=s.seed)
         m = build_model(small_config(), s)
-        curve = train(m, smp, epochs=2, deterministic=det)
+        curve = train(m, smp, epochs=2, deterministic=det, dp_mode=dp_mode)
         arrays = {f"a{i:03d}": a for i, a in enumerate(m.model_arrays())}
         np.savez(os.path.join(out, f"rank{rank}.npz"), curve=curve,
                  **{"s_" + k: v for k, v in smp.host().items()}, **arrays)
@@ -283,6 +283,67 @@ def test_dp_two_ranks_gloo_package_code(det, cuda, golden, scenes):
         close += int(np.sum(np.abs(got - ref) <= 1e-5))
         total += ref.size
     assert close / total >= 0.995, close / total
+
+
+def test_dp_throughput_mode_equals_doubled_batch(cuda, scenes):
+    """dp_mode="throughput": every rank gets a full reference
+    batch, i.e. the global batch is W x the configured size -- the same
+    optimisation as one process with W x larger batches."""
+    import torch.multiprocessing as mp
+    from golden_cfg import small_config
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.train import collect_samples, train
+    world = 2
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_dp_worker, args=(world, _free_port(), out, False, "throughput"),
+                           nprocs=world, join=True, start_method="spawn")
+        res = [dict(np.load(os.path.join(out, f"rank{r}.npz"))) for r in range(world)]
+    for k in res[0]:
+        if k.startswith("a"):
+            assert np.array_equal(res[0][k], res[1][k]), k
+    s = scenes("overlap")
+    smp = collect_samples(s, spp=2, seed=s.seed)
+    cfg = small_config()
+    cfg.outer.batch_size *= world
+    cfg.inner.batch_size *= world
+    m = build_model(cfg, s)
+    curve = train(m, smp, epochs=2)
+    np.testing.assert_allclose(res[0]["curve"], curve, rtol=1e-4)
+    close = total = 0
+    for i, ref in enumerate(m.model_arrays()):
+        got = res[0][f"a{i:03d}"]
+        close += int(np.sum(np.abs(got - ref) <= 1e-5))
+        total += ref.size
+    assert close / total >= 0.995, close / total
+
+
+def test_online_schedule_passes(cuda, golden, scenes):
+    """train_online: pass s collects sample index s (collect_samples with
+    sample_offset -- bit-identical to that pass's part of the reference's
+    2-spp samples) and trains on it; deterministic mode reproduces the
+    explicit collect + train sequence bit for bit."""
+    import numpy as np
+    from paper_2306_07191_b200.train import collect_samples, train, train_online
+    s = scenes("overlap")
+    g = golden("overlap")
+    n_pix = s.camera.width * s.camera.height
+    p1 = collect_samples(s, spp=1, seed=s.seed, sample_offset=1).host()
+    for fam in ("outer", "inner"):
+        sel = g[f"samples_{fam}_ray"] >= n_pix
+        for k in ("obj", "label", "ray"):
+            np.testing.assert_array_equal(p1[f"{fam}_{k}"], g[f"samples_{fam}_{k}"][sel],
+                                          err_msg=f"{fam}_{k}")
+    m1 = _model("overlap", scenes)
+    curves = train_online(m1, s, spp=2, epochs_per_pass=1, deterministic=True)
+    assert curves.shape == (2, 1, 3)
+    m2 = _model("overlap", scenes)
+    for p in range(2):
+        smp = collect_samples(s, spp=1, seed=s.seed, sample_offset=p)
+        ps = int(np.random.SeedSequence([m2.config.seed, p]).generate_state(1)[0])
+        c = train(m2, smp, epochs=1, seed=ps, deterministic=True)
+        np.testing.assert_allclose(curves[p], c, rtol=1e-12)
+    for a, b in zip(m1.model_arrays(), m2.model_arrays()):
+        assert np.array_equal(a, b)
 
 
 def _nccl_worker(rank, port, out):
