@@ -324,7 +324,8 @@ def main():
     n = int(t.numel())
     model = build_model(NifConfig(seed=0, sharing=args.sharing), scene)
     if args.train_epochs > 0:
-        from paper_2306_07191_b200 import train as tr
+        import importlib
+        tr = importlib.import_module("paper_2306_07191_b200.train")
         samples = tr.collect_samples_dev(scene, spp=1, seed=scene.seed)
         tr.train(model, samples, epochs=args.train_epochs)
     eng = VisibilityEngine(scene, model, n)
@@ -543,7 +544,8 @@ def main():
     # graph. Host clock around the synchronous train() call, max over ranks.
     train_leg = None
     if not args.no_train_leg and not args.profile:
-        from paper_2306_07191_b200 import train as tr
+        import importlib
+        tr = importlib.import_module("paper_2306_07191_b200.train")
         smp = tr.collect_samples(scene, spp=1, seed=scene.seed)
         tm = build_model(NifConfig(seed=0, sharing=args.sharing), scene)
         tr.train(tm, smp, epochs=1)  # warm: graph capture, communicators

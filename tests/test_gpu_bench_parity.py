@@ -191,7 +191,8 @@ def test_c2_frame_trained(c2):
     (the north_star "trained" case: logits spread around the decision
     boundary)."""
     from paper_2306_07191_b200 import build_model
-    from paper_2306_07191_b200 import train as tr
+    import importlib
+    tr = importlib.import_module("paper_2306_07191_b200.train")
     from paper_2306_07191_b200.nif import NifConfig
     from paper_2306_07191_b200.pipeline import VisibilityEngine
     scene, (o, d, t) = c2
