@@ -105,8 +105,11 @@ def _hot_path(eng, n):
     return out
 
 
-def _compare(scene, model, rays, hot, min_agree=0.999):
-    """The bars above; returns a summary dict."""
+def _compare(scene, model, rays, hot, min_agree=0.999, cap=np.inf):
+    """The bars above; returns a summary dict. With a finite cap the absolute
+    logit bar applies to the records with |logit_ref| < cap (a long-trained
+    model's large logits carry the fp16 operands' relative error); their
+    largest relative error is reported."""
     from oracle import oracle
     o, d, t = rays
     n = len(t)
@@ -135,10 +138,13 @@ def _compare(scene, model, rays, hot, min_agree=0.999):
         ref_s = ref[o_ref]
         err = np.abs(got - ref_s)
         assert np.abs(ref).mean() > 0.05 or len(ref) == 0, "logits too small to test anything"
-        assert err.max(initial=0.0) <= LOGIT_TOL, (fam, err.max(), err.mean())
+        small = np.abs(ref_s) < cap
+        assert err[small].max(initial=0.0) <= LOGIT_TOL, (fam, err[small].max(), err.mean())
+        big_rel = float((err[~small] / np.abs(ref_s[~small])).max(initial=0.0))
         ref_occ[r_ray[ref < 0.0]] = True
         undecided[r_ray[np.abs(ref) <= LOGIT_TOL]] = True
         summary[fam] = {"records": int(len(ref)), "max_logit_err": float(err.max(initial=0.0)),
+                        "records_above_cap": int((~small).sum()), "max_rel_err_above_cap": big_rel,
                         "mean_abs_logit": float(np.abs(ref).mean()) if len(ref) else 0.0}
     occ = hot["occ"]
     decided = ~undecided
@@ -206,6 +212,36 @@ def test_c2_frame_trained(c2):
     eng.tmaxs[:n].copy_(t)
     hot = _hot_path(eng, n)
     _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
+
+
+def test_c2_frame_trained_long(c2):
+    """A model trained 10 epochs on 4 spp of the frame: logits reach |l| ~ 200.
+    fp16 operands bound the error relative to the layers' magnitudes, so the
+    absolute 2e-2 bar is checked where decisions live -- every record with
+    |l| < 1 -- and the larger logits' relative error is bounded (< 1 %);
+    decided rays bit-identical, agreement >= 99.9 %
+    (profiles/r2_logit_error_by_magnitude.jsonl: up to 0.035 absolute at
+    |l| in [1, 10) on such a model, ~5e-4 relative at |l| ~ 200)."""
+    from paper_2306_07191_b200 import build_model
+    import importlib
+    tr = importlib.import_module("paper_2306_07191_b200.train")
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import VisibilityEngine
+    scene, (o, d, t) = c2
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0), scene)
+    tr.train(model, tr.collect_samples(scene, spp=4, seed=scene.seed), epochs=10)
+    eng = VisibilityEngine(scene, model, n)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    hot = _hot_path(eng, n)
+    rays = (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+    s = _compare(scene, model, rays, hot, cap=1.0)
+    for fam in ("outer", "inner"):
+        assert s[fam]["records"] - s[fam]["records_above_cap"] > 20, fam
+        assert s[fam]["max_rel_err_above_cap"] < 1e-2, (fam, s[fam])
+    assert s["agreement"] >= 0.999
 
 
 def test_c2_drop_in_backend_matches_hot_path(c2):
