@@ -35,6 +35,10 @@ constexpr int kK1 = 16;          // padded layer-1 K (features + bias column)
 // SM hide the MMA round trip better than batching it).
 constexpr int kTpc = 1;
 
+#ifndef NIF_TS_PROF
+#define NIF_TS_PROF 0  // 1: clock64 phase stamps in query_ts_kernel (nif_debug_set_prof)
+#endif
+
 // ---------------------------------------------------------------------------
 // fast blob layout
 // ---------------------------------------------------------------------------
@@ -1243,8 +1247,20 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   const float* headw = reinterpret_cast<const float*>(sW + C::OFF_HEADF);
 
   uint32_t phase = 0;
+#if NIF_TS_PROF  // diagnostic phase stamps (tools/probe_phases.py; costs ~8 %)
+  int it = 0;
+  long long* prof = a.prof;
+#define TS_PROF(k)                                                                     \
+  if (prof != nullptr && trow == 0 && it < 8)                                          \
+    prof[(((int64_t)blockIdx.x * G + wg) * 8 + it) * 16 + (k)] = clock64();
+#define TS_PROF_NEXT() ++it
+#else
+#define TS_PROF(k)
+#define TS_PROF_NEXT()
+#endif
   int cur_obj = -1;
   for (int64_t t = first; t < n_tiles; t += stride) {
+    TS_PROF(0);
     const int64_t row = ea.rec;
     const bool valid = ea.valid;
     const int my_ray = ea.ray;
@@ -1268,8 +1284,10 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
       tc::tmem_st8(lane_a, fv);
     }
     tc::tmem_wait_st();
+    TS_PROF(1);
     tc::fence_before_sync();
     tc::named_sync(bar_id, 128);
+    TS_PROF(2);
     if (leader) {
       tc::fence_after_sync();
       tc::mma_f16_ts(acc, a_op, tc::smem_desc(opaque_u32(sWa), 128, kK1 * 16), idW, 0);
@@ -1282,11 +1300,14 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
     tc::mbar_wait_sleep(bar, phase);
     phase ^= 1;
     tc::fence_after_sync();
+    TS_PROF(3);
 #pragma unroll
     for (int layer = 1; layer < L; ++layer) {
       epilogue_act_tmem<W>(lane_acc, lane_a, slope2);
+      TS_PROF(1 + 3 * layer);
       tc::fence_before_sync();
       tc::named_sync(bar_id, 128);
+      TS_PROF(2 + 3 * layer);
       if (leader) {
         tc::fence_after_sync();
         const uint32_t wb = opaque_u32(sWa + off_hidden + (uint32_t)((layer - 1) * W * Kp * 2));
@@ -1303,6 +1324,7 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
       tc::mbar_wait_sleep(bar, phase);
       phase ^= 1;
       tc::fence_after_sync();
+      TS_PROF(3 + 3 * layer);
     }
     float hout[HD];
     head_simt_n<W, 16, HD>(lane_acc, headw, hout);
@@ -1316,7 +1338,11 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
       }
     }
     tc::fence_before_sync();
+    TS_PROF(15);
+    TS_PROF_NEXT();
   }
+#undef TS_PROF
+#undef TS_PROF_NEXT
   __syncthreads();
   if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
 }
@@ -1775,7 +1801,8 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
         return fail(NIF_ERR_UNSUPPORTED, "no tcgen05 geometry-head kernel for W=%d L=%d", l.W, l.L);
       goto simt;
     }
-    if (impl != NIF_IMPL_TCGEN05_GENERIC && g_prof == nullptr && g_query_variant != 2) {
+    if (impl != NIF_IMPL_TCGEN05_GENERIC && (g_prof == nullptr || NIF_TS_PROF) &&
+        g_query_variant != 2) {
       int rc = NIF_OK;
       if (launch_ts_any(a, *f, st, &rc) == 0) return rc;
     }
