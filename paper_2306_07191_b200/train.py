@@ -434,6 +434,9 @@ def train_batch(model: NifModel, which: str, obj, coord, label) -> float:
 _train_batch = train_batch
 
 
+_FAMILY_GROUPS = {}  # (ranks, backend) -> {family: process group}
+
+
 def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional[int] = None,
           group=None, deterministic: bool = False, dp_mode: str = "parity") -> np.ndarray:
     """nif.py:752-795: shuffled mini-batch epochs over both families; loss
@@ -485,10 +488,14 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
     fam_groups = {}
     if world > 1:
         # one communicator per family: the two families' steps (and their
-        # collectives) run on separate streams, concurrently
+        # collectives) run on separate streams, concurrently; created once
+        # per (ranks, backend) and reused by later train() calls
         ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
-        for which in ("outer", "inner"):
-            fam_groups[which] = dist.new_group(ranks, backend=dist.get_backend(group))
+        key = (tuple(ranks), dist.get_backend(group))
+        if key not in _FAMILY_GROUPS:
+            _FAMILY_GROUPS[key] = {which: dist.new_group(ranks, backend=key[1])
+                                   for which in ("outer", "inner")}
+        fam_groups = _FAMILY_GROUPS[key]
     gsteps = {}
     fams = ((0, bo, "outer", samples.outer_obj, samples.outer_coord, samples.outer_label),
             (1, bi, "inner", samples.inner_obj, samples.inner_coord, samples.inner_label))
