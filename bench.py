@@ -12,13 +12,15 @@ T_inner) -> fused grid encoding + visibility MLP (tcgen05) -> p < 0.5 ->
 per-ray OR. Rays are generated on the GPU by the sample pass (not timed).
 
 Multi-GPU (torchrun, one process per GPU): ONE frame
-split into N equal row bands (parallel.tile_pixels); rank r generates and
-resolves its own band's shadow rays -- no collective on the data path
-(strong scaling, total work = one frame). Default config under torchrun:
-C4 = the C2 scene at 3840x2160 (5.2M shadow rays), so per-GPU bands stay
+cut into 8N row strips dealt round-robin to the ranks
+(parallel.rank_strips; contiguous bands left the top ranks with the ray-less
+sky: tools/band_balance.py); rank r generates its strips' shadow rays and
+resolves them in one pass -- no collective on the data path (strong
+scaling, total work = one frame). Default config under torchrun:
+C4 = the C2 scene at 3840x2160 (5.2M shadow rays), so per-GPU shares stay
 large at 8 GPUs; --config c2 splits the 1080p frame instead.
 
-value : shadow rays of the frame resolved per second (all bands), rays
+value : shadow rays of the frame resolved per second (all ranks), rays
         resident in HBM, L2 flushed (256 MiB write) between steps, CUDA
         events on the launching stream, max over ranks.
 e2e   : the same metric through the drop-in plugin NifBackend.occluded
@@ -57,11 +59,12 @@ WORKLOADS = {
     "c3": ("C3: 24x icosphere(8) + NIF plane, 31,457,282 tris, 25 objects, 1920x1080, "
            "1 spp point-light shadow rays, inference"),
     "c4": ("C4: C2 scene (12x icosphere(6) + NIF plane, 983,042 tris) at 3840x2160, "
-           "1 spp point-light shadow rays, inference, frame split in row bands across GPUs"),
+           "1 spp point-light shadow rays, inference, frame split in row strips across GPUs"),
 }
 RESOLUTION = {"c1": (256, 256), "c2": (1920, 1080), "c3": (1920, 1080), "c4": (3840, 2160)}
 # kernels of one visibility pass (names as ncu reports them) and their
 # algorithmic work: see DESIGN.md section 4
+STRIPS_PER_RANK = 8  # row strips per rank when a frame is split across GPUs
 K_GATHER = "gather_warp_kernel"
 K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4, 0, 1, 0>"
 K_INNER = "query_ts_kernel<5, 3, 48, 3, 1, 4, 0, 1, 1>"
@@ -84,7 +87,8 @@ def config_of(args, ws, n_frame, counts):
             "model": f"NifConfig() defaults (R 256/128, seed 0, random init), "
                      f"sharing={args.sharing}",
             "trained_epochs": args.train_epochs,
-            "parallelism": f"one frame split in {ws} row band(s), one per GPU"}
+            "parallelism": (f"one frame cut in {ws * STRIPS_PER_RANK} row strips dealt "
+                            f"round-robin to {ws} GPUs" if ws > 1 else "one frame, one GPU")}
 
 
 def parse():
@@ -94,7 +98,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4"],
-                   help="default: c2 on one GPU, c4 (4K frame in row bands) under torchrun")
+                   help="default: c2 on one GPU, c4 (4K frame in row strips) under torchrun")
     p.add_argument("--width", type=int, default=None)
     p.add_argument("--height", type=int, default=None)
     p.add_argument("--train-epochs", type=int, default=0,
@@ -314,13 +318,18 @@ def main():
                                                 shadow_rays_dev)
     dev = torch.device("cuda", torch.cuda.current_device())
     scene = build_workload(args, rank, build_device=dev)
-    # this rank's row band of the frame (the whole frame at N=1); the sample
-    # pass keys its RNG by the global pixel index, so the bands' rays are
+    # this rank's row strips of the frame (the whole frame at N=1); the sample
+    # pass keys its RNG by the global pixel index, so the strips' rays are
     # exactly the single-GPU frame's
-    from paper_2306_07191_b200.parallel import tile_pixels
-    pix0, n_pix = tile_pixels(scene.camera.width, scene.camera.height, rank, ws)
-    data = sample_pass_dev(scene, scene.camera, 0, scene.seed, "importance", pix0, n_pix)
-    _, o, d, t = shadow_rays_dev(data, require_emit=False)
+    from paper_2306_07191_b200.parallel import rank_strips
+    parts = []
+    for pix0, n_pix in rank_strips(scene.camera.width, scene.camera.height, rank, ws,
+                                   STRIPS_PER_RANK if ws > 1 else 1):
+        data = sample_pass_dev(scene, scene.camera, 0, scene.seed, "importance", pix0, n_pix)
+        parts.append(shadow_rays_dev(data, require_emit=False)[1:])
+        del data
+    o, d, t = (torch.cat([p_[k] for p_ in parts]) for k in range(3))
+    del parts
     n = int(t.numel())
     model = build_model(NifConfig(seed=0, sharing=args.sharing), scene)
     if args.train_epochs > 0:
@@ -503,7 +512,7 @@ def main():
     del h2d_src, h2d_dst
 
     # --- the C4 frame (3840x2160, the same scene) on this one GPU: the N=1
-    # point of the multi-GPU curve, whose N>1 runs split this frame in bands
+    # point of the multi-GPU curve, whose N>1 runs split this frame in row strips
     c4_single = None
     if ws == 1 and args.config == "c2" and not args.profile:
         import dataclasses
@@ -529,11 +538,11 @@ def main():
             e1.record(stream)
         torch.cuda.synchronize()
         ms4 = float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev4]))
-        c4_single = {"workload": WORKLOADS["c4"].replace(", frame split in row bands across GPUs",
+        c4_single = {"workload": WORKLOADS["c4"].replace(", frame split in row strips across GPUs",
                                                          ", one GPU"),
                      "rays_per_frame": n4, "frame_ms": ms4, "value": n4 / (ms4 / 1e3),
                      "unit": UNIT, "note": "N=1 point of the C4 curve (bench.py under torchrun "
-                                           "splits this frame in N row bands)"}
+                                           "splits this frame in 8N row strips)"}
         del eng4, g4, o4, dd4, t4
 
     # --- online training: one spp of samples collected

@@ -23,6 +23,16 @@ int nif_debug_set_prof_gather(void* buf);
 int nif_debug_set_gather_variant(int v);
 /* CTAs per SM of the hot-path gather / fused query grids (0: default) */
 int nif_debug_set_gather_grid(int ctas_per_sm);
+/* Hot-path gather: this many of each warp's static chunk rounds are handed
+ * out on demand instead (one atomic per chunk).                        */
+int nif_debug_set_gather_dynamic(int rounds);
+/* Diagnostic timelines (%globaltimer, ns) of the hot-path kernels, NULL to
+ * disable: gather buf[warp][4] = entry, after the prologue, exit, chunks;
+ * fused tcgen05 query buf[cta * G + warpgroup][5] = entry, after the grid
+ * dependency wait, after the first tile, exit, tiles.                   */
+int nif_debug_set_timeline_gather(void* buf);
+
+int nif_debug_set_timeline_query(void* buf);
 int nif_debug_set_query_grid(int ctas_per_sm);
 /* Culling statistics of the hot-path gather since the last call (rays,
  * bundle survivors, prefilter survivors, classified hits); only in a

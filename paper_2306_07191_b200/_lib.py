@@ -161,6 +161,9 @@ _SIGS = {
     "nif_debug_set_prof_gather": (C.c_int, [P]),
     "nif_debug_set_gather_variant": (C.c_int, [C.c_int]),
     "nif_debug_set_gather_grid": (C.c_int, [C.c_int]),
+    "nif_debug_set_gather_dynamic": (C.c_int, [C.c_int]),
+    "nif_debug_set_timeline_gather": (C.c_int, [C.c_void_p]),
+    "nif_debug_set_timeline_query": (C.c_int, [C.c_void_p]),
     "nif_debug_set_query_grid": (C.c_int, [C.c_int]),
     "nif_debug_set_query_variant": (C.c_int, [C.c_int]),
     "nif_debug_set_train_variant": (C.c_int, [C.c_int]),

@@ -958,7 +958,8 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
                    const double* __restrict__ org, const double* __restrict__ dir,
                    const double* __restrict__ tms, int64_t n, nif_gather_out out,
                    unsigned long long* __restrict__ reserve, unsigned int* __restrict__ done,
-                   unsigned int* __restrict__ tail) {
+                   unsigned int* __restrict__ tail, unsigned long long* __restrict__ deg_acc,
+                   int dyn_rounds, unsigned long long* __restrict__ tl) {
   __shared__ ObjC objs[kMaxObjFused];
   __shared__ float4 flo[kMaxObjFused], fhi[kMaxObjFused];
   __shared__ float s_absmax;
@@ -970,6 +971,12 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int n_obj = s.n_obj;
+  // diagnostic timeline (nif_debug_set_timeline_gather): per warp entry,
+  // after the prologue, exit, chunks processed
+  unsigned long long* wtl =
+      tl != nullptr && lane == 0 ? tl + ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 4 : nullptr;
+  if (wtl) wtl[0] = globaltimer();
+  int n_done = 0;
   if (tid == 0) s_absmax = 0.f;
   __syncthreads();
   if (tid < n_obj) {
@@ -1007,7 +1014,8 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
   // remainder is handed out one chunk at a time on demand, so warps that
   // drew cheap chunks absorb the tail instead of idling
   const int64_t wid = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-  const int64_t rounds = n_chunks / nw;
+  const int64_t rounds = max((int64_t)0, n_chunks / nw - dyn_rounds);
+  if (wtl) wtl[1] = globaltimer();
   for (int64_t k = 0;; ++k) {
     int64_t c;
     if (k < rounds) {
@@ -1018,6 +1026,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       c = rounds * nw + __shfl_sync(0xffffffffu, t, 0);
       if (c >= n_chunks) break;
     }
+    ++n_done;
     const int64_t i = c * 32 + lane;
     const bool valid = i < n;
     RayX r;  // written for valid lanes; invalid lanes never read their ray
@@ -1123,12 +1132,11 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     base = __shfl_sync(0xffffffffu, base, 0);
     const int64_t base_o = (int64_t)(base >> 32);
     const int64_t base_i = (int64_t)(base & 0xffffffffull);
-    if (mask == 0) continue;
     const int excl = incl - packed;
     int64_t jo = base_o + (excl >> 16);
     int64_t ji = base_i + (excl & 0xffff);
-    float du, dv;
-    sph32f((float)r.dx, (float)r.dy, (float)r.dz, 1.0f, &du, &dv);
+    float du = 0.f, dv = 0.f;
+    if (mask != 0) sph32f((float)r.dx, (float)r.dy, (float)r.dz, 1.0f, &du, &dv);
     uint64_t m = mask;
     while (m != 0) {
       const int bit = __ffsll((long long)m) - 1;
@@ -1172,8 +1180,11 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     }
   }
   const int dsum = __reduce_add_sync(0xffffffffu, deg_count);
-  if (lane == 0 && dsum)
-    atomicAdd((unsigned long long*)(out.counts + 3), (unsigned long long)dsum);
+  if (lane == 0 && dsum) atomicAdd(deg_acc, (unsigned long long)dsum);
+  if (wtl) {
+    wtl[2] = globaltimer();
+    wtl[3] = (unsigned long long)n_done;
+  }
   // the last CTA to finish publishes the queue lengths
   __shared__ bool s_last;
   __threadfence();
@@ -1185,11 +1196,14 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     out.counts[0] = (int64_t)(v >> 32);
     out.counts[1] = (int64_t)(v & 0xffffffffull);
     out.counts[2] = out.counts[0] + out.counts[1];
+    out.counts[3] = (int64_t)atomicAdd(deg_acc, 0ull);
   }
 }
 
 long long* g_gprof = nullptr;  // diagnostic phase stamps (nif_debug_set_prof_gather)
 int g_gather_cpsm = 0;     // CTAs per SM of the hot-path gather grid (0: NIF_GATHER_MINB_U)
+int g_gather_dyn = 0;      // static rounds of the hot-path gather handed out on demand instead
+unsigned long long* g_tl_gather = nullptr;  // nif_debug_set_timeline_gather
 int g_gather_variant = 0;  // 0 unordered warp chunks, 1 one tile per CTA, 2 persistent ordered
 
 size_t fused_ws(int64_t n) {
@@ -1202,9 +1216,15 @@ size_t fused_ws(int64_t n) {
 
 using namespace nif;
 
+// Workspace: a fixed header [0, kGatherHdr) -- the hot-path kernel's
+// counters (reservation, CTA done, degenerate sum; the remainder-chunk tail
+// on its own line), zeroed by every call -- then the per-variant scratch
+// (look-back status words / two-pass buffers).
+constexpr size_t kGatherHdr = 256;
+
 extern "C" size_t nif_gather_workspace_bytes(int64_t n) {
   const size_t a = gather_two_pass_workspace(n), b = fused_ws(n);
-  return a > b ? a : b;
+  return kGatherHdr + (a > b ? a : b);
 }
 
 extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
@@ -1218,46 +1238,55 @@ extern "C" int nif_gather_dev(const nif_scene_view* s, const uint8_t* route,
   if (workspace_bytes < nif_gather_workspace_bytes(n))
     return fail(NIF_ERR_VALUE, "gather workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  cudaMemsetAsync(out->counts, 0, 4 * sizeof(int64_t), st);
-  if (n == 0) return check_launch("gather(empty)");
-  if (s->n_obj > kMaxObjFused)
-    return gather_two_pass(s, route, origins, dirs, tmaxs, n, out, workspace, workspace_bytes,
-                           st);
-  const int64_t tiles = (n + kThreads - 1) / kThreads;
-  uint8_t* ws = (uint8_t*)workspace;
-  unsigned long long* status = (unsigned long long*)ws;
-  int* ctr = (int*)(ws + align_up((size_t)tiles * 8, 256));
+  uint8_t* hdr = (uint8_t*)workspace;
+  uint8_t* ws = hdr + kGatherHdr;
+  const size_t ws_bytes = workspace_bytes - kGatherHdr;
   const bool unordered = out->rec_kind == nullptr && g_gprof == nullptr && g_gather_variant == 0;
-  if (!unordered) cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
-  else cudaMemsetAsync(ctr, 0, 16, st);  // reservation, done and tail counters
-  if (out->rec_kind != nullptr)
-    gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
-        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
-  else if (g_gprof != nullptr || g_gather_variant == 1)
-    gather_fused_kernel<false><<<(unsigned)tiles, kThreads, 0, st>>>(
-        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
-  else if (g_gather_variant == 0) {
+  const bool warp_path = n > 0 && s->n_obj <= kMaxObjFused && unordered;
+  // the hot-path kernel writes all four counts itself
+  if (!warp_path) cudaMemsetAsync(out->counts, 0, 4 * sizeof(int64_t), st);
+  cudaMemsetAsync(hdr, 0, kGatherHdr, st);
+  int rc = NIF_OK;
+  if (n == 0) {
+    rc = check_launch("gather(empty)");
+  } else if (s->n_obj > kMaxObjFused) {
+    rc = gather_two_pass(s, route, origins, dirs, tmaxs, n, out, ws, ws_bytes, st);
+  } else if (warp_path) {
     const int64_t chunks = (n + 31) / 32;
     int64_t grid = (int64_t)sm_count() * (g_gather_cpsm > 0 ? g_gather_cpsm : NIF_GATHER_MINB_U);
     if (grid * (kThreads / 32) > chunks) grid = (chunks + kThreads / 32 - 1) / (kThreads / 32);
     gather_warp_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
-        *s, route, origins, dirs, tmaxs, n, *out, (unsigned long long*)ctr,
-        (unsigned int*)((unsigned long long*)ctr + 1),
-        (unsigned int*)((unsigned long long*)ctr + 1) + 1);
+        *s, route, origins, dirs, tmaxs, n, *out, (unsigned long long*)hdr,
+        (unsigned int*)(hdr + 8), (unsigned int*)(hdr + 128), (unsigned long long*)(hdr + 16),
+        g_gather_dyn, g_tl_gather);
+    rc = check_launch("nif_gather_dev");
   } else {
-    const int smem = kStages * kStageBytes;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gather_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem);
-      attr = true;
+    const int64_t tiles = (n + kThreads - 1) / kThreads;
+    unsigned long long* status = (unsigned long long*)ws;
+    int* ctr = (int*)(ws + align_up((size_t)tiles * 8, 256));
+    cudaMemsetAsync(ws, 0, align_up((size_t)tiles * 8, 256) + 256, st);
+    if (out->rec_kind != nullptr)
+      gather_fused_kernel<true><<<(unsigned)tiles, kThreads, 0, st>>>(
+          *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
+    else if (g_gprof != nullptr || g_gather_variant == 1)
+      gather_fused_kernel<false><<<(unsigned)tiles, kThreads, 0, st>>>(
+          *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles, g_gprof);
+    else {
+      const int smem = kStages * kStageBytes;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(gather_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem);
+        attr = true;
+      }
+      int64_t grid = (int64_t)sm_count() * NIF_GATHER_MINB;
+      if (grid > tiles) grid = tiles;
+      gather_persist_kernel<<<(unsigned)grid, kThreads, smem, st>>>(
+          *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
     }
-    int64_t grid = (int64_t)sm_count() * NIF_GATHER_MINB;
-    if (grid > tiles) grid = tiles;
-    gather_persist_kernel<<<(unsigned)grid, kThreads, smem, st>>>(
-        *s, route, origins, dirs, tmaxs, n, *out, status, ctr, tiles);
+    rc = check_launch("nif_gather_dev");
   }
-  return check_launch("nif_gather_dev");
+  return rc;
 }
 
 extern "C" int nif_debug_set_prof_gather(void* buf) {
@@ -1275,6 +1304,16 @@ extern "C" int nif_debug_gather_stats(unsigned long long* out) {
   (void)out;
   return fail(NIF_ERR_UNSUPPORTED, "built without NIF_GATHER_STATS");
 #endif
+}
+
+extern "C" int nif_debug_set_timeline_gather(void* buf) {
+  g_tl_gather = (unsigned long long*)buf;
+  return NIF_OK;
+}
+
+extern "C" int nif_debug_set_gather_dynamic(int rounds) {
+  g_gather_dyn = rounds < 0 ? 0 : rounds;
+  return NIF_OK;
 }
 
 extern "C" int nif_debug_set_gather_grid(int ctas_per_sm) {

@@ -344,9 +344,14 @@ struct TcArgs {
   const int32_t* perm;      // [tile * 128 + row] -> record index, -1 = padding
   const int32_t* tile_obj;  // [tile] -> object (= head)
   const int64_t* n_tiles;   // device count of bucketed tiles
+  // diagnostic timeline (nif_debug_set_timeline), or NULL: per warpgroup
+  // globaltimer at entry, after the grid dependency wait, after the first
+  // tile, at exit, and the tile count
+  unsigned long long* tl;
 };
 
 long long* g_prof = nullptr;
+unsigned long long* g_tl_query = nullptr;
 int g_query_variant = 0;  // nif_debug_set_query_variant
 int g_query_cpsm = 0;     // CTAs per SM cap of the fused query grids (0: TMEM/occupancy bound)
 
@@ -1191,6 +1196,9 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   const __half* tpos = reinterpret_cast<const __half*>(a.blob + l.off_pos);
   const __half* tdir = reinterpret_cast<const __half*>(a.blob + l.off_dir);
   const __half* tdist = reinterpret_cast<const __half*>(a.blob + l.off_dist);
+  unsigned long long* tl =
+      a.tl != nullptr && trow == 0 ? a.tl + ((int64_t)blockIdx.x * G + wg) * 5 : nullptr;
+  if (tl) tl[0] = globaltimer();
   // prologue first (barriers, weights -> smem, TMEM): under programmatic
   // dependent launch it overlaps the tail of the gather that fills the queues
   if (tid == 0) {
@@ -1204,6 +1212,7 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
   }
   if (tid < 32) tc::tmem_alloc<C::COLS>(tslot);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the queues are final from here
+  if (tl) tl[1] = globaltimer();
   const int64_t n = min(*a.count, a.cap);
   int64_t n_tiles, stride, first;
   if constexpr (PO) {  // contiguous tile range per warpgroup (objects change rarely)
@@ -1340,9 +1349,14 @@ __global__ void __launch_bounds__(128 * G, TPS / G) query_ts_kernel(TcArgs a) {
     tc::fence_before_sync();
     TS_PROF(15);
     TS_PROF_NEXT();
+    if (tl && t == first) tl[2] = globaltimer();
   }
 #undef TS_PROF
 #undef TS_PROF_NEXT
+  if (tl) {
+    tl[3] = globaltimer();
+    tl[4] = (unsigned long long)(n_tiles > first ? (n_tiles - first + stride - 1) / stride : 0);
+  }
   __syncthreads();
   if (tid < 32) tc::tmem_dealloc(*tslot, C::COLS);
 }
@@ -1794,6 +1808,7 @@ extern "C" int nif_query_dev(const nif_family_view* f, const int32_t* obj, const
     if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
     TcArgs a{(const uint8_t*)f->fast, l, obj, ray, coord4, r, count_dev, capacity, occ_ray,
              logits, g_prof};
+    a.tl = g_tl_query;
     if (l.HD != 1) {  // geometry head: the TMEM-operand kernel only
       int rc = NIF_OK;
       if (launch_ts_any(a, *f, st, &rc) == 0) return rc;
@@ -1913,6 +1928,11 @@ extern "C" int nif_debug_set_query_grid(int ctas_per_sm) {
 
 extern "C" int nif_debug_set_query_variant(int v) {
   g_query_variant = v;
+  return NIF_OK;
+}
+
+extern "C" int nif_debug_set_timeline_query(void* buf) {
+  g_tl_query = (unsigned long long*)buf;
   return NIF_OK;
 }
 

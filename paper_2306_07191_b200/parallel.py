@@ -39,6 +39,31 @@ def tile_pixels(width: int, height: int, rank: int, world: int) -> Tuple[int, in
     return y0 * width, (y1 - y0) * width
 
 
+def rank_strips(width: int, height: int, rank: int, world: int,
+                strips_per_rank: int = 1) -> List[Tuple[int, int]]:
+    """Pixel ranges [(pix0, n_pix), ...] owned by `rank` when the frame is
+    cut into world * strips_per_rank row strips dealt round-robin (strip s
+    to rank s mod world). strips_per_rank=1 is `tile_pixels`' contiguous
+    band; more strips spread every rank over the whole image height, so
+    the ranks' shares of costly regions (and of ray-less sky) even out.
+    Ranges are in increasing pixel order; touching strips are merged."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    if strips_per_rank < 1:
+        raise ValueError("strips_per_rank must be >= 1")
+    ns = world * strips_per_rank
+    out: List[Tuple[int, int]] = []
+    for s in range(rank, ns, world):
+        y0, y1 = band(height, s, ns)
+        if y1 == y0:
+            continue
+        if out and out[-1][0] + out[-1][1] == y0 * width:
+            out[-1] = (out[-1][0], out[-1][1] + (y1 - y0) * width)
+        else:
+            out.append((y0 * width, (y1 - y0) * width))
+    return out
+
+
 def world_rank(group=None) -> Tuple[int, int]:
     """(world, rank) of `group` (1, 0 without torch.distributed)."""
     import torch.distributed as dist

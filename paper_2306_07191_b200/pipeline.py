@@ -302,21 +302,7 @@ class VisibilityEngine:
         return n
 
     def run(self, n: int, stream=None):
-        L = _lib.lib()
-        sp = _lib.stream_ptr(stream)
-        torch = _torch()
-        b = self.buf
-        gather_dev(self.ds, self.route, self.origins, self.dirs, self.tmaxs, n, b, stream)
-        if self.model is None:
-            return
-        vo, vi = self._family_views()
-        p = _lib.ptr
-        # the two families are independent: outer on a side stream, inner on
-        # the main one, joined before returning (fork/join is graph-capturable)
-        main = stream if stream is not None else torch.cuda.current_stream()
-        self.side.wait_stream(main)
-        self._query(vo, vi, p(self.occ), self.side.cuda_stream, sp)
-        main.wait_stream(self.side)
+        self.run_range(0, n, stream)
 
     def overflowed(self) -> bool:
         """Did the last run emit more records than the queues hold? (syncs)"""
@@ -357,10 +343,13 @@ class VisibilityEngine:
         L = _lib.lib()
         torch = _torch()
         n = s1 - s0
-        if n <= 0:
+        if n < 0 or (n == 0 and s0 > 0):
             return
         b = self.buf
         sp = _lib.stream_ptr(stream)
+        vo = vi = None
+        if self.model is not None:
+            vo, vi = self._family_views()  # (re)pack before the gather is queued
         out = _lib.GatherOut.from_buffer_copy(b.out)
         out.bvh_occ = b.bvh_occ.data_ptr() + s0
         L.nif_gather_dev(self.ds.view, _lib.ptr(self.route), self.origins.data_ptr() + 24 * s0,
@@ -368,9 +357,10 @@ class VisibilityEngine:
                          _lib.ptr(b.workspace), b.workspace.numel(), sp)
         if self.model is None:
             return
-        vo, vi = self._family_views()
         occ = self.occ.data_ptr() + s0
         main = stream if stream is not None else torch.cuda.current_stream()
+        # the two families are independent: outer on a side stream, inner on
+        # the main one, joined before returning (fork/join is graph-capturable)
         self.side.wait_stream(main)
         self._query(vo, vi, occ, self.side.cuda_stream, sp)
         main.wait_stream(self.side)

@@ -18,7 +18,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2306_07191_b200.parallel import band, tile_pixels
+from paper_2306_07191_b200.parallel import band, rank_strips, tile_pixels
 
 
 def test_band_partition_exact():
@@ -31,6 +31,27 @@ def test_band_partition_exact():
             assert seen == list(range(n))
     total = sum(tile_pixels(1920, 1080, r, 8)[1] for r in range(8))
     assert total == 1920 * 1080
+
+
+def test_rank_strips_partition_exact():
+    for wd, ht in ((7, 5), (64, 33), (3840, 2160)):
+        for w in (1, 2, 3, 8):
+            for k in (1, 2, 8):
+                seen = np.zeros(wd * ht, np.int32)
+                for r in range(w):
+                    strips = rank_strips(wd, ht, r, w, k)
+                    if k == 1:
+                        assert strips == [tile_pixels(wd, ht, r, w)] or strips == []
+                    for (a, m), nxt in zip(strips, strips[1:] + [None]):
+                        assert m > 0 and a % wd == 0 and m % wd == 0
+                        if nxt is not None:
+                            assert a + m < nxt[0]  # increasing, touching strips merged
+                        seen[a:a + m] += 1
+                assert (seen == 1).all(), (wd, ht, w, k)
+    # every rank reaches into every part of the frame's height
+    for r in range(8):
+        ys = [a // 3840 for a, _ in rank_strips(3840, 2160, r, 8, 8)]
+        assert min(ys) < 2160 // 8 and max(ys) >= 2160 * 7 // 8
 
 
 def _free_port():

@@ -223,6 +223,52 @@ def test_render_bands_union_is_single_gpu_frame(cuda, scenes):
             assert torch.equal(got, full), (type(backend).__name__, world)
 
 
+def test_rank_strips_union_is_single_gpu_frame(cuda):
+    """bench.py's multi-GPU split: each rank's round-robin row strips, one
+    visibility pass over their concatenated rays; scattered back to pixel
+    order the per-ray answers equal the single-pass frame's bit for bit."""
+    import dataclasses
+
+    import torch
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.parallel import rank_strips
+    from paper_2306_07191_b200.pipeline import (VisibilityEngine, sample_pass_dev,
+                                                shadow_rays_dev)
+    from paper_2306_07191_b200.synthetic import c2
+    scene = c2()
+    cam = dataclasses.replace(scene.camera, width=480, height=270)
+    model = build_model(NifConfig(seed=0), scene)
+
+    def answers(strips):
+        occ, pix = [], []
+        rays = []
+        for pix0, n_pix in strips:
+            data = sample_pass_dev(scene, cam, 0, scene.seed, "importance", pix0, n_pix)
+            m, o, d, t = shadow_rays_dev(data, require_emit=False)
+            rays.append((o, d, t))
+            pix.append(pix0 + m.nonzero().squeeze(1))
+        o, d, t = (torch.cat([r[k] for r in rays]) for k in range(3))
+        n = int(t.numel())
+        eng = VisibilityEngine(scene, model, max(n, 1))
+        eng.origins[:n].copy_(o)
+        eng.dirs[:n].copy_(d)
+        eng.tmaxs[:n].copy_(t)
+        eng.checked_run(n)
+        return torch.cat(pix), eng.occ[:n].clone()
+
+    pix_full, occ_full = answers([(0, cam.width * cam.height)])
+    assert int(occ_full.sum()) > 0 and int((occ_full == 0).sum()) > 0
+    for world, k in ((2, 8), (4, 8), (3, 5)):
+        got = torch.full((cam.width * cam.height,), 2, dtype=torch.uint8, device="cuda")
+        want = got.clone()
+        want[pix_full] = occ_full
+        for r in range(world):
+            pix, occ = answers(rank_strips(cam.width, cam.height, r, world, k))
+            got[pix] = occ
+        assert torch.equal(got, want), (world, k)
+
+
 def _free_port():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
