@@ -128,6 +128,9 @@ typedef struct nif_gather_out {
   int64_t* counts;      /* [4]: n_outer, n_inner, n_total, n_degenerate */
 } nif_gather_out;
 
+/* The workspace (nif_gather_workspace_bytes) must be zero-filled before its
+ * first use and not shared by concurrent gathers: the hot-path kernel keeps
+ * its counters in it and re-arms them itself (no memset per call).     */
 size_t nif_gather_workspace_bytes(int64_t n_rays);
 int nif_gather_dev(const nif_scene_view* scene, const uint8_t* route_dev,
                    const double* origins, const double* dirs, const double* tmaxs,

@@ -400,6 +400,11 @@ extern "C" int nif_engine_create(const nif_scene_view* scene, const uint8_t* rou
     release(e);
     return rc;
   }
+  // the gather workspace starts zero-filled (its hot-path counters re-arm)
+  if (cudaMemset(e->workspace, 0, e->ws_bytes) != cudaSuccess) {
+    release(e);
+    return nif::fail(NIF_ERR_CUDA, "engine: workspace memset failed");
+  }
   // a shadow ray meets only a few network-routed boxes; start at 4 slots per
   // ray (C2: 1.16 records per ray) and grow on overflow
   if ((rc = alloc_queues(e, std::min(e->n_net, 4)))) {

@@ -77,7 +77,8 @@ class GatherBuffers:
             self.rec_ray = torch.empty(cap, **i32)
             self.rec_coord = torch.empty(cap * 5, dtype=torch.float64, device=device)
         ws = _lib.lib().nif_gather_workspace_bytes(max(n, 1))
-        self.workspace = torch.empty(ws, dtype=torch.uint8, device=device)
+        # zero-filled once: the hot-path gather keeps its counters re-armed
+        self.workspace = torch.zeros(ws, dtype=torch.uint8, device=device)
         p = _lib.ptr
         self.out = _lib.GatherOut(
             outer_obj=p(self.outer_obj), outer_ray=p(self.outer_ray),

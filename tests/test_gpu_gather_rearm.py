@@ -1,0 +1,47 @@
+"""The hot-path gather keeps its reservation / completion counters in the
+caller's workspace and re-arms them itself (no memset node per call): a
+workspace reused across gathers of different sizes, overflowing queues,
+empty batches and the ordered variant in between must give exactly the
+counts and per-ray answers of a fresh workspace every time.
+"""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reused_workspace_counts_match_fresh(cuda):
+    import torch
+    from paper_2306_07191_b200 import _lib
+    from paper_2306_07191_b200.pipeline import (GatherBuffers, gather_dev, sample_pass_dev,
+                                                shadow_rays_dev)
+    from paper_2306_07191_b200.synthetic import c2
+    scene = c2()
+    ds = scene.device()
+    data = sample_pass_dev(scene, scene.camera, 0, scene.seed)
+    _, o, d, t = shadow_rays_dev(data, require_emit=False)
+    route = scene.nif_route_mask(None)
+    rd = ds.route(route)
+    n_net = int(route.sum())
+    N = int(t.numel())
+    shared = GatherBuffers(N, n_net, ds.device, slots=2)
+    tiny = GatherBuffers(N, n_net, ds.device, slots=1)  # overflows on dense blocks
+    L = _lib.lib()
+    plan = [(N, 0), (1000, 0), (0, 0), (250000, 1), (77, 0), (N, 0), (4096, 0)]
+    for n, variant in plan:
+        a = (N - n) // 2
+        oo, dd, tt = o[a:a + n], d[a:a + n], t[a:a + n]
+        fresh = GatherBuffers(max(n, 1), n_net, ds.device, slots=2)
+        gather_dev(ds, rd, oo, dd, tt, n, fresh)
+        L.nif_debug_set_gather_variant(variant)
+        try:
+            gather_dev(ds, rd, oo, dd, tt, n, shared)
+            gather_dev(ds, rd, oo, dd, tt, n, tiny)
+        finally:
+            L.nif_debug_set_gather_variant(0)
+        torch.cuda.synchronize()
+        want = fresh.counts.cpu().tolist()
+        assert shared.counts.cpu().tolist() == want, (n, variant)
+        assert tiny.counts.cpu().tolist() == want, (n, variant)  # true totals despite overflow
+        if n:
+            assert torch.equal(shared.bvh_occ[:n], fresh.bvh_occ[:n])
