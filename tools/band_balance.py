@@ -8,7 +8,7 @@ rows to ranks:
   contiguous   rank r owns rows band(H, r, N)                (round-2 bench)
   interleaved  the frame cut in N*K row strips, rank r owns strips r, r+N, ...
 
-    python tools/band_balance.py [width height] [K] -> JSON lines
+    python tools/band_balance.py [width height] [K] [scene c2|c3] -> JSON lines
 """
 import json
 import sys
@@ -23,15 +23,16 @@ from paper_2306_07191_b200.nif import NifConfig  # noqa: E402
 from paper_2306_07191_b200.parallel import band, rank_strips  # noqa: E402
 from paper_2306_07191_b200.pipeline import (VisibilityEngine, sample_pass_dev,  # noqa: E402
                                             shadow_rays_dev)
-from paper_2306_07191_b200.synthetic import c2  # noqa: E402
+from paper_2306_07191_b200 import synthetic  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 2 else 3840
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 2160
 K = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+SCENE = sys.argv[4] if len(sys.argv) > 4 else "c2"
 torch.cuda.set_device(0)
 import dataclasses  # noqa: E402
 
-scene = c2()
+scene = getattr(synthetic, SCENE)(build_device=torch.device("cuda", 0))
 cam = dataclasses.replace(scene.camera, width=W, height=H)
 model = build_model(NifConfig(seed=0), scene)
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
@@ -74,7 +75,8 @@ def frame_ms(strips, steps=20):
 
 
 t1, n1, occ1 = frame_ms([(0, W * H)])
-print(json.dumps({"frame": f"{W}x{H}", "n_gpus": 1, "frame_ms": t1, "rays": n1}), flush=True)
+print(json.dumps({"scene": SCENE, "frame": f"{W}x{H}", "n_gpus": 1, "frame_ms": t1, "rays": n1}),
+      flush=True)
 for N in (2, 4, 8):
     for mode in ("contiguous", "interleaved"):
         per = []
@@ -88,7 +90,7 @@ for N in (2, 4, 8):
         ms = [p[0] for p in per]
         rays = [p[1] for p in per]
         assert sum(rays) == n1 and sum(p[2] for p in per) == occ1
-        print(json.dumps({"frame": f"{W}x{H}", "n_gpus": N, "mode": mode,
+        print(json.dumps({"scene": SCENE, "frame": f"{W}x{H}", "n_gpus": N, "mode": mode,
                           "strips_per_rank": 1 if mode == "contiguous" else K,
                           "band_ms": [round(x, 4) for x in ms], "rays": rays,
                           "max_ms": max(ms), "mean_ms": float(np.mean(ms)),
