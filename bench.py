@@ -502,7 +502,7 @@ def main():
         h2d_dst.copy_(h2d_src, non_blocking=True)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h2d_gbs = 0.0
-    for _ in range(3):  # best of three trials of five copies (the link is noisy)
+    for _ in range(8):  # best of eight trials of five copies (the link is noisy)
         c0.record(stream)
         for _ in range(5):
             h2d_dst.copy_(h2d_src, non_blocking=True)
