@@ -219,7 +219,8 @@ int nif_query_split_dev(const nif_family_view* f, const int32_t* obj, const int3
  * (padding rows inert) inside scratch (nif_bucket_scratch_bytes), then the
  * TMEM-operand kernel runs each tile with its object's weights. Same
  * outputs as nif_query_dev; without bucketing per-object MLPs run on the
- * SIMT kernel.                                                         */
+ * SIMT kernel. The scratch must be zero-filled before its first use and
+ * not shared by concurrent calls (the histogram is re-zeroed in place). */
 size_t nif_bucket_scratch_bytes(int64_t capacity, int32_t n_obj);
 int nif_query_bucketed_dev(const nif_family_view* f, const int32_t* obj, const int32_t* ray,
                            const float* coord4, const float* r, const int64_t* count_dev,

@@ -337,6 +337,10 @@ int alloc_queues(nif_engine* e, int64_t slots_per_ray) {
   if (e->outer.n_heads > 1) {
     const size_t nb = nif_bucket_scratch_bytes(cap, e->outer.n_obj);
     if ((rc = dev_alloc(&e->bucket[0], nb)) || (rc = dev_alloc(&e->bucket[1], nb))) return rc;
+    // zero-filled once: the bucketed query re-zeroes its histogram itself
+    if (cudaMemset(e->bucket[0], 0, nb) != cudaSuccess ||
+        cudaMemset(e->bucket[1], 0, nb) != cudaSuccess)
+      return nif::fail(NIF_ERR_CUDA, "engine: bucket scratch memset failed");
   }
   uint8_t* q = (uint8_t*)e->queues;
   auto carve = [&](size_t bytes) {

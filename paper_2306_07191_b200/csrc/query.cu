@@ -1664,6 +1664,10 @@ __device__ void bucket_scan_block(const BucketWs& w, int n_obj) {
          p += blockDim.x)
       w.perm[p] = -1;
   }
+  __syncthreads();
+  // the histogram is consumed: re-zero it for the next call (no memset
+  // node in front of the histogram kernel; the scratch starts zero-filled)
+  for (int o = threadIdx.x; o < n_obj; o += blockDim.x) w.hist[o] = 0;
   (void)s_off;
 }
 
@@ -1863,8 +1867,7 @@ extern "C" int nif_query_bucketed_dev(const nif_family_view* f, const int32_t* o
   if (!l.tc_ok) return fail(NIF_ERR_UNSUPPORTED, "configuration not covered by the tcgen05 kernels");
   if (!f->fast) return fail(NIF_ERR_VALUE, "tcgen05 path needs nif_fast_pack_dev first");
   cudaStream_t st = (cudaStream_t)stream;
-  const BucketWs w = bucket_ws(scratch, capacity, f->n_obj);
-  cudaMemsetAsync(w.hist, 0, (size_t)f->n_obj * 4, st);
+  const BucketWs w = bucket_ws(scratch, capacity, f->n_obj);  // hist zero on entry
   int64_t blocks = (capacity + 255) / 256;
   const int64_t cap_blocks = (int64_t)sm_count() * 8;
   if (blocks > cap_blocks) blocks = cap_blocks;

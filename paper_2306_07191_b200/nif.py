@@ -511,7 +511,7 @@ def query_family(model: NifModel, which: str, obj, coord, impl: int = _lib.IMPL_
     if fam.n_heads > 1 and impl in (_lib.IMPL_AUTO, _lib.IMPL_TCGEN05) and not split:
         # per_object sharing: bucket by object, then the tensor-core kernel
         L = _lib.lib()
-        scratch = torch.empty(int(L.nif_bucket_scratch_bytes(m, fam.n_obj)), dtype=torch.uint8,
+        scratch = torch.zeros(int(L.nif_bucket_scratch_bytes(m, fam.n_obj)), dtype=torch.uint8,
                               device=dev)
         L.nif_query_bucketed_dev(fam.view(with_fast=True), _lib.ptr(d_obj), _lib.ptr(d_ray),
                                  _lib.ptr(d_c4), _lib.ptr(d_r), _lib.ptr(d_cnt), m, None,

@@ -279,8 +279,9 @@ class VisibilityEngine:
         if self.model is not None and self.model.outer.n_heads > 1:
             L = _lib.lib()
             nb = int(L.nif_bucket_scratch_bytes(self.buf.cap, self.model.outer.n_obj))
-            self.bucket = (torch.empty(nb, dtype=torch.uint8, device=dev),
-                           torch.empty(nb, dtype=torch.uint8, device=dev))
+            # zero-filled once: the bucketed query re-zeroes its histogram
+            self.bucket = (torch.zeros(nb, dtype=torch.uint8, device=dev),
+                           torch.zeros(nb, dtype=torch.uint8, device=dev))
         self.graphs = {}
 
     def _family_views(self):

@@ -45,3 +45,33 @@ def test_reused_workspace_counts_match_fresh(cuda):
         assert tiny.counts.cpu().tolist() == want, (n, variant)  # true totals despite overflow
         if n:
             assert torch.equal(shared.bvh_occ[:n], fresh.bvh_occ[:n])
+
+
+def test_bucketed_query_scratch_reused_across_sizes(cuda):
+    """per_object sharing: the bucketed query re-zeroes its histogram in
+    the scratch itself; passes of different sizes through one engine equal
+    fresh engines' answers."""
+    import torch
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import VisibilityEngine, sample_pass_dev, shadow_rays_dev
+    from paper_2306_07191_b200.synthetic import c2
+    scene = c2()
+    data = sample_pass_dev(scene, scene.camera, 0, scene.seed)
+    _, o, d, t = shadow_rays_dev(data, require_emit=False)
+    model = build_model(NifConfig(seed=0, sharing="per_object"), scene)
+    N = int(t.numel())
+    eng = VisibilityEngine(scene, model, N)
+    eng.origins.copy_(o)
+    eng.dirs.copy_(d)
+    eng.tmaxs.copy_(t)
+    for n in (N, 5000, 0, 300000, N):
+        eng.checked_run(n)
+        torch.cuda.synchronize()
+        fresh = VisibilityEngine(scene, model, max(n, 1))
+        fresh.origins[:n].copy_(o[:n])
+        fresh.dirs[:n].copy_(d[:n])
+        fresh.tmaxs[:n].copy_(t[:n])
+        fresh.checked_run(n)
+        assert torch.equal(eng.occ[:n], fresh.occ[:n]), n
+    assert int(eng.occ[:N].sum()) > 0
