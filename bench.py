@@ -682,9 +682,11 @@ def main():
                 "h2d_peak_gbs": h2d_gbs,
                 "h2d_frac": (n * 56 * args.steps / (e2e_ms / 1e3) / 1e9) / h2d_gbs,
                 "pinned_torch_value": n_total * args.steps / (pinned_ms / 1e3)},
-        # per step: gather_fused, query_tc outer (side stream), query_tc inner
-        # (plus two memset nodes for the gather's counters / scan state)
-        "gpu_launches": args.steps * 3,
+        # per step: gather_warp_kernel, query_ts_kernel outer (side stream) and
+        # inner (no memset nodes: the gather re-arms its own counters); the
+        # per_object mode adds the bucketing kernels (histogram, scan, scatter)
+        # of both families
+        "gpu_launches": args.steps * (3 + (6 if args.sharing == "per_object" else 0)),
         "train": train_leg,
         "c4_single_gpu": c4_single,
         "clocks": clocks.summary(),
