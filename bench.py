@@ -448,6 +448,25 @@ def main():
         render_ms[name] = e0.elapsed_time(e1) / 5
     del nif_be
 
+    # the e2e roofline: pinned host -> device copy bandwidth of this box,
+    # measured before the plugin's staging threads exist (they are
+    # spinning copy workers; measured after them the copy reads ~half),
+    # measured on the same stream with one copy of a step's input bytes
+    h2d_src = torch.empty(n * 56, dtype=torch.uint8).pin_memory()
+    h2d_dst = torch.empty(n * 56, dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        h2d_dst.copy_(h2d_src, non_blocking=True)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d_gbs = 0.0
+    for _ in range(8):  # best of eight trials of five copies (the link is noisy)
+        c0.record(stream)
+        for _ in range(5):
+            h2d_dst.copy_(h2d_src, non_blocking=True)
+        c1.record(stream)
+        c1.synchronize()
+        h2d_gbs = max(h2d_gbs, n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9)
+    del h2d_src, h2d_dst
+
     # --- e2e through the drop-in plugin: NifBackend.occluded (the reference's
     # PredictorBackend.occluded, renderer.py:675-683) on pageable numpy rays,
     # answered through the native engine's C-ABI (pinned staging ring,
@@ -494,22 +513,6 @@ def main():
         e1.record(stream)
     torch.cuda.synchronize()
     pinned_ms = float(np.sum([e0.elapsed_time(e1) for e0, e1 in p_evs]))
-    # the e2e roofline: pinned host -> device copy bandwidth of this box,
-    # measured on the same stream with one copy of a step's input bytes
-    h2d_src = torch.empty(n * 56, dtype=torch.uint8).pin_memory()
-    h2d_dst = torch.empty(n * 56, dtype=torch.uint8, device=dev)
-    for _ in range(2):
-        h2d_dst.copy_(h2d_src, non_blocking=True)
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    h2d_gbs = 0.0
-    for _ in range(8):  # best of eight trials of five copies (the link is noisy)
-        c0.record(stream)
-        for _ in range(5):
-            h2d_dst.copy_(h2d_src, non_blocking=True)
-        c1.record(stream)
-        c1.synchronize()
-        h2d_gbs = max(h2d_gbs, n * 56 * 5 / (c0.elapsed_time(c1) / 1e3) / 1e9)
-    del h2d_src, h2d_dst
 
     # --- the C4 frame (3840x2160, the same scene) on this one GPU: the N=1
     # point of the multi-GPU curve, whose N>1 runs split this frame in row strips
