@@ -821,10 +821,17 @@ __device__ __forceinline__ float head_simt(uint32_t taddr, const float* __restri
 template <int W, int CH, int HD>
 __device__ __forceinline__ void head_simt_n(uint32_t taddr, const float* __restrict__ hw,
                                             float (&out)[HD]) {
-  unsigned long long acc[HD];
+  // leaky(x) = A x + B |x| (A = (1 + slope) / 2, B = (1 - slope) / 2), so
+  // w . leaky(z) = A (w . z) + B (w . |z|): one packed FFMA2 per pair for
+  // the linear sum and one FFMA per element with the |.| operand modifier,
+  // instead of the product, max and FFMA of max(z, slope z)
+  unsigned long long lin[HD];
+  float mag[HD], mag2[HD];  // two partial sums: shorter dependent chains
 #pragma unroll
-  for (int j = 0; j < HD; ++j) acc[j] = f2pack(hw[HD * W + j], 0.f);
-  const unsigned long long slope = f2pack(kSlope, kSlope);
+  for (int j = 0; j < HD; ++j) {
+    lin[j] = 0ull;
+    mag[j] = mag2[j] = 0.f;
+  }
 #pragma unroll
   for (int g0 = 0; g0 < W; g0 += CH) {
     uint32_t r[CH];
@@ -835,25 +842,25 @@ __device__ __forceinline__ void head_simt_n(uint32_t taddr, const float* __restr
 #pragma unroll
     for (int c = 0; c < CH; c += 4) {
       if (c >= gw) break;
-      const unsigned long long z01 = f2pack(__uint_as_float(r[c]), __uint_as_float(r[c + 1]));
-      const unsigned long long z23 = f2pack(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
-      const float2 t01 = f2unpack(fmul2(z01, slope)), t23 = f2unpack(fmul2(z23, slope));
-      const unsigned long long a01 =
-          f2pack(fmaxf(__uint_as_float(r[c]), t01.x), fmaxf(__uint_as_float(r[c + 1]), t01.y));
-      const unsigned long long a23 = f2pack(fmaxf(__uint_as_float(r[c + 2]), t23.x),
-                                            fmaxf(__uint_as_float(r[c + 3]), t23.y));
+      const float z0 = __uint_as_float(r[c]), z1 = __uint_as_float(r[c + 1]);
+      const float z2 = __uint_as_float(r[c + 2]), z3 = __uint_as_float(r[c + 3]);
 #pragma unroll
       for (int j = 0; j < HD; ++j) {
         const float4 w4 = *reinterpret_cast<const float4*>(hw + j * W + g0 + c);
-        acc[j] = ffma2(a01, f2pack(w4.x, w4.y), acc[j]);
-        acc[j] = ffma2(a23, f2pack(w4.z, w4.w), acc[j]);
+        lin[j] = ffma2(f2pack(z0, z1), f2pack(w4.x, w4.y), lin[j]);
+        lin[j] = ffma2(f2pack(z2, z3), f2pack(w4.z, w4.w), lin[j]);
+        mag[j] = fmaf(fabsf(z0), w4.x, mag[j]);
+        mag2[j] = fmaf(fabsf(z1), w4.y, mag2[j]);
+        mag[j] = fmaf(fabsf(z2), w4.z, mag[j]);
+        mag2[j] = fmaf(fabsf(z3), w4.w, mag2[j]);
       }
     }
   }
+  constexpr float kA = 0.5f * (1.0f + kSlope), kB = 0.5f * (1.0f - kSlope);
 #pragma unroll
   for (int j = 0; j < HD; ++j) {
-    const float2 s = f2unpack(acc[j]);
-    out[j] = s.x + s.y;
+    const float2 s = f2unpack(lin[j]);
+    out[j] = fmaf(kB, mag[j] + mag2[j], fmaf(kA, s.x + s.y, hw[HD * W + j]));
   }
 }
 
