@@ -392,6 +392,30 @@ def test_online_schedule_passes(cuda, golden, scenes):
         assert np.array_equal(a, b)
 
 
+def test_train_reuses_captured_graphs_across_calls(cuda, scenes):
+    """A second train() call on the same samples replays the step graphs
+    the first call captured (no recapture), with results bit-identical to a
+    recapture (deterministic mode); other samples or settings recapture."""
+    from paper_2306_07191_b200.train import collect_samples, train
+    s = scenes("overlap")
+    smp = collect_samples(s, spp=1, seed=s.seed)
+    m1 = _model("overlap", scenes)
+    train(m1, smp, epochs=1, deterministic=True)
+    g1 = {k: v[2] for k, v in m1._train_graphs.items()}
+    c1 = train(m1, smp, epochs=1, deterministic=True)
+    assert all(m1._train_graphs[k][2] is g1[k] for k in g1)  # replayed, not recaptured
+    m2 = _model("overlap", scenes)
+    train(m2, smp, epochs=1, deterministic=True)
+    m2._train_graphs.clear()
+    c2 = train(m2, smp, epochs=1, deterministic=True)
+    np.testing.assert_allclose(c1, c2, rtol=1e-12)  # loss sums: fp64 atomics
+    for a, b in zip(m1.model_arrays(), m2.model_arrays()):
+        assert np.array_equal(a, b)  # parameters: bit for bit
+    other = collect_samples(s, spp=1, seed=s.seed, sample_offset=1)
+    train(m1, other, epochs=1, deterministic=True)
+    assert all(m1._train_graphs[k][2] is not g1[k] for k in g1)
+
+
 def _nccl_worker(rank, port, out):
     import torch
     import torch.distributed as dist
