@@ -570,11 +570,99 @@ __device__ __forceinline__ void acc_entry(const uint4 (&q)[NQ], const float (&w)
   }
 }
 
+#ifndef NIF_INTERP_FHFMA
+// 1: interpolation with the mixed-precision FMA (f16 latent x f16 weight +
+// f32 accumulator, one FHFMA per latent: no separate f16 -> f32 conversion
+// and no work on the padding latents): C2 pass -1.3 us, but the bilinear
+// weights rounded to f16 grow the logit error ~1.5x (1-epoch model: 0.0088
+// vs 0.0066 max, 10-epoch |l| < 1: 0.009 vs 0.004); 0 (default): convert
+// the latent pairs and interpolate with fp32 weights (FFMA2)
+#define NIF_INTERP_FHFMA 0
+#endif
+
+// d = h(a) * h(b) + c with f16 operands taken from the low (L) / high (H)
+// halves of two 32-bit registers; the f16 x f16 product is exact in fp32
+#define NIF_FHFMA(NAME, AS, BS)                                                      \
+  __device__ __forceinline__ float NAME(uint32_t a2, uint32_t b2, float c) {         \
+    float d;                                                                         \
+    asm("{.reg .f16 a0, a1, b0, b1;\n\t"                                            \
+        "mov.b32 {a0, a1}, %1;\n\t"                                                  \
+        "mov.b32 {b0, b1}, %2;\n\t"                                                  \
+        "fma.rn.f32.f16 %0, " AS ", " BS ", %3;}"                                     \
+        : "=f"(d) : "r"(a2), "r"(b2), "f"(c));                                      \
+    return d;                                                                        \
+  }
+NIF_FHFMA(fhfma_ll, "a0", "b0")
+NIF_FHFMA(fhfma_lh, "a0", "b1")
+NIF_FHFMA(fhfma_hl, "a1", "b0")
+NIF_FHFMA(fhfma_hh, "a1", "b1")
+#undef NIF_FHFMA
+
+// latent i (0..7) of a corner held in words (w0, w1, w2, w3), times the
+// weight in half `wh` (0 low, 1 high) of the f16 pair `wp`, into acc
+__device__ __forceinline__ float fh_latent(int i, uint32_t w0, uint32_t w1, uint32_t w2,
+                                           uint32_t w3, uint32_t wp, int wh, float acc) {
+  const uint32_t word = i < 2 ? w0 : i < 4 ? w1 : i < 6 ? w2 : w3;
+  if (i & 1) return wh ? fhfma_hh(word, wp, acc) : fhfma_hl(word, wp, acc);
+  return wh ? fhfma_lh(word, wp, acc) : fhfma_ll(word, wp, acc);
+}
+
+// the N real latents of one 2-D lookup (corner-packed entry; corner c's
+// weight w[c] in f16), accumulated in fp32 over the corners in order
+template <int N, int NP, int NQ>
+__device__ __forceinline__ void fh_entry(const uint4 (&q)[NQ], const float (&w)[4],
+                                         float (&acc)[8]) {
+  const uint32_t wa = h2u(__floats2half2_rn(w[0], w[1]));
+  const uint32_t wb = h2u(__floats2half2_rn(w[2], w[3]));
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t wp = c < 2 ? wa : wb;
+    uint32_t w0, w1, w2 = 0u, w3 = 0u;
+    if constexpr (NP == 4) {  // corner c: words (2c, 2c + 1) of the 8
+      const uint4& u = q[c >> 1];
+      w0 = (c & 1) ? u.z : u.x;
+      w1 = (c & 1) ? u.w : u.y;
+    } else {
+      w0 = q[c].x;
+      w1 = q[c].y;
+      w2 = q[c].z;
+      w3 = q[c].w;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = fh_latent(i, w0, w1, w2, w3, wp, c & 1, acc[i]);
+  }
+}
+
 template <int N, int ND>
 __device__ __forceinline__ void finish_enc(const EncIn<N, ND>& e, float (&x)[16]) {
   constexpr int NP = EncIn<N, ND>::NP, NQ = EncIn<N, ND>::NQ;
 #pragma unroll
   for (int i = 0; i < 16; ++i) x[i] = 0.f;
+#if NIF_INTERP_FHFMA
+  if (e.valid) {
+    float ap[8], ad[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ap[i] = ad[i] = 0.f;
+    fh_entry<N, NP, NQ>(e.qp, e.wp, ap);
+    fh_entry<N, NP, NQ>(e.qd, e.wd, ad);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      x[i] = ap[i];
+      x[N + i] = ad[i];
+    }
+    if constexpr (ND > 0) {  // 1-D distance pair: corner 0 in words x, y; corner 1 in z, w
+      const uint32_t wr = h2u(__floats2half2_rn(1.f - e.wr, e.wr));
+#pragma unroll
+      for (int i = 0; i < ND; ++i) {
+        float a = fh_latent(i, e.qr.x, e.qr.y, 0u, 0u, wr, 0, 0.f);
+        a = fh_latent(i, e.qr.z, e.qr.w, 0u, 0u, wr, 1, a);
+        x[2 * N + i] = a;
+      }
+    }
+  }
+  x[2 * N + ND] = 1.f;
+  return;
+#endif
   if (e.valid) {
     unsigned long long ap[NP / 2], ad[NP / 2];
 #pragma unroll
