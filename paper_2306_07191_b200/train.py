@@ -435,6 +435,7 @@ _train_batch = train_batch
 
 
 _FAMILY_GROUPS = {}  # (ranks, backend) -> {family: process group}
+_GRAPH_CACHE_MAX_SAMPLES = 1 << 24  # train(): captured step graphs kept up to this family size
 
 
 def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional[int] = None,
@@ -568,7 +569,14 @@ def train(model: NifModel, samples, epochs: Optional[int] = None, seed: Optional
                             if world > 1:  # communicator set up outside any capture
                                 dist.all_reduce(sink.comm, group=fam_groups[which])
                         gsteps[which] = _GraphStep(st, obj, coord, label, n, bs, sink, capture)
-                        cache[which] = (key, st, gsteps[which])
+                        # small sample sets only: a cached entry keeps its
+                        # sample-sized permutation buffers (8 B/sample on the
+                        # device + 16 B pinned) alive with the model; for
+                        # large sets the one-off capture is negligible anyway
+                        if n <= _GRAPH_CACHE_MAX_SAMPLES:
+                            cache[which] = (key, st, gsteps[which])
+                        else:
+                            cache.pop(which, None)
                 st = steps[which]
                 st.sq.zero_()
                 gsteps[which].epoch(perms[fam])
