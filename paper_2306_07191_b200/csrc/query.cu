@@ -1719,7 +1719,6 @@ inline BucketWs bucket_ws(void* scratch, int64_t capacity, int n_obj) {
 // tile offsets (exclusive scan of padded counts), tile -> object, and the
 // -1 padding rows of each object's last tile; run by one block
 __device__ void bucket_scan_block(const BucketWs& w, int n_obj) {
-  __shared__ int64_t s_off;
   if (n_obj <= 32) {  // one warp: lane o scans object o (no serial chain)
     if (threadIdx.x < 32) {
       const int o = threadIdx.x;
@@ -1748,7 +1747,6 @@ __device__ void bucket_scan_block(const BucketWs& w, int n_obj) {
     }
     w.tile_off[n_obj] = off;
     *w.n_tiles = off;
-    s_off = off;
   }
   __syncthreads();
   for (int o = 0; o < n_obj; ++o) {
@@ -1763,7 +1761,6 @@ __device__ void bucket_scan_block(const BucketWs& w, int n_obj) {
   // the histogram is consumed: re-zero it for the next call (no memset
   // node in front of the histogram kernel; the scratch starts zero-filled)
   for (int o = threadIdx.x; o < n_obj; o += blockDim.x) w.hist[o] = 0;
-  (void)s_off;
 }
 
 __global__ void bucket_hist_kernel(const int32_t* __restrict__ obj,
