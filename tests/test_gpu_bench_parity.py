@@ -1,8 +1,9 @@
 """Parity at the configurations the bench line is quoted on (VERDICT r1,
 "next" #1): the bench's own C2 frame -- 12 x icosphere(6) + NIF plane, 13
 objects, default NifConfig (R 256/128), 1920x1080, 1.31M shadow rays --
-and a strided sample of a C3 frame (24 x icosphere(8) + plane, 31.5M
-triangles), run through the hot path (VisibilityEngine: unordered fp32
+a strided sample of a C3 frame (24 x icosphere(8) + plane, 31.5M
+triangles) and one rank's share of the C4 frame (4K, round-robin row strips
+of an 8-GPU split), run through the hot path (VisibilityEngine: unordered fp32
 gather queues -> fused tcgen05 encode+MLP -> per-ray OR) and compared with
 the oracle's restatement of the reference path on the same rays:
 
@@ -300,6 +301,37 @@ def test_c3_strided_sample(cuda):
     hot = _hot_path(eng, n)
     s = _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
     assert s["rays"] > 60_000
+
+
+def test_c4_rank_share(cuda):
+    """C4 (the C2 scene at 3840x2160) as bench.py splits it under torchrun:
+    one rank's round-robin row strips of an 8-GPU run (64 strips), their
+    concatenated shadow rays in one pass, against the oracle."""
+    import dataclasses
+
+    import torch
+    from paper_2306_07191_b200 import build_model, synthetic
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.parallel import rank_strips
+    from paper_2306_07191_b200.pipeline import (VisibilityEngine, sample_pass_dev,
+                                                shadow_rays_dev)
+    scene = synthetic.c2(build_device=cuda)
+    cam = dataclasses.replace(scene.camera, width=3840, height=2160)
+    parts = []
+    for pix0, n_pix in rank_strips(cam.width, cam.height, 3, 8, 8):
+        data = sample_pass_dev(scene, cam, 0, scene.seed, "importance", pix0, n_pix)
+        parts.append(shadow_rays_dev(data, require_emit=False)[1:])
+    o, d, t = (torch.cat([p_[k] for p_ in parts]) for k in range(3))
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0), scene)
+    _randomize(model, seed=5)
+    eng = VisibilityEngine(scene, model, n)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    hot = _hot_path(eng, n)
+    s = _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
+    assert s["rays"] > 500_000
 
 
 def test_queue_overflow_regrows(cuda):
