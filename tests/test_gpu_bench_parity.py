@@ -93,10 +93,15 @@ def _hot_path(eng, n):
     for fam, v, k, co in (("outer", vo, 0, 0), ("inner", vi, 1, 8)):
         m = int(cnt[k])
         logit = torch.empty(max(m, 1), dtype=torch.float32, device=eng.ds.device)
-        L.nif_query_dev(v, p(getattr(b, f"{fam}_obj")), p(getattr(b, f"{fam}_ray")),
-                        p(getattr(b, f"{fam}_coord")), p(b.inner_r) if fam == "inner" else None,
-                        b.counts.data_ptr() + co, b.cap, None, p(logit), _lib.IMPL_AUTO,
-                        _lib.stream_ptr())
+        r_ptr = p(b.inner_r) if fam == "inner" else None
+        if eng.bucket is not None:  # per_object: the bucketed tensor-core query, as in the pass
+            L.nif_query_bucketed_dev(v, p(getattr(b, f"{fam}_obj")), p(getattr(b, f"{fam}_ray")),
+                                     p(getattr(b, f"{fam}_coord")), r_ptr, b.counts.data_ptr() + co,
+                                     b.cap, None, p(logit), p(eng.bucket[k]), _lib.stream_ptr())
+        else:
+            L.nif_query_dev(v, p(getattr(b, f"{fam}_obj")), p(getattr(b, f"{fam}_ray")),
+                            p(getattr(b, f"{fam}_coord")), r_ptr, b.counts.data_ptr() + co,
+                            b.cap, None, p(logit), _lib.IMPL_AUTO, _lib.stream_ptr())
         coord = getattr(b, f"{fam}_coord")[:4 * m].view(m, 4).cpu().numpy()
         if fam == "inner":
             coord = np.concatenate([coord, b.inner_r[:m].cpu().numpy()[:, None]], axis=1)
@@ -134,7 +139,18 @@ def _compare(scene, model, rays, hot, min_agree=0.999, cap=np.inf):
         _check_coords(r_coord[o_ref], h["coord"][o_hot], fam)
         f = _oracle_family(model, fam)
         x = oracle.encode(f["pos"], f["dir"], f["dist"], r_obj, r_coord)
-        ref = oracle.dense_forward(f["w"], f["b"], f["dims"], x, sigmoid_head=0)[:, 0]
+        heads = model.host_layers(fam)
+        if len(heads) == 1:
+            ref = oracle.dense_forward(f["w"], f["b"], f["dims"], x, sigmoid_head=0)[:, 0]
+        else:  # per_object sharing: each record through its object's MLP (nif.py:380-397)
+            ref = np.zeros(len(x))
+            for ob in np.unique(r_obj):
+                sel_o = r_obj == ob
+                hl = heads[int(ob)]
+                ref[sel_o] = oracle.dense_forward(
+                    np.concatenate([a.reshape(-1) for a, _ in hl]),
+                    np.concatenate([bb for _, bb in hl]), f["dims"], x[sel_o],
+                    sigmoid_head=0)[:, 0]
         got = h["logit"][o_hot].astype(np.float64)
         ref_s = ref[o_ref]
         err = np.abs(got - ref_s)
@@ -243,6 +259,27 @@ def test_c2_frame_trained_long(c2):
         assert s[fam]["records"] - s[fam]["records_above_cap"] > 20, fam
         assert s[fam]["max_rel_err_above_cap"] < 1e-2, (fam, s[fam])
     assert s["agreement"] >= 0.999
+
+
+def test_c2_frame_per_object(c2):
+    """sharing="per_object" (one MLP per object, the bucketed tensor-core
+    query) on the bench's C2 frame with O(1) logits, against the oracle
+    running each record through its own object's MLP."""
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import VisibilityEngine
+    scene, (o, d, t) = c2
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0, sharing="per_object"), scene)
+    assert model.outer.n_heads > 1
+    _randomize(model, seed=7)
+    eng = VisibilityEngine(scene, model, n)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    assert eng.bucket is not None
+    hot = _hot_path(eng, n)
+    _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
 
 
 def test_c2_drop_in_backend_matches_hot_path(c2):
