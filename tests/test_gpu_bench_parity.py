@@ -282,6 +282,47 @@ def test_c2_frame_per_object(c2):
     _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
 
 
+def test_c2_frame_geometry_head(c2):
+    """head="geometry" (4-wide identity output, nif.py:445-464) on the
+    tensor cores for the C2 frame's queue: every raw output within 2e-2 of
+    the oracle's dense forward (O(1) latents and biases)."""
+    import torch
+    from oracle import oracle
+    from paper_2306_07191_b200 import _lib, build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import GatherBuffers, gather_dev
+    scene, (o, d, t) = c2
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0, head="geometry"), scene)
+    _randomize(model, seed=11)
+    ds = scene.device()
+    route = scene.nif_route_mask(None)
+    buf = GatherBuffers(n, int(route.sum()), ds.device, slots=4)
+    gather_dev(ds, ds.route(route), o, d, t, n, buf)
+    cnt = buf.counts.cpu().numpy()
+    L, p = _lib.lib(), _lib.ptr
+    for fam, k, co, width in (("outer", 0, 0, 4), ("inner", 1, 8, 5)):
+        m = int(cnt[k])
+        v = model.family(fam).view(with_fast=True)
+        out = torch.empty((max(m, 1), 4), dtype=torch.float32, device=ds.device)
+        L.nif_query_dev(v, p(getattr(buf, f"{fam}_obj")), p(getattr(buf, f"{fam}_ray")),
+                        p(getattr(buf, f"{fam}_coord")), p(buf.inner_r) if fam == "inner" else None,
+                        buf.counts.data_ptr() + co, buf.cap, None, p(out), _lib.IMPL_TCGEN05,
+                        _lib.stream_ptr())
+        obj = getattr(buf, f"{fam}_obj")[:m].cpu().numpy().astype(np.int64)
+        coord = getattr(buf, f"{fam}_coord")[:4 * m].view(m, 4).cpu().numpy().astype(np.float64)
+        if fam == "inner":
+            coord = np.concatenate([coord, buf.inner_r[:m].cpu().numpy()[:, None]], axis=1)
+        f = _oracle_family(model, fam)
+        x = oracle.encode(f["pos"], f["dir"], f["dist"], obj, coord[:, :width])
+        ref = oracle.dense_forward(f["w"], f["b"], f["dims"], x, sigmoid_head=0)
+        got = out[:m].cpu().numpy().astype(np.float64)
+        assert m > 100_000 and ref.shape == got.shape == (m, 4)
+        assert np.abs(ref).mean() > 0.05
+        err = np.abs(got - ref).max()
+        assert err <= LOGIT_TOL, (fam, err)
+
+
 def test_c2_drop_in_backend_matches_hot_path(c2):
     """NifBackend.occluded (the reference-named plugin: numpy rays through
     the native engine's pinned staging, C-ABI) returns the hot path's bits,
