@@ -111,7 +111,7 @@ def _hot_path(eng, n):
     return out
 
 
-def _compare(scene, model, rays, hot, min_agree=0.999, cap=np.inf):
+def _compare(scene, model, rays, hot, min_agree=0.999, cap=np.inf, hybrid_threshold=None):
     """The bars above; returns a summary dict. With a finite cap the absolute
     logit bar applies to the records with |logit_ref| < cap (a long-trained
     model's large logits carry the fp16 operands' relative error); their
@@ -120,7 +120,8 @@ def _compare(scene, model, rays, hot, min_agree=0.999, cap=np.inf):
     o, d, t = rays
     n = len(t)
     osc = oracle.OracleScene(scene.pack, scene.epsilon_t)
-    kind, obj, ray, coord, bvh_occ, _ = oracle.gather(osc, o, d, t, scene.nif_route_mask(None))
+    kind, obj, ray, coord, bvh_occ, _ = oracle.gather(osc, o, d, t,
+                                                      scene.nif_route_mask(hybrid_threshold))
     n_obj = scene.n_objects
     ref_occ = bvh_occ.copy()
     undecided = np.zeros(n, bool)
@@ -280,6 +281,30 @@ def test_c2_frame_per_object(c2):
     assert eng.bucket is not None
     hot = _hot_path(eng, n)
     _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
+
+
+def test_c2_frame_hybrid_routing(c2):
+    """Hybrid routing (renderer.py:439-445): with a threshold of 100
+    triangles the NIF plane (2 triangles) goes to the BVH -- any-hit inside
+    the gather -- and only the spheres to the networks; records, logits and
+    per-ray bits against the oracle with the same route mask."""
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import VisibilityEngine
+    scene, (o, d, t) = c2
+    n = int(t.numel())
+    route = scene.nif_route_mask(100)
+    assert 0 < int(route.sum()) < int(scene.nif_route_mask(None).sum())
+    model = build_model(NifConfig(seed=0), scene)
+    _randomize(model, seed=1)
+    eng = VisibilityEngine(scene, model, n, hybrid_threshold=100)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    hot = _hot_path(eng, n)
+    s = _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot,
+                 hybrid_threshold=100)
+    assert s["shadowed"] > 0.0
 
 
 def test_c2_frame_geometry_head(c2):
