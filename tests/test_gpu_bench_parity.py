@@ -307,6 +307,29 @@ def test_c2_frame_hybrid_routing(c2):
     assert s["shadowed"] > 0.0
 
 
+def test_c2_frame_uniform_sampler_rays(cuda):
+    """The C2 frame's shadow rays drawn by the uniform light sampler
+    (renderer.py:535-547: a different ray distribution from the bench's
+    importance sampler) through the hot path vs the oracle."""
+    from paper_2306_07191_b200 import build_model, synthetic
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import (VisibilityEngine, sample_pass_dev,
+                                                shadow_rays_dev)
+    scene = synthetic.c2(build_device=cuda)
+    data = sample_pass_dev(scene, scene.camera, 1, scene.seed, "uniform")
+    _, o, d, t = shadow_rays_dev(data, require_emit=False)
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0), scene)
+    _randomize(model, seed=2)
+    eng = VisibilityEngine(scene, model, n)
+    eng.origins[:n].copy_(o)
+    eng.dirs[:n].copy_(d)
+    eng.tmaxs[:n].copy_(t)
+    hot = _hot_path(eng, n)
+    s = _compare(scene, model, (o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy()), hot)
+    assert s["rays"] > 500_000  # (the cast filter keeps fewer uniform samples)
+
+
 def test_c2_frame_geometry_head(c2):
     """head="geometry" (4-wide identity output, nif.py:445-464) on the
     tensor cores for the C2 frame's queue: every raw output within 2e-2 of
