@@ -12,7 +12,7 @@ T_inner) -> fused grid encoding + visibility MLP (tcgen05) -> p < 0.5 ->
 per-ray OR. Rays are generated on the GPU by the sample pass (not timed).
 
 Multi-GPU (torchrun, one process per GPU): ONE frame
-cut into 8N row strips dealt round-robin to the ranks
+cut into 32N row strips dealt round-robin to the ranks
 (parallel.rank_strips; contiguous bands left the top ranks with the ray-less
 sky: tools/band_balance.py); rank r generates its strips' shadow rays and
 resolves them in one pass -- no collective on the data path (strong
@@ -64,7 +64,7 @@ WORKLOADS = {
 RESOLUTION = {"c1": (256, 256), "c2": (1920, 1080), "c3": (1920, 1080), "c4": (3840, 2160)}
 # kernels of one visibility pass (names as ncu reports them) and their
 # algorithmic work: see DESIGN.md section 4
-STRIPS_PER_RANK = 8  # row strips per rank when a frame is split across GPUs
+STRIPS_PER_RANK = 32  # row strips per rank when a frame is split across GPUs
 K_GATHER = "gather_warp_kernel"
 K_OUTER = "query_ts_kernel<3, 0, 64, 2, 2, 4, 0, 1, 0>"
 K_INNER = "query_ts_kernel<5, 3, 48, 3, 1, 4, 0, 1, 1>"
@@ -545,7 +545,7 @@ def main():
                                                          ", one GPU"),
                      "rays_per_frame": n4, "frame_ms": ms4, "value": n4 / (ms4 / 1e3),
                      "unit": UNIT, "note": "N=1 point of the C4 curve (bench.py under torchrun "
-                                           "splits this frame in 8N row strips)"}
+                                           "splits this frame in 32N row strips)"}
         del eng4, g4, o4, dd4, t4
 
     # --- online training: one spp of samples collected

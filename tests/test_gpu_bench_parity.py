@@ -433,7 +433,7 @@ def test_c3_strided_sample(cuda):
 
 def test_c4_rank_share(cuda):
     """C4 (the C2 scene at 3840x2160) as bench.py splits it under torchrun:
-    one rank's round-robin row strips of an 8-GPU run (64 strips), their
+    one rank's round-robin row strips of an 8-GPU run, their
     concatenated shadow rays in one pass, against the oracle."""
     import dataclasses
 
@@ -446,7 +446,7 @@ def test_c4_rank_share(cuda):
     scene = synthetic.c2(build_device=cuda)
     cam = dataclasses.replace(scene.camera, width=3840, height=2160)
     parts = []
-    for pix0, n_pix in rank_strips(cam.width, cam.height, 3, 8, 8):
+    for pix0, n_pix in rank_strips(cam.width, cam.height, 3, 8, 32):  # bench.STRIPS_PER_RANK
         data = sample_pass_dev(scene, cam, 0, scene.seed, "importance", pix0, n_pix)
         parts.append(shadow_rays_dev(data, require_emit=False)[1:])
     o, d, t = (torch.cat([p_[k] for p_ in parts]) for k in range(3))
