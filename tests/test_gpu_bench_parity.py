@@ -462,6 +462,37 @@ def test_c4_rank_share(cuda):
     assert s["rays"] > 500_000
 
 
+def test_c2_collect_samples_matches_oracle(c2, cuda):
+    """The training data at bench scale: collect_samples on the C2 frame
+    (1 spp, nif.py:569-674) -- records in the reference's order, fp64
+    coordinates and per-object BVH visibility labels -- against the oracle's
+    ordered gather and label_visible on the same hit-pixel shadow rays."""
+    from oracle import oracle
+    from paper_2306_07191_b200.pipeline import sample_pass_dev
+    from paper_2306_07191_b200.train import collect_samples
+    scene, _ = c2
+    smp = collect_samples(scene, spp=1, seed=scene.seed).host()
+    data = sample_pass_dev(scene, scene.camera, 0, scene.seed)
+    idx = (data["hit"] != 0).nonzero().squeeze(1)
+    o = data["point"][idx].cpu().numpy()
+    d = data["ldir"][idx].cpu().numpy()
+    t = data["tmax"][idx].cpu().numpy()
+    pix = idx.cpu().numpy().astype(np.int64)
+    osc = oracle.OracleScene(scene.pack, scene.epsilon_t)
+    kind, obj, ray, coord, _, _ = oracle.gather(osc, o, d, t, scene.nif_enabled.copy())
+    vis = np.asarray(oracle.label_visible(osc, obj, ray, o, d, t)).astype(np.float32)
+    assert len(kind) > 1_000_000
+    for fam, k, width in (("outer", 0, 4), ("inner", 1, 5)):
+        sel = kind == k
+        np.testing.assert_array_equal(smp[f"{fam}_obj"], obj[sel].astype(np.int64), err_msg=fam)
+        np.testing.assert_array_equal(smp[f"{fam}_ray"], pix[ray[sel].astype(np.int64)],
+                                      err_msg=fam)
+        np.testing.assert_array_equal(smp[f"{fam}_label"].reshape(-1), vis[sel], err_msg=fam)
+        np.testing.assert_allclose(smp[f"{fam}_coord"], coord[sel, :width], rtol=0, atol=1e-14,
+                                   err_msg=fam)
+    assert 0.0 < float(vis.mean()) < 1.0
+
+
 def test_queue_overflow_regrows(cuda):
     """Queues sized below the records a batch emits: the gather bounds its
     writes, the totals reveal the overflow, and checked_run re-runs with
