@@ -493,6 +493,56 @@ def test_c2_collect_samples_matches_oracle(c2, cuda):
     assert 0.0 < float(vis.mean()) < 1.0
 
 
+@pytest.mark.parametrize("which", ["outer", "inner"])
+def test_c2_training_step_gradients_match_oracle(c2, which):
+    """One optimiser step's gradients at bench scale: the default NifConfig
+    (R 256/128) on a reference-sized batch of the C2 frame's samples (2^11
+    outer / 2^12 inner, nif.py:682-749), fused forward/backward with the
+    grid scatter, against the oracle's numpy restatement (mlp.py:82-167,
+    grids.py:171-202) -- loss 1e-5 relative, gradients 1e-4."""
+    import torch
+    from oracle.oracle import OModel
+    from paper_2306_07191_b200 import _lib, build_model
+    from paper_2306_07191_b200.nif import NifConfig, init_arrays
+    from paper_2306_07191_b200.train import collect_samples
+    scene, _ = c2
+    cfg = NifConfig(seed=0)
+    smp = collect_samples(scene, spp=1, seed=scene.seed).host()
+    bs = cfg.outer.batch_size if which == "outer" else cfg.inner.batch_size
+    rng = np.random.default_rng(0)
+    pick = rng.choice(len(smp[f"{which}_obj"]), bs, replace=False)
+    obj = smp[f"{which}_obj"][pick]
+    coord = smp[f"{which}_coord"][pick]
+    label = smp[f"{which}_label"][pick].reshape(bs, -1)
+    outer, inner, grids, _, _ = init_arrays(cfg, scene.n_objects)
+    om = OModel(outer[0], inner[0], grids)
+    ref_loss = om.train_batch(which, obj, coord, label, apply=False)
+    m = build_model(cfg, scene)
+    fam = m.family(which)
+    dev = m.device
+    t_obj = torch.from_numpy(obj.astype(np.int64)).to(dev)
+    t_coord = torch.from_numpy(np.ascontiguousarray(coord)).to(dev)
+    t_lab = torch.from_numpy(np.ascontiguousarray(label.astype(np.float32))).to(dev)
+    sq = torch.zeros(1, dtype=torch.float64, device=dev)
+    L, p, sp = _lib.lib(), _lib.ptr, _lib.stream_ptr()
+    fam.grad.zero_()
+    L.nif_batch_counts_dev(p(t_obj), None, bs, fam.n_obj, p(fam.counts), sp)
+    L.nif_train_fwdbwd_dev(fam.view(), fam.train_view(), p(t_obj), p(t_coord), p(t_lab), None,
+                           bs, 0, 1, p(sq), sp)
+    assert float(sq.item()) / bs == pytest.approx(ref_loss, rel=1e-5)
+    mlp = om.outer if which == "outer" else om.inner
+    refs = {"w": np.concatenate([l_.gw.reshape(-1) for l_ in mlp.layers]),
+            "b": np.concatenate([l_.gb for l_ in mlp.layers])}
+    names = {"pos": f"{which}_pos", "dir": f"{which}_dir", "dist": "inner_dist"}
+    for key in ("pos", "dir") + (("dist",) if which == "inner" else ()):
+        refs[key] = np.stack([gg[names[key]].grad for gg in om.grids]).reshape(-1)
+    for key, ref in refs.items():
+        got = fam.part(key, fam.grad).detach().cpu().numpy().reshape(-1)
+        scale = np.abs(ref).max()
+        assert scale > 0, key
+        np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-5 * scale, err_msg=key)
+
+
 def test_queue_overflow_regrows(cuda):
     """Queues sized below the records a batch emits: the gather bounds its
     writes, the totals reveal the overflow, and checked_run re-runs with
