@@ -543,6 +543,49 @@ def test_c2_training_step_gradients_match_oracle(c2, which):
         np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-5 * scale, err_msg=key)
 
 
+def test_c2_training_steps_parameters_match_oracle(c2):
+    """Three optimiser steps per family at bench scale through the public
+    train_batch (fused forward/backward + grid scatter + dense Adam over the
+    touched objects, nif.py:682-749) against the oracle's train_batch: every
+    parameter array of the model within 1e-6 for >= 99.5 % of its entries
+    (Adam divides by sqrt(v); near-zero v amplifies fp32 summation-order
+    differences of the gradients)."""
+    from oracle.oracle import OModel
+    from paper_2306_07191_b200 import build_model
+    from paper_2306_07191_b200.nif import NifConfig, init_arrays
+    from paper_2306_07191_b200.train import collect_samples, train_batch
+    scene, _ = c2
+    cfg = NifConfig(seed=0)
+    smp = collect_samples(scene, spp=1, seed=scene.seed).host()
+    outer, inner, grids, _, _ = init_arrays(cfg, scene.n_objects)
+    om = OModel(outer[0], inner[0], grids)
+    m = build_model(cfg, scene)
+    rng = np.random.default_rng(1)
+    for step in range(3):
+        for which in ("outer", "inner"):
+            bs = cfg.outer.batch_size if which == "outer" else cfg.inner.batch_size
+            pick = rng.choice(len(smp[f"{which}_obj"]), bs, replace=False)
+            obj, coord = smp[f"{which}_obj"][pick], smp[f"{which}_coord"][pick]
+            label = smp[f"{which}_label"][pick].reshape(bs, -1)
+            ref_loss = om.train_batch(which, obj, coord, label)
+            loss = train_batch(m, which, obj, coord, label)
+            assert loss == pytest.approx(ref_loss, rel=1e-4), (step, which)
+    ref = []
+    for mlp in (om.outer, om.inner):
+        for l_ in mlp.layers:
+            ref += [l_.w, l_.b]
+    for g in om.grids:
+        ref += [g[k].latents for k in ("outer_pos", "outer_dir", "inner_pos", "inner_dir",
+                                       "inner_dist")]
+    got = m.model_arrays()
+    assert len(got) == len(ref)
+    for i, (a, b) in enumerate(zip(got, ref)):
+        a = np.asarray(a, np.float64).reshape(-1)
+        b = np.asarray(b, np.float64).reshape(-1)
+        frac = float(np.mean(np.abs(a - b) <= 1e-6))
+        assert frac >= 0.995, (i, frac, float(np.abs(a - b).max()))
+
+
 def test_queue_overflow_regrows(cuda):
     """Queues sized below the records a batch emits: the gather bounds its
     writes, the totals reveal the overflow, and checked_run re-runs with
