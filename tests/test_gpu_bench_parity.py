@@ -586,6 +586,45 @@ def test_c2_training_steps_parameters_match_oracle(c2):
         assert frac >= 0.995, (i, frac, float(np.abs(a - b).max()))
 
 
+def test_c2_checkpoint_round_trip_answers(c2, tmp_path):
+    """NIF1 checkpoints at bench scale (scene_io.py:308-387): a trained
+    default-config model (13 objects, R 256/128) saved with its Adam state
+    and loaded into a fresh process-local model gives bit-identical
+    parameters and the identical per-ray answers on the C2 frame; training
+    resumes from the restored Adam state exactly as the original does."""
+    import importlib
+
+    import torch
+    from paper_2306_07191_b200 import build_model, load_checkpoint, save_checkpoint
+    from paper_2306_07191_b200.nif import NifConfig
+    from paper_2306_07191_b200.pipeline import VisibilityEngine
+    tr = importlib.import_module("paper_2306_07191_b200.train")
+    scene, (o, d, t) = c2
+    n = int(t.numel())
+    model = build_model(NifConfig(seed=0), scene)
+    smp = tr.collect_samples(scene, spp=1, seed=scene.seed)
+    tr.train(model, smp, epochs=1)
+    path = tmp_path / "c2.nif1"
+    save_checkpoint(model, path, adam=True)
+    back = load_checkpoint(path, device=model.device)
+    for a, b in zip(model.model_arrays(), back.model_arrays()):
+        assert np.array_equal(a, b)
+    occ = []
+    for m in (model, back):
+        eng = VisibilityEngine(scene, m, n)
+        eng.origins[:n].copy_(o)
+        eng.dirs[:n].copy_(d)
+        eng.tmaxs[:n].copy_(t)
+        eng.checked_run(n)
+        occ.append(eng.occ[:n].clone())
+    assert torch.equal(occ[0], occ[1])
+    # one more deterministic epoch from each: identical parameters
+    for m in (model, back):
+        tr.train(m, smp, epochs=1, deterministic=True)
+    for a, b in zip(model.model_arrays(), back.model_arrays()):
+        assert np.array_equal(a, b)
+
+
 def test_queue_overflow_regrows(cuda):
     """Queues sized below the records a batch emits: the gather bounds its
     writes, the totals reveal the overflow, and checked_run re-runs with
