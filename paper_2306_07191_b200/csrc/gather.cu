@@ -29,6 +29,12 @@ namespace nif {
 namespace {
 
 constexpr int kThreads = 256;    // rays per tile (one per thread)
+#ifndef NIF_BUNDLE_SIGN
+#define NIF_BUNDLE_SIGN 1  // warp-bundle cull: two sign-selected products per axis instead of eight
+#endif
+#ifndef NIF_SLAB_NF
+#define NIF_SLAB_NF 1  // hot path: sign-selected slab planes (slab_nf) for rays with |d_a| > 1e-20
+#endif
 #ifndef NIF_GATHER_MINB
 #define NIF_GATHER_MINB 3        // resident CTAs per SM the register budget targets
 #endif
@@ -78,6 +84,49 @@ __device__ __forceinline__ Hit3 slab(const RayX& r, const ObjC& b) {
   }
   if (t1 < t0 || t1 < 0.0) return {false, t0, t1};
   return {true, t0, t1};
+}
+
+// slab() for rays with every |d_a| > 1e-20 (finite, nonzero reciprocals):
+// the entry plane of each axis is known from the reciprocal's sign, so the
+// per-axis swap (a DSETP and four 32-bit selects per axis) becomes a
+// shared-memory load at a per-ray offset. Exact: with finite operands
+// (lo - o) * inv <= (hi - o) * inv for inv > 0 and >= for inv < 0 (rounding
+// is monotone), so the reference's swap picks the same pair; where the two
+// are equal they are the same bits (a zero here is lo == hi == o, and
+// (+0) * inv has one sign). lh points at ObjC::lo (hi follows it);
+// s3 = 3 * [inv_a < 0] packed per axis (bits 0-1 x, 2-3 y, 4-5 z).
+__device__ __forceinline__ Hit3 slab_nf(const RayX& r, const ObjC& b, int s3) {
+  const double* lh = b.lo;
+  const int sx = s3 & 3, sy = (s3 >> 2) & 3, sz = s3 >> 4;
+  double t0 = -CUDART_INF, t1 = CUDART_INF;
+  {
+    const double ta = (lh[sx] - r.ox) * r.ix, tb = (lh[3 - sx] - r.ox) * r.ix;
+    if (ta > t0) t0 = ta;
+    if (tb < t1) t1 = tb;
+  }
+  {
+    const double ta = (lh[1 + sy] - r.oy) * r.iy, tb = (lh[4 - sy] - r.oy) * r.iy;
+    if (ta > t0) t0 = ta;
+    if (tb < t1) t1 = tb;
+  }
+  {
+    const double ta = (lh[2 + sz] - r.oz) * r.iz, tb = (lh[5 - sz] - r.oz) * r.iz;
+    if (ta > t0) t0 = ta;
+    if (tb < t1) t1 = tb;
+  }
+  if (t1 < t0 || t1 < 0.0) return {false, t0, t1};
+  return {true, t0, t1};
+}
+
+__device__ __forceinline__ int classify_nf(const RayX& r, const ObjC& b, bool test_box,
+                                           double tol, int s3) {
+  const Hit3 h = slab_nf(r, b, s3);
+  if (test_box && !(h.hit && h.t0 <= r.tmax && h.t1 >= -tol)) return 0;
+  if (b.lt[0] <= r.ox && r.ox <= b.ht[0] && b.lt[1] <= r.oy && r.oy <= b.ht[1] &&
+      b.lt[2] <= r.oz && r.oz <= b.ht[2])
+    return 2;
+  if (h.hit && h.t0 > 0.0 && h.t0 < r.tmax) return 1;
+  return 0;
 }
 
 // 0 none, 1 outer, 2 inner (see trace.cu classify())
@@ -221,6 +270,24 @@ __device__ __forceinline__ float wmax(float v) {
 __device__ __forceinline__ void interval_slab(float lo, float hi, float ol, float oh, float il,
                                               float ih, float& E, float& X) {
   if (!(il > 0.f || ih < 0.f)) return;  // mixed signs: no bound from this axis
+#if NIF_BUNDLE_SIGN
+  // The sign of the reciprocals (warp-uniform) says which plane is the
+  // entry and which corner of [o] x [inv] bounds each product, so only the
+  // two extremal products are formed. They are the same fp32 products the
+  // four-corner form below takes the min / max of (rounding is monotone),
+  // and its min(ta, tb) / max(ta, tb) pick the entry / exit side because
+  // hi - o >= lo - o: E and X are bit-identical.
+  if (il > 0.f) {  // entry lo, exit hi
+    const float v0 = lo - oh, u1 = hi - ol;
+    E = fmaxf(E, v0 * (v0 >= 0.f ? il : ih));
+    X = fminf(X, u1 * (u1 >= 0.f ? ih : il));
+  } else {         // entry hi, exit lo
+    const float u1 = hi - ol, v0 = lo - oh;
+    E = fmaxf(E, u1 * (u1 >= 0.f ? il : ih));
+    X = fminf(X, v0 * (v0 <= 0.f ? il : ih));
+  }
+  return;
+#endif
   const float a0 = lo - oh, a1 = lo - ol, b0 = hi - oh, b1 = hi - ol;
   const float p0 = a0 * il, p1 = a0 * ih, p2 = a1 * il, p3 = a1 * ih;
   const float q0 = b0 * il, q1 = b0 * ih, q2 = b1 * il, q3 = b1 * ih;
@@ -1032,6 +1099,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
     RayX r;  // written for valid lanes; invalid lanes never read their ray
     RayF q;
     bool use_pf = false;
+    int s3 = -1;  // entry-plane offsets for slab_nf, -1: the general slab
     if (valid) {
       r.ox = __ldg(org + i * 3 + 0);
       r.oy = __ldg(org + i * 3 + 1);
@@ -1059,6 +1127,8 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         q.dt = 1e-5f * S * imax;
         q.tmax_ru = __double2float_ru(r.tmax);
         use_pf = isfinite(q.dt);
+        // finite origin and reciprocals (dt is finite): no NaN in slab_nf
+        if (use_pf) s3 = (r.ix < 0.0 ? 3 : 0) | (r.iy < 0.0 ? 12 : 0) | (r.iz < 0.0 ? 48 : 0);
       }
     }
     uint64_t mask = 0;
@@ -1089,8 +1159,13 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       while (pmask) {
         const int k = __ffs(pmask) - 1;
         pmask &= pmask - 1;
-        double t0;
-        const int kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
+        int kind;
+        if (NIF_SLAB_NF && s3 >= 0) {
+          kind = classify_nf(r, objs[k], test_box, s.tol, s3);
+        } else {
+          double t0;
+          kind = classify_obj(r, objs[k], test_box, s.tol, &t0);
+        }
         if (kind == 0) continue;
 #ifdef NIF_GATHER_STATS
         atomicAdd(&g_gstats[3], 1ull);
@@ -1148,7 +1223,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       float rnf, rinvf;
       bool deg;
       if (kind == 1) {
-        const Hit3 hh = slab(r, b);
+        const Hit3 hh = (NIF_SLAB_NF && s3 >= 0) ? slab_nf(r, b, s3) : slab(r, b);
         const double ex = r.ox + hh.t0 * r.dx, ey = r.oy + hh.t0 * r.dy, ez = r.oz + hh.t0 * r.dz;
         const double rx = ex - b.c[0], ry = ey - b.c[1], rz = ez - b.c[2];
         deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
