@@ -3,6 +3,7 @@ gather alone and the whole visibility pass, CUDA events, L2 flushed.
 
     python tools/ab_gather.py [variants, default 3,0]
 """
+import os
 import sys
 from pathlib import Path
 
@@ -52,6 +53,9 @@ for rep in range(2):
     for v in variants:
         _lib.lib().nif_debug_set_gather_variant(v)
         g = timeit(lambda: gather_dev(ds, ds.route(route), o, d, t, n, buf))
+        if os.environ.get("GATHER_ONLY"):  # queue formats under test the queries cannot read
+            print(f"variant {v}: gather {g:.1f} us", flush=True)
+            continue
         f = timeit(lambda: eng.run(n))
         occ = eng.occ[:n].clone()
         print(f"variant {v}: gather {g:.1f} us  pass {f:.1f} us  occluded {int(occ.sum())}",
