@@ -32,6 +32,9 @@ constexpr int kThreads = 256;    // rays per tile (one per thread)
 #ifndef NIF_BUNDLE_SIGN
 #define NIF_BUNDLE_SIGN 1  // warp-bundle cull: two sign-selected products per axis instead of eight
 #endif
+#ifndef NIF_NF_LEAN
+#define NIF_NF_LEAN 1  // slab_nf / classify_nf without the first-axis compares and short circuits (A/B)
+#endif
 #ifndef NIF_SLAB_NF
 #define NIF_SLAB_NF 1  // hot path: sign-selected slab planes (slab_nf) for rays with |d_a| > 1e-20
 #endif
@@ -98,12 +101,18 @@ __device__ __forceinline__ Hit3 slab(const RayX& r, const ObjC& b) {
 __device__ __forceinline__ Hit3 slab_nf(const RayX& r, const ObjC& b, int s3) {
   const double* lh = b.lo;
   const int sx = s3 & 3, sy = (s3 >> 2) & 3, sz = s3 >> 4;
+#if NIF_NF_LEAN
+  // first axis: the reference's max(-inf, ta) / min(+inf, tb) are ta / tb
+  // (no NaN here: finite origin and reciprocal)
+  double t0 = (lh[sx] - r.ox) * r.ix, t1 = (lh[3 - sx] - r.ox) * r.ix;
+#else
   double t0 = -CUDART_INF, t1 = CUDART_INF;
   {
     const double ta = (lh[sx] - r.ox) * r.ix, tb = (lh[3 - sx] - r.ox) * r.ix;
     if (ta > t0) t0 = ta;
     if (tb < t1) t1 = tb;
   }
+#endif
   {
     const double ta = (lh[1 + sy] - r.oy) * r.iy, tb = (lh[4 - sy] - r.oy) * r.iy;
     if (ta > t0) t0 = ta;
@@ -114,19 +123,26 @@ __device__ __forceinline__ Hit3 slab_nf(const RayX& r, const ObjC& b, int s3) {
     if (ta > t0) t0 = ta;
     if (tb < t1) t1 = tb;
   }
-  if (t1 < t0 || t1 < 0.0) return {false, t0, t1};
-  return {true, t0, t1};
+  return {!((t1 < t0) | (t1 < 0.0)), t0, t1};
 }
 
 __device__ __forceinline__ int classify_nf(const RayX& r, const ObjC& b, bool test_box,
                                            double tol, int s3) {
   const Hit3 h = slab_nf(r, b, s3);
+#if NIF_NF_LEAN
+  // the same predicates without short-circuit branches (no side effects)
+  if (test_box & !(h.hit & (h.t0 <= r.tmax) & (h.t1 >= -tol))) return 0;
+  const bool inside = (b.lt[0] <= r.ox) & (r.ox <= b.ht[0]) & (b.lt[1] <= r.oy) &
+                      (r.oy <= b.ht[1]) & (b.lt[2] <= r.oz) & (r.oz <= b.ht[2]);
+  return inside ? 2 : ((h.hit & (h.t0 > 0.0) & (h.t0 < r.tmax)) ? 1 : 0);
+#else
   if (test_box && !(h.hit && h.t0 <= r.tmax && h.t1 >= -tol)) return 0;
   if (b.lt[0] <= r.ox && r.ox <= b.ht[0] && b.lt[1] <= r.oy && r.oy <= b.ht[1] &&
       b.lt[2] <= r.oz && r.oz <= b.ht[2])
     return 2;
   if (h.hit && h.t0 > 0.0 && h.t0 < r.tmax) return 1;
   return 0;
+#endif
 }
 
 // 0 none, 1 outer, 2 inner (see trace.cu classify())
