@@ -35,6 +35,9 @@ constexpr int kThreads = 256;    // rays per tile (one per thread)
 #ifndef NIF_NF_LEAN
 #define NIF_NF_LEAN 1  // slab_nf / classify_nf without the first-axis compares and short circuits (A/B)
 #endif
+#ifndef NIF_EMIT_UNIFIED
+#define NIF_EMIT_UNIFIED 1  // hot-path record emission: one path for outer and inner records (A/B)
+#endif
 #ifndef NIF_SLAB_NF
 #define NIF_SLAB_NF 1  // hot path: sign-selected slab planes (slab_nf) for rays with |d_a| > 1e-20
 #endif
@@ -1235,6 +1238,37 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
       const int kind = (int)((m >> (2 * k)) & 3);
       m &= ~(3ull << (2 * k));
       const ObjC& b = objs[k];
+#if NIF_EMIT_UNIFIED
+      // one path for both kinds (a warp mixing outer and inner records no
+      // longer runs the map twice): the record point is the entry point
+      // o + t0 d (outer, same fp64 expression) or the origin (inner)
+      const bool outer = kind == 1;
+      double px = r.ox, py = r.oy, pz = r.oz;
+      if (outer) {
+        const Hit3 hh = (NIF_SLAB_NF && s3 >= 0) ? slab_nf(r, b, s3) : slab(r, b);
+        px = r.ox + hh.t0 * r.dx;
+        py = r.oy + hh.t0 * r.dy;
+        pz = r.oz + hh.t0 * r.dz;
+      }
+      const double rx = px - b.c[0], ry = py - b.c[1], rz = pz - b.c[2];
+      float rnf, rinvf, c0 = 0.5f, c1 = 0.5f, rr = 0.f;
+      const bool deg = degenerate_f32(rx, ry, rz, &rnf, &rinvf);
+      if (!deg) {
+        sph32f((float)rx, (float)ry, (float)rz, rinvf, &c0, &c1);
+        rr = fminf(rnf * b.hinv, 1.0f);  // within 1 ulp of rnf / hn (fp32); inner only
+      }
+      const int64_t j = outer ? jo : ji;
+      if (j < (outer ? out.cap_outer : out.cap_inner)) {
+        (outer ? out.outer_obj : out.inner_obj)[j] = b.id;
+        (outer ? out.outer_ray : out.inner_ray)[j] = (int32_t)i;
+        reinterpret_cast<float4*>(outer ? out.outer_coord : out.inner_coord)[j] =
+            make_float4(c0, c1, du, dv);
+        if (!outer) out.inner_r[j] = rr;
+      }
+      jo += outer ? 1 : 0;
+      ji += outer ? 0 : 1;
+      deg_count += deg ? 1 : 0;
+#else
       float c0, c1, rr = 0.f;
       float rnf, rinvf;
       bool deg;
@@ -1268,6 +1302,7 @@ gather_warp_kernel(nif_scene_view s, const uint8_t* __restrict__ route,
         ++ji;
       }
       deg_count += deg ? 1 : 0;
+#endif
     }
   }
   const int dsum = __reduce_add_sync(0xffffffffu, deg_count);
